@@ -1,0 +1,254 @@
+/*
+ * propring — proportional task allocation + sample-count-weighted ring allreduce for B200 (sm_100a).
+ *
+ * C ABI of libpropring.so: the data-parallel hot path of arXiv 2111.08272, "Task allocation for
+ * decentralized training in heterogeneous environment" (Chao, Liao, Gao).
+ * Citation keys: P:n = PAPER.md line n (paper source), S:n = SPEC.md line n, DESIGN §3 #k = the k-th
+ * reading of a silent/ambiguous passage listed in DESIGN.md §3.
+ *
+ * Conventions (every call):
+ *   - returns int: PR_OK (0) on success, a negative PR_ERR_* code otherwise; nothing aborts on user
+ *     error and no C++ exception crosses the ABI;
+ *   - output parameters are written only on success;
+ *   - "d_" pointers are CUDA device pointers (or host pointers mapped into the device address space),
+ *     "h_"/plain pointers are host memory; all memory passed in stays caller-owned unless stated;
+ *   - `stream` is a cudaStream_t (passed as void* so this header needs no CUDA include); device work
+ *     is enqueued asynchronously and stream-ordered;
+ *   - pr_alloc handles are pure host state, not thread-safe per handle; pr_comm calls are serialised
+ *     per communicator and are collective (same order on every rank), like NCCL.
+ */
+#ifndef PROPRING_H
+#define PROPRING_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PR_VERSION 10000       /* 1.0.0 */
+#define PR_MAX_RANKS 64
+
+/* ---- error codes (SPEC error names in parentheses) ------------------------------------------- */
+#define PR_OK                      0
+#define PR_ERR_INVALID            -1   /* bad argument, null handle, bad version/size               */
+#define PR_ERR_INFEASIBLE_FLOOR   -2   /* C < P·floor (InfeasibleFloor)                       */
+#define PR_ERR_DATASET_TOO_SMALL  -3   /* N < B = g·C (DatasetTooSmall)                       */
+#define PR_ERR_ZERO_TIMING        -4   /* a step time <= 0, NaN or Inf (ZeroTiming)            */
+#define PR_ERR_CUDA               -5   /* a CUDA runtime call failed                                  */
+#define PR_ERR_ALIGN              -6   /* pointer or row size not 16-byte aligned                    */
+#define PR_ERR_NO_P2P             -7   /* peer access between two ranks' GPUs is not possible        */
+#define PR_ERR_LENGTH_MISMATCH    -8   /* ranks called the allreduce with different count/dtype (LengthMismatch) */
+#define PR_ERR_ZERO_SAMPLES       -9   /* Σ n_local = 0 (ZeroSampleCount)                     */
+#define PR_ERR_PEER_TIMEOUT      -10   /* watchdog expired waiting for a peer (TransportClosed) */
+#define PR_ERR_CAPACITY          -11   /* output capacity too small                                  */
+#define PR_ERR_INTERNAL          -12   /* invariant violated inside the library (a bug)              */
+
+const char *pr_strerror(int code);
+int pr_version(void);
+
+/* =================================================================================================
+ * 1. Allocation (host control plane) — §8(a) rows a1 and a10
+ * ================================================================================================= */
+
+typedef struct pr_alloc pr_alloc;
+
+/* Read-only snapshot of an allocation.  Arrays are indexed by rank (first P entries valid). */
+typedef struct {
+    int64_t N;        /* dataset rows D                                                      */
+    int32_t P;        /* workers                                                                      */
+    int32_t frozen;   /* 1 once the stop rule fired                                           */
+    int64_t C;        /* Σ w_i, units per aggregation, constant (Eq. 4)                    */
+    int64_t g;        /* samples per unit: the paper's "minibatch" (DESIGN §3 #1)        */
+    int64_t floor;    /* minimum units per worker                                             */
+    int64_t B;        /* global samples per aggregation = g·C ("minibatch*(Σw_i)")        */
+    int64_t S;        /* aggregations per epoch = floor(N / B) (DESIGN §3 #10)                        */
+    int64_t epoch;    /* number of successful pr_alloc_update calls                                   */
+    int64_t hist_len; /* number of allocation vectors in the history (initial one included)           */
+    int64_t w[PR_MAX_RANKS];   /* units per aggregation w_i^(k)                        */
+    int64_t n[PR_MAX_RANKS];   /* samples per aggregation n_i = g·w_i                                 */
+    int64_t len[PR_MAX_RANKS]; /* shard sizes D_i = D·w_i/Σw, exact-integer Hamilton (DESIGN §3 #9) */
+    int64_t off[PR_MAX_RANKS]; /* shard offsets: exclusive prefix sum of len in rank order             */
+} pr_alloc_view;
+
+/* Stop-rule / smoothing policy of the self-adaptive controller. */
+typedef struct {
+    int32_t window;        /* stable when the last `window` vectors differ by <= tol (default 2)     */
+    int32_t never_freeze;  /* 1: keep re-allocating every epoch (default 0)                          */
+    int64_t tol;           /* per-component tolerance in units (default 1)                           */
+    double  ema_alpha;     /* t_eff = a·t + (1−a)·t_eff_prev; 1.0 = raw last-epoch times (default)   */
+} pr_alloc_policy;
+
+/* Static allocation (§3.1; a1).  w = Hamilton(C·r_i/Σr, floor) with ties to the lowest rank
+ * (identity when the ratios are integers summing to C); n_i = g·w_i; len = Hamilton(N·w_i/C) in exact
+ * integer arithmetic; off = prefix sum; S = floor(N/(g·C)).
+ *   ratios: host double[P], each finite and > 0.  C = 0 means C = Σratios (ratios must be integers).
+ *   Errors: PR_ERR_INVALID (P<1 or P>PR_MAX_RANKS, N<1, g<1, floor<0, bad ratio, C<0),
+ *           PR_ERR_INFEASIBLE_FLOOR, PR_ERR_DATASET_TOO_SMALL.
+ *   Deterministic and replicated: every rank calls it with identical arguments and gets identical state.
+ *   Ownership: *out is library-owned; free with pr_alloc_destroy. */
+int pr_alloc_init(pr_alloc **out, int64_t N, int32_t P, const double *ratios, int64_t C, int64_t g,
+                  int64_t floor);
+int pr_alloc_set_policy(pr_alloc *a, const pr_alloc_policy *policy);
+
+/* Self-adaptive update (Algorithm 1 steps 1-3; Eq. 10; rounding P:181; a10).
+ *   step_times: host double[P], rank i's gradient-computing time t_s^i of the last epoch in seconds
+ *   (per-epoch sum of CUDA-event step times; DESIGN §3 #4-#5).  Any t <= 0 / NaN / Inf ->
+ *   PR_ERR_ZERO_TIMING with the state unchanged (the first epoch's "t_s is set to 0").
+ *   v_i = w_i / t_i;  S_v = Σ v left to right;  q_i = (C·v_i)/S_v;  w' = Hamilton(q, C, floor);
+ *   history += w'; epoch += 1; then the stop rule may freeze the allocation.
+ *   If already frozen: no-op, *changed = 0, PR_OK.  changed (may be NULL): 1 if w' != w. */
+int pr_alloc_update(pr_alloc *a, const double *step_times, int32_t *changed);
+int pr_alloc_query(const pr_alloc *a, pr_alloc_view *out);
+/* k-th allocation vector of the history (0 = initial); w_out: host int64[P]. */
+int pr_alloc_history(const pr_alloc *a, int64_t k, int64_t *w_out);
+/* Checkpoint (POD bytes: w, history, frozen flag, policy, EMA state).  *size receives the byte count;
+ * with buf == NULL only the size is returned.  PR_ERR_CAPACITY if cap is too small. */
+int pr_alloc_save(const pr_alloc *a, void *buf, size_t cap, size_t *size);
+int pr_alloc_load(pr_alloc **out, const void *buf, size_t size);
+void pr_alloc_destroy(pr_alloc *a);
+
+/* =================================================================================================
+ * 2. Sharder (K1) and gather (K2) — §8(a) rows a2 and a3
+ * ================================================================================================= */
+
+/* Per-epoch permutation + proportional split ("assigned a corresponding proportion", Algorithm 1
+ * step 3 "Redistribute the subdataset"; shuffle is build-defined, DESIGN §3 #8):
+ *   d_out[t] = π_{seed,epoch}(off_rank + t), t < len_rank, where π is a 4-round Feistel network with
+ *   Philox4x32-10 round functions on a 2^b domain, cycle-walked into [0, N).
+ *   d_out: caller-owned device int64[cap], cap >= len_rank.  Async on stream.
+ *   Errors: PR_ERR_INVALID (rank out of range), PR_ERR_CAPACITY, PR_ERR_CUDA. */
+int pr_shard_indices(const pr_alloc *a, int32_t rank, int64_t epoch, uint64_t seed, int64_t *d_out,
+                     int64_t cap, void *stream);
+/* The permutation itself on positions [begin, begin+count): d_out[t] = π_{seed,epoch}(begin + t).
+ * Requires 1 <= N <= 2^62 and begin + count <= N. */
+int pr_permute(int64_t N, uint64_t seed, int64_t epoch, int64_t begin, int64_t count, int64_t *d_out,
+               void *stream);
+
+#define PR_GATHER_COPY              0  /* bit copy of each row                                       */
+#define PR_GATHER_U8_TO_F32_AFFINE  1  /* (float(x) − shift_c)·scale_c, two fp32 roundings, no FMA   */
+#define PR_GATHER_U8_TO_BF16_AFFINE 2  /* the same value rounded to bfloat16 (RNE)                   */
+#define PR_GATHER_MAX_CHANNELS 16
+
+typedef struct {
+    int32_t op;                              /* PR_GATHER_*                                           */
+    int32_t channels;                        /* affine ops: number of channels (<= 16)               */
+    int64_t plane;                           /* affine ops: elements per channel (H·W of a CHW row)   */
+    float scale[PR_GATHER_MAX_CHANNELS];     /* per-channel multiplier                                */
+    float shift[PR_GATHER_MAX_CHANNELS];     /* per-channel subtrahend                                */
+} pr_gather_op;
+
+/* Step-batch gather (Algorithm 1 step 4, "Proportionally draw samples from the sub-data set"):
+ *   for t < n:  dst[t, :] = op(src[idx[t], :]);  if d_lab_src: d_lab_dst[t] = d_lab_src[idx[t]].
+ *   d_src: [n_src, row_bytes] bytes (device memory, or mapped pinned host memory for the e2e path);
+ *   d_idx: int64[n] in [0, n_src) (out-of-range is a contract violation);
+ *   d_dst: COPY -> [n, row_bytes] bytes; U8_TO_F32 -> [n, row_bytes] float; U8_TO_BF16 -> bf16.
+ *   op == NULL means COPY.  row_bytes, d_src and d_dst must be 16-byte aligned (PR_ERR_ALIGN);
+ *   for affine ops channels·plane must equal row_bytes (PR_ERR_INVALID).  n = 0 is a no-op. */
+int pr_gather_rows(const void *d_src, int64_t n_src, int64_t row_bytes, const int64_t *d_idx, int64_t n,
+                   void *d_dst, const pr_gather_op *op, const int64_t *d_lab_src, int64_t *d_lab_dst,
+                   void *stream);
+
+/* Emulated heterogeneity (K4): a 32-thread kernel that busy-waits on %globaltimer for `ns`
+ * nanoseconds on `stream` (the per-rank calibrated slowdown of the north star). ns <= 0: no launch. */
+int pr_spin(int64_t ns, void *stream);
+
+/* =================================================================================================
+ * 3. Weighted ring allreduce (K3) — §8(a) rows a6, a7, a8
+ * ================================================================================================= */
+
+typedef struct pr_comm pr_comm;
+
+#define PR_DTYPE_F32  0
+#define PR_DTYPE_BF16 1
+
+#define PR_COMM_FLAG_FORCE_STAGED 1   /* all-gather through staging even when buffers are registered */
+
+typedef struct {
+    int32_t channels;     /* ring channels = CTAs per rank (default 16)                               */
+    int32_t slots;        /* staging slots per channel (pipeline depth, default 4)                    */
+    int32_t threads;      /* threads per CTA, <= 512 (default 512)                                         */
+    int32_t flags;        /* PR_COMM_FLAG_* (default 0)                                                */
+    int64_t slot_bytes;   /* bytes per staging slot, multiple of 16 (default 131072)                  */
+    int64_t watchdog_ns;  /* spin-wait deadline per call (default 10 s); <= 0 disables               */
+} pr_comm_config;
+
+/* Byte allgather supplied by the caller (e.g. over a torch process group): every rank passes `len`
+ * bytes in `send` and receives the P·len bytes of all ranks, rank-ordered, in `recv`.  Returns 0 on
+ * success. */
+typedef int (*pr_exchange_fn)(void *ctx, const void *send, size_t len, void *recv);
+
+/* One process per GPU (collective over P processes).  Allocates this rank's flag page + staging
+ * (cudaMalloc), exports it with CUDA IPC, exchanges the handles through `fn`, and maps every peer's
+ * memory (NVLink 5 / NVSwitch P2P).  cfg may be NULL (defaults).  device = CUDA ordinal of this rank.
+ * Errors: PR_ERR_INVALID, PR_ERR_NO_P2P, PR_ERR_CUDA. */
+int pr_comm_init(pr_comm **out, int32_t rank, int32_t P, int32_t device, pr_exchange_fn fn, void *ctx,
+                 const pr_comm_config *cfg);
+/* Single-process group of P ranks on ONE device (test and emulation mode: the P ranks' memories are
+ * all local, the ring protocol and kernel are the same).  out: host pr_comm*[P]. */
+int pr_comm_init_local(pr_comm **out, int32_t P, int32_t device, const pr_comm_config *cfg);
+
+/* Collective: register [d_buf, d_buf+bytes) so that the all-gather phase stores the reduced chunks
+ * straight into every peer's buffer (no staging copy).  d_buf must be the base of a cudaMalloc
+ * allocation (CUDA IPC requirement) — pr_comm_alloc returns such memory.  Buffers passed to
+ * pr_weighted_allreduce inside a registered region take the direct path when every rank's buffer is
+ * registered, else the staged path.  Registered memory stays caller-owned. */
+int pr_comm_register(pr_comm *c, void *d_buf, size_t bytes);
+/* Collective: allocate `bytes` of device memory (zeroed) on this rank's device and register it.
+ * Library-owned; released by pr_comm_destroy. */
+int pr_comm_alloc(pr_comm *c, size_t bytes, void **d_ptr);
+
+/* Sample-count-weighted ring allreduce, in place (Eq. 1; ring of P:63 / S:195):
+ *     buf <- Σ_r (n_r / Σn) · buf_r
+ * where buf_r is rank r's LOCAL MEAN gradient over its n_r = n_local samples (DESIGN §3 #11).
+ * One kernel: handshake (seq, count, dtype, n_r) with every peer = the barrier of P:54/P:63 (its
+ * duration is t_w), Σn and s_r = fp32(n_r/Σn) (fp64 division); P−1 reduce-scatter hops where each
+ * rank's contribution is scaled as it enters the ring (hop 0: y = s_r·g_r; later hops y = fma(s_r, g_r,
+ * recv), fp32 math, round-to-nearest-even to the dtype); P−1 all-gather hops (bit copies).
+ *   count: elements; dt: PR_DTYPE_F32 / PR_DTYPE_BF16; d_buf 16-byte aligned (PR_ERR_ALIGN);
+ *   n_local >= 0: a rank with n_local = 0 contributes exactly nothing (never multiplied).
+ *   P = 1: identity (no launch) unless n_local = 0 (PR_ERR_ZERO_SAMPLES).
+ * Every rank must call with the same count and dtype in the same order; a mismatch is detected in the
+ * handshake and latched as PR_ERR_LENGTH_MISMATCH on every rank with buf untouched; Σn = 0 latches
+ * PR_ERR_ZERO_SAMPLES; a peer that never arrives latches PR_ERR_PEER_TIMEOUT after watchdog_ns.
+ * Latched device errors are returned by pr_comm_status() once the stream has completed, and by the
+ * next call.  Async; stream-ordered; the caller keeps buf alive until the stream completes. */
+int pr_weighted_allreduce(pr_comm *c, void *d_buf, int64_t count, int32_t dt, int64_t n_local,
+                          void *stream);
+/* Local-group form: one cooperative launch runs all P ranks of a pr_comm_init_local group (rank r uses
+ * d_bufs[r], n_local[r]); comms: host pr_comm*[P] in rank order.  (pr_weighted_allreduce on a single
+ * rank of a local group launches that rank alone: the caller must issue all P ranks' calls on distinct
+ * streams so that they are co-resident — used to exercise the mismatch / timeout paths.) */
+int pr_weighted_allreduce_local(pr_comm *const *comms, void *const *d_bufs, int64_t count, int32_t dt,
+                                const int64_t *n_local, void *stream);
+
+/* Algorithm 1 step 1: every rank contributes `local` and receives all P values in rank
+ * order into host out[P].  Synchronous (waits for `stream`). */
+int pr_comm_allgather_f64(pr_comm *c, double local, double *out, void *stream);
+
+/* Latched device error of the last completed call (PR_OK if none). Non-blocking host read. */
+int pr_comm_status(pr_comm *c);
+/* %globaltimer stamps (ns) of the last completed call on this rank: [0] kernel entry, [1] handshake
+ * complete (barrier left: t_w = [1]−[0]), [2] kernel exit (t_c = [2]−[1]).  out: host int64[3]. */
+int pr_comm_timestamps(pr_comm *c, int64_t *out);
+/* Rank and size of a communicator. */
+int pr_comm_rank(const pr_comm *c, int32_t *rank, int32_t *size);
+/* Collective teardown (frees staging, flags, pr_comm_alloc memory, closes IPC mappings). */
+void pr_comm_destroy(pr_comm *c);
+
+/* =================================================================================================
+ * 4. Test hooks (parity pins against library routines; no hot-path role)
+ * ================================================================================================= */
+
+/* d_out[4·i + j] = word j of Philox4x32-10(ctr_i, key) computed by the library's device function,
+ * ctr_i = (d_ctr[4i..4i+3]) ; with use_curand != 0 the same through cuRAND's curand_Philox4x32_10
+ * (the library routine pin of SURVEY §8(c) O3 (ii)).  n counters. */
+int pr_test_philox(const uint32_t *d_ctr, int64_t n, uint64_t key, int32_t use_curand, uint32_t *d_out,
+                   void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PROPRING_H */

@@ -1,0 +1,24 @@
+// Internal helpers shared by the library's translation units (not part of the ABI).
+#pragma once
+#include <stdint.h>
+
+#include "../../include/propring.h"
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#define PR_CUDA_TRY(expr)                                   \
+    do {                                                    \
+        cudaError_t _e = (expr);                            \
+        if (_e != cudaSuccess) {                            \
+            pr_internal_set_cuda_error(_e, #expr);          \
+            return PR_ERR_CUDA;                             \
+        }                                                   \
+    } while (0)
+void pr_internal_set_cuda_error(cudaError_t e, const char* what);
+#endif
+
+// alloc.cpp
+int pr_internal_shard_range(const pr_alloc* a, int32_t rank, int64_t* N, int64_t* off, int64_t* len);
+
+// Last CUDA error text (thread-local), for debugging from Python.
+extern "C" const char* pr_last_cuda_error(void);

@@ -1,0 +1,200 @@
+// K2 — step-batch gather of sampled rows into the local batch, with the u8 -> f32/bf16 affine fused.
+//
+// Paper: Algorithm 1 step 4, "Proportionally draw samples from the sub-data set for training";
+// static allocation, "Worker i draws w_i samples from subdataset".  Data-plane definition is
+// build-defined (DESIGN.md §3 #38): dst[t,:] = op(src[idx[t],:]), lab_dst[t] = lab_src[idx[t]].
+//
+// HBM-bound: per row, row_bytes read + out_bytes written (+8 B index, +16 B label).  Layout: work item =
+// (row, 2 KiB segment of the input row); one warp per work item; every lane issues its 16-byte loads
+// (ld.global.nc.L1::no_allocate — the dataset is read-only and streamed) before any store (MLP 4 per
+// lane), converts in registers and stores 16-byte vectors (2 per input vector for bf16, 4 for f32).
+// Grid = 148 SMs × 8 CTAs × 8 warps, grid-stride over work items.
+#include <cuda_bf16.h>
+
+#include "common.h"
+
+namespace {
+
+constexpr int kWarpsPerCta = 8;
+constexpr int kVecPerLane = 4;                            // 16-byte input vectors per lane per work item
+constexpr int kSegVec = 32 * kVecPerLane;                 // input vectors per work item (2 KiB)
+
+struct GatherParams {
+    const uint8_t* src;
+    int64_t row_bytes;
+    const int64_t* idx;
+    int64_t n;
+    uint8_t* dst;
+    int32_t op;
+    int32_t channels;
+    int64_t plane;
+    float scale[PR_GATHER_MAX_CHANNELS];
+    float shift[PR_GATHER_MAX_CHANNELS];
+    const int64_t* lab_src;
+    int64_t* lab_dst;
+};
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// (float(x) − shift) · scale: two separately rounded fp32 operations (no contraction).
+__device__ __forceinline__ float affine(uint32_t x, float sc, float sh) {
+    return __fmul_rn(__fsub_rn((float)x, sh), sc);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat16 a = __float2bfloat16_rn(lo), b = __float2bfloat16_rn(hi);
+    return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+}
+
+template <int OP>
+__device__ __forceinline__ void convert_store(const GatherParams& p, uint8_t* drow, int64_t v, uint4 x) {
+    if (OP == PR_GATHER_COPY) {
+        st_v4(drow + v * 16, x);
+        return;
+    }
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    float f[16];
+    const uint32_t k0 = (uint32_t)v * 16u;  // element index of the first byte (row_bytes < 2^31)
+    const uint32_t plane = (uint32_t)p.plane;
+    if (plane % 16u == 0) {
+        const int c = (int)(k0 / plane);
+        const float sc = p.scale[c], sh = p.shift[c];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = affine((w[j >> 2] >> (8 * (j & 3))) & 0xffu, sc, sh);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int c = (int)((k0 + (uint32_t)j) / plane);
+            f[j] = affine((w[j >> 2] >> (8 * (j & 3))) & 0xffu, p.scale[c], p.shift[c]);
+        }
+    }
+    if (OP == PR_GATHER_U8_TO_BF16_AFFINE) {
+        uint8_t* d = drow + v * 32;
+        st_v4(d, make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                            pack_bf16x2(f[6], f[7])));
+        st_v4(d + 16, make_uint4(pack_bf16x2(f[8], f[9]), pack_bf16x2(f[10], f[11]), pack_bf16x2(f[12], f[13]),
+                                 pack_bf16x2(f[14], f[15])));
+    } else {
+        uint8_t* d = drow + v * 64;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            st_v4(d + 16 * q, make_uint4(__float_as_uint(f[4 * q]), __float_as_uint(f[4 * q + 1]),
+                                         __float_as_uint(f[4 * q + 2]), __float_as_uint(f[4 * q + 3])));
+    }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) gather_kernel(const __grid_constant__ GatherParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t vpr = p.row_bytes / 16;                      // input vectors per row
+    const int64_t segs = (vpr + kSegVec - 1) / kSegVec;         // work items per row
+    const int64_t out_mul = (OP == PR_GATHER_COPY) ? 1 : (OP == PR_GATHER_U8_TO_BF16_AFFINE ? 2 : 4);
+    const int64_t items = p.n * segs;
+
+    // labels: one thread per row
+    if (p.lab_dst) {
+        const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < p.n; t += nthreads)
+            p.lab_dst[t] = p.lab_src[p.idx[t]];
+    }
+
+    for (int64_t it = warp; it < items; it += nwarps) {
+        const int64_t row = it / segs;
+        const int64_t seg = it - row * segs;
+        const int64_t src_row = __ldg(p.idx + row);
+        const uint8_t* srow = p.src + src_row * p.row_bytes;
+        uint8_t* drow = p.dst + row * p.row_bytes * out_mul;
+        const int64_t v0 = seg * kSegVec + lane;
+        uint4 x[kVecPerLane];
+#pragma unroll
+        for (int u = 0; u < kVecPerLane; ++u) {
+            const int64_t v = v0 + 32 * u;
+            if (v < vpr) x[u] = ld_nc_v4(srow + v * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < kVecPerLane; ++u) {
+            const int64_t v = v0 + 32 * u;
+            if (v < vpr) convert_store<OP>(p, drow, v, x[u]);
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_bytes, const int64_t* d_idx, int64_t n,
+                              void* d_dst, const pr_gather_op* op, const int64_t* d_lab_src, int64_t* d_lab_dst,
+                              void* stream) {
+    if (n < 0 || n_src < 0 || row_bytes <= 0) return PR_ERR_INVALID;
+    if (n == 0) return PR_OK;
+    if (!d_src || !d_idx || !d_dst || (d_lab_dst && !d_lab_src)) return PR_ERR_INVALID;
+    if (row_bytes >= ((int64_t)1 << 31)) return PR_ERR_INVALID;
+    if (row_bytes % 16 || ((uintptr_t)d_src & 15) || ((uintptr_t)d_dst & 15)) return PR_ERR_ALIGN;
+    GatherParams p;
+    p.src = (const uint8_t*)d_src;
+    p.row_bytes = row_bytes;
+    p.idx = d_idx;
+    p.n = n;
+    p.dst = (uint8_t*)d_dst;
+    p.op = op ? op->op : PR_GATHER_COPY;
+    p.channels = 1;
+    p.plane = row_bytes;
+    for (int i = 0; i < PR_GATHER_MAX_CHANNELS; ++i) { p.scale[i] = 1.0f; p.shift[i] = 0.0f; }
+    if (p.op != PR_GATHER_COPY) {
+        if (p.op != PR_GATHER_U8_TO_F32_AFFINE && p.op != PR_GATHER_U8_TO_BF16_AFFINE) return PR_ERR_INVALID;
+        if (op->channels < 1 || op->channels > PR_GATHER_MAX_CHANNELS || op->plane < 1 ||
+            op->plane * op->channels != row_bytes)
+            return PR_ERR_INVALID;
+        p.channels = op->channels;
+        p.plane = op->plane;
+        for (int i = 0; i < op->channels; ++i) { p.scale[i] = op->scale[i]; p.shift[i] = op->shift[i]; }
+    }
+    p.lab_src = d_lab_src;
+    p.lab_dst = d_lab_dst;
+    const int64_t vpr = row_bytes / 16;
+    const int64_t items = n * ((vpr + kSegVec - 1) / kSegVec);
+    int64_t blocks = (items + kWarpsPerCta - 1) / kWarpsPerCta;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (p.op) {
+        case PR_GATHER_COPY: gather_kernel<PR_GATHER_COPY><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, s>>>(p); break;
+        case PR_GATHER_U8_TO_F32_AFFINE:
+            gather_kernel<PR_GATHER_U8_TO_F32_AFFINE><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, s>>>(p);
+            break;
+        default: gather_kernel<PR_GATHER_U8_TO_BF16_AFFINE><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, s>>>(p);
+    }
+    PR_CUDA_TRY(cudaGetLastError());
+    return PR_OK;
+}
+
+// ---- K4: emulated heterogeneity --------------------------------------------------------------------
+namespace {
+__global__ void spin_kernel(int64_t ns) {
+    if (threadIdx.x != 0) return;
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while ((int64_t)(t - t0) < ns);
+}
+}  // namespace
+
+extern "C" int pr_spin(int64_t ns, void* stream) {
+    if (ns <= 0) return PR_OK;
+    spin_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(ns);
+    PR_CUDA_TRY(cudaGetLastError());
+    return PR_OK;
+}

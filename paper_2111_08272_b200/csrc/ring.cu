@@ -1,0 +1,925 @@
+// K3 — sample-count-weighted ring allreduce over NVLink 5 / NVSwitch peer memory (+ its communicator).
+//
+// Paper: Ring AllReduce (§2.2): n workers on a ring, the gradient cut into n parts; a reduce-scatter
+// phase ("the kth worker ... send the kth data to the next worker, and at the same time receive the k−1th
+// data from the previous worker") then an all-gather phase ("each worker sends the integrated part to the
+// next worker"), preceded by the barrier that synchronises all workers — the wait the
+// method shrinks (t_w).  Eq. 1: the update is the mean over N = Σ_i minibatch·w_i
+// samples, so with buf_r = rank r's local mean over n_r samples the reduction is buf = Σ_r (n_r/Σn)·buf_r.
+// Readings: #11 local-mean convention, #13 ring schedule, #14 chunk boundaries, #15 order
+// and rounding, #32 Σn exchanged in the handshake, #33 n_r = 0 contributes nothing, #36 the n_r/Σn scale
+// is applied where a contribution enters the ring (hop 0: y = s·g; later: y = fma(s, g, recv)).
+//
+// Design (B200): ONE kernel per call, one CTA per ring "channel".  Each channel owns a contiguous slice
+// of every chunk and runs an independent ring with its own flags and K staging slots:
+//   * all synchronisation is local polling (ld.acquire.sys) + remote signalling (st.release.sys), i.e.
+//     every NVLink transaction is a store: data is PUSHED into the next rank's staging slot (reduce-scatter)
+//     or straight into the next rank's registered gradient buffer (all-gather, no staging copy);
+//   * monotone 64-bit counters (ready / credit / ag_ready) — never reset, so back-to-back calls and
+//     CUDA-graph replays need no host involvement; handshake entries are double-buffered by seq parity;
+//   * every spin has a %globaltimer deadline (watchdog) that latches PR_ERR_PEER_TIMEOUT.
+// Data path per slice: 16-byte vector loads (ld.global.cg: peer-written data bypasses the non-coherent
+// L1), fp32 math, RNE to the storage dtype, 16-byte vector stores to local and peer memory.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+#define PR_MAX_REGS 8
+
+namespace {
+
+constexpr int kUnroll = 4;
+
+// ---- window layout (one cudaMalloc per rank, CUDA-IPC exported) ------------------------------------
+struct ChanFlags {          // written by peers, polled locally
+    unsigned long long rs_ready;   uint64_t p0[15];   // by prev: slot-slices produced into my staging
+    unsigned long long rs_credit;  uint64_t p1[15];   // by next: my slot-slices it has consumed
+    unsigned long long ag_ready;   uint64_t p2[15];   // by prev: direct all-gather slices written into my buf
+};
+struct HsEntry {            // handshake entry, written by rank q into every peer's page (slot [parity][q])
+    unsigned long long seq;
+    int64_t count;
+    int64_t n;
+    int32_t dtype;
+    int32_t reg_id;
+    int64_t offset;
+    uint64_t pad[3];
+};
+struct ChanState {          // local only
+    unsigned long long seq, slot_base, ag_base;
+    uint64_t pad[13];
+};
+struct AgEntry {
+    unsigned long long seq;
+    double v;
+};
+static_assert(sizeof(ChanFlags) == 384, "flags");
+static_assert(sizeof(HsEntry) == 64, "hs");
+static_assert(sizeof(ChanState) == 128, "state");
+
+struct DevTable {
+    int32_t rank, P, channels, slots;
+    int64_t slot_bytes;
+    int64_t watchdog_ns;
+    uint64_t off_flags, off_hs, off_state, off_ag, off_staging, window_bytes;
+    volatile int* status;           // host-mapped
+    volatile long long* stamps;     // host-mapped [3]
+    uint8_t* win[PR_MAX_RANKS];
+    uint8_t* reg[PR_MAX_REGS][PR_MAX_RANKS];
+};
+
+struct RankCall {
+    const DevTable* tab;
+    void* buf;
+    int64_t n_local;
+    int32_t reg_id;
+    int32_t pad;
+    int64_t reg_off;
+};
+
+struct LaunchArgs {
+    int64_t count;
+    int32_t dtype;
+    int32_t nranks;     // entries in calls[] (gridDim.y)
+    RankCall calls[PR_MAX_RANKS];
+};
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+void layout(DevTable& t) {
+    t.off_flags = 0;
+    uint64_t o = (uint64_t)t.channels * sizeof(ChanFlags);
+    t.off_hs = o = align_up(o, 256);
+    o += (uint64_t)t.channels * 2 * t.P * sizeof(HsEntry);
+    t.off_state = o = align_up(o, 256);
+    o += (uint64_t)t.channels * sizeof(ChanState);
+    t.off_ag = o = align_up(o, 256);
+    o += 2ull * t.P * sizeof(AgEntry);
+    t.off_staging = o = align_up(o, 4096);
+    o += (uint64_t)t.channels * t.slots * (uint64_t)t.slot_bytes;
+    t.window_bytes = align_up(o, 4096);
+}
+
+// ---- device helpers --------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ long long ld_relaxed_s64(const void* p) {
+    long long v;
+    asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_s64(void* p, long long v) {
+    asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ ChanFlags* flags_of(uint8_t* w, const DevTable* t, int ch) {
+    return reinterpret_cast<ChanFlags*>(w + t->off_flags) + ch;
+}
+__device__ __forceinline__ HsEntry* hs_of(uint8_t* w, const DevTable* t, int ch, int par, int q) {
+    return reinterpret_cast<HsEntry*>(w + t->off_hs) + ((size_t)ch * 2 + par) * t->P + q;
+}
+__device__ __forceinline__ ChanState* state_of(uint8_t* w, const DevTable* t, int ch) {
+    return reinterpret_cast<ChanState*>(w + t->off_state) + ch;
+}
+__device__ __forceinline__ uint8_t* slot_of(uint8_t* w, const DevTable* t, int ch, unsigned long long J) {
+    return w + t->off_staging + ((size_t)ch * t->slots + (size_t)(J % (unsigned long long)t->slots)) * t->slot_bytes;
+}
+
+enum Mode { M_SCALE = 0, M_FMA = 1, M_COPY = 2, M_ZERO = 3 };
+
+// Element traits: fp32 math on 16-byte vectors of the storage dtype.
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+    static constexpr int V = 4;
+    __device__ static float ld(const float* p) { float v; asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p)); return v; }
+    __device__ static void st(float* p, float v) { *p = v; }
+    __device__ static float to_f(float v) { return v; }
+    __device__ static float from_f(float v) { return v; }
+    __device__ static uint4 op(int mode, float s, uint4 g, uint4 in) {
+        uint4 y;
+        const uint32_t gi[4] = {g.x, g.y, g.z, g.w}, ii[4] = {in.x, in.y, in.z, in.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float gv = __uint_as_float(gi[j]), iv = __uint_as_float(ii[j]);
+            float r;
+            if (mode == M_SCALE) r = __fmul_rn(s, gv);
+            else if (mode == M_FMA) r = __fmaf_rn(s, gv, iv);
+            else if (mode == M_COPY) r = iv;
+            else r = 0.0f;
+            o[j] = __float_as_uint(r);
+        }
+        y.x = o[0]; y.y = o[1]; y.z = o[2]; y.w = o[3];
+        return y;
+    }
+};
+template <> struct Vec<__nv_bfloat16> {
+    static constexpr int V = 8;
+    __device__ static __nv_bfloat16 ld(const __nv_bfloat16* p) {
+        unsigned short v;
+        asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(v) : "l"(p));
+        return __ushort_as_bfloat16(v);
+    }
+    __device__ static void st(__nv_bfloat16* p, __nv_bfloat16 v) { *p = v; }
+    __device__ static float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+    __device__ static __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
+    __device__ static float lo(uint32_t w) { return __uint_as_float(w << 16); }
+    __device__ static float hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+    __device__ static uint32_t pack(float a, float b) {
+        return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
+               ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
+    }
+    __device__ static float one(int mode, float s, float gv, float iv) {
+        if (mode == M_SCALE) return __fmul_rn(s, gv);
+        if (mode == M_FMA) return __fmaf_rn(s, gv, iv);
+        if (mode == M_COPY) return iv;
+        return 0.0f;
+    }
+    __device__ static uint4 op(int mode, float s, uint4 g, uint4 in) {
+        if (mode == M_COPY) return in;
+        const uint32_t gi[4] = {g.x, g.y, g.z, g.w}, ii[4] = {in.x, in.y, in.z, in.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            o[j] = pack(one(mode, s, lo(gi[j]), lo(ii[j])), one(mode, s, hi(gi[j]), hi(ii[j])));
+        return make_uint4(o[0], o[1], o[2], o[3]);
+    }
+};
+
+// Move one slice: out1[e] (and out2[e]) = f(g[e], in[e]) for e < len.  All threads of the CTA.
+template <typename T>
+__device__ __forceinline__ void move_slice(int mode, float s, const T* g, const T* in, T* out1, T* out2, int64_t len) {
+    constexpr int V = Vec<T>::V;
+    const int64_t nv = len / V;
+    const int64_t nt = blockDim.x;
+    const bool need_g = (mode == M_SCALE || mode == M_FMA), need_in = (mode == M_FMA || mode == M_COPY);
+    for (int64_t base = threadIdx.x; base < nv; base += nt * kUnroll) {
+        uint4 a[kUnroll], b[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int64_t v = base + u * nt;
+            a[u] = make_uint4(0, 0, 0, 0);
+            b[u] = make_uint4(0, 0, 0, 0);
+            if (v < nv) {
+                if (need_g) a[u] = ld_cg_v4(g + v * V);
+                if (need_in) b[u] = ld_cg_v4(in + v * V);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int64_t v = base + u * nt;
+            if (v < nv) {
+                const uint4 y = Vec<T>::op(mode, s, a[u], b[u]);
+                st_v4(out1 + v * V, y);
+                if (out2) st_v4(out2 + v * V, y);
+            }
+        }
+    }
+    for (int64_t e = nv * V + threadIdx.x; e < len; e += nt) {   // ragged tail (end of the buffer only)
+        const float gv = need_g ? Vec<T>::to_f(Vec<T>::ld(g + e)) : 0.0f;
+        const float iv = need_in ? Vec<T>::to_f(Vec<T>::ld(in + e)) : 0.0f;
+        float r;
+        if (mode == M_SCALE) r = __fmul_rn(s, gv);
+        else if (mode == M_FMA) r = __fmaf_rn(s, gv, iv);
+        else if (mode == M_COPY) r = iv;
+        else r = 0.0f;
+        const T y = (mode == M_COPY) ? Vec<T>::ld(in + e) : Vec<T>::from_f(r);
+        Vec<T>::st(out1 + e, y);
+        if (out2) Vec<T>::st(out2 + e, y);
+    }
+}
+
+struct Shared {
+    int err;
+    int direct;
+    long long sumn;
+    void* next_buf;
+};
+
+__device__ __forceinline__ void latch(const DevTable* t, int code) {
+    if (*t->status == 0) *t->status = code;
+}
+
+// Spin until *p >= target; false on watchdog expiry.
+__device__ __forceinline__ bool wait_ge(const unsigned long long* p, unsigned long long target,
+                                        unsigned long long deadline) {
+    while (ld_acquire(p) < target) {
+        if (gtimer() > deadline) return false;
+    }
+    return true;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, 1) ring_kernel(const __grid_constant__ LaunchArgs A) {
+    __shared__ Shared sh;
+    const RankCall& rc = A.calls[blockIdx.y];
+    const DevTable* tab = rc.tab;
+    const int ch = blockIdx.x;
+    const int r = tab->rank, P = tab->P;
+    const int next = (r + 1) % P, prev = (r + P - 1) % P;
+    uint8_t* my = tab->win[r];
+    ChanState* st = state_of(my, tab, ch);
+    ChanFlags* myf = flags_of(my, tab, ch);
+    ChanFlags* nxf = flags_of(tab->win[next], tab, ch);
+    ChanFlags* pvf = flags_of(tab->win[prev], tab, ch);
+    const bool t0 = threadIdx.x == 0;
+    unsigned long long deadline = ~0ull;
+
+    // ---- handshake = the barrier; its duration is t_w ---------------------------------
+    if (t0) {
+        const unsigned long long start = gtimer();
+        if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
+        if (ch == 0) tab->stamps[0] = (long long)start;
+        const unsigned long long seq = st->seq + 1;
+        const int par = (int)(seq & 1ull);
+        for (int q = 0; q < P; ++q) {
+            HsEntry* e = hs_of(tab->win[q], tab, ch, par, r);
+            st_relaxed_s64(&e->count, A.count);
+            st_relaxed_s64(&e->n, rc.n_local);
+            st_relaxed_s64(&e->dtype, ((long long)rc.reg_id << 32) | (unsigned)A.dtype);  // dtype | reg_id
+            st_relaxed_s64(&e->offset, rc.reg_off);
+            st_release(&e->seq, seq);
+        }
+        int err = 0, direct = 1, next_reg = -1;
+        long long sumn = 0, next_off = 0;
+        for (int q = 0; q < P && !err; ++q) {
+            HsEntry* e = hs_of(my, tab, ch, par, q);
+            if (!wait_ge(&e->seq, seq, deadline)) { err = PR_ERR_PEER_TIMEOUT; break; }
+            const long long cnt = ld_relaxed_s64(&e->count);
+            const long long n = ld_relaxed_s64(&e->n);
+            const long long dr = ld_relaxed_s64(&e->dtype);
+            const long long off = ld_relaxed_s64(&e->offset);
+            const int dt = (int)(dr & 0xffffffffll), rid = (int)(dr >> 32);
+            if (cnt != A.count || dt != A.dtype) err = PR_ERR_LENGTH_MISMATCH;
+            sumn += n;
+            if (rid < 0) direct = 0;
+            if (q == next) { next_reg = rid; next_off = off; }
+        }
+        if (!err && sumn <= 0) err = PR_ERR_ZERO_SAMPLES;
+        st->seq = seq;
+        sh.err = err;
+        sh.direct = direct;
+        sh.sumn = sumn;
+        sh.next_buf = (direct && next_reg >= 0)
+                          ? (void*)((uintptr_t)tab->reg[next_reg][next] + (uintptr_t)next_off)
+                          : nullptr;
+        if (ch == 0) tab->stamps[1] = (long long)gtimer();
+    }
+    __syncthreads();
+    if (sh.err) {
+        if (t0) latch(tab, sh.err);
+        return;
+    }
+
+    // ---- geometry (DESIGN.md §3 #14) ----------------------------------------------------------------
+    constexpr int V = Vec<T>::V;
+    const int64_t count = A.count;
+    const int64_t per = (count + P - 1) / P;
+    const int64_t cs = (per + V - 1) / V * V;                      // chunk elements
+    const int64_t subp = (cs + tab->channels - 1) / tab->channels;
+    const int64_t sub = (subp + V - 1) / V * V;                   // this channel's share of a chunk
+    const int64_t sl = tab->slot_bytes / (int64_t)sizeof(T);       // slice elements
+    const int64_t nsl = sub > 0 ? (sub + sl - 1) / sl : 0;
+    const float s = (float)((double)rc.n_local / (double)sh.sumn);  // n_r/Σn: fp64 division, fp32 weight
+    const bool act = rc.n_local > 0;
+    const bool direct = sh.direct != 0;
+    T* buf = reinterpret_cast<T*>(rc.buf);
+    T* nbuf = reinterpret_cast<T*>(sh.next_buf);
+    unsigned long long prodJ = st->slot_base, consJ = st->slot_base, agP = st->ag_base, agC = st->ag_base;
+    const unsigned long long K = (unsigned long long)tab->slots;
+
+    auto range = [&](int c, int64_t i, int64_t& lo, int64_t& len) {
+        const int64_t clo = (int64_t)c * cs;
+        const int64_t chi = min(clo + cs, count);
+        const int64_t a = clo + (int64_t)ch * sub + i * sl;
+        const int64_t b = min(min(a + sl, clo + min((int64_t)(ch + 1) * sub, cs)), chi);
+        lo = a;
+        len = b > a ? b - a : 0;
+    };
+    // thread 0 waits, then the CTA proceeds together; false = abort (watchdog)
+    auto sync_ok = [&]() -> bool {
+        __syncthreads();
+        return sh.err == 0;
+    };
+    auto fail = [&]() {
+        sh.err = PR_ERR_PEER_TIMEOUT;
+        latch(tab, PR_ERR_PEER_TIMEOUT);
+    };
+    auto wait_credit = [&]() {   // slot prodJ % K in next's staging is free once next consumed prodJ − K
+        if (prodJ + 1 > K && !wait_ge(&myf->rs_credit, prodJ + 1 - K, deadline)) fail();
+    };
+    auto wait_ready = [&]() {
+        if (!wait_ge(&myf->rs_ready, consJ + 1, deadline)) fail();
+    };
+
+    // RS hop 0: chunk r, y = s·g (or 0 if this rank has no samples)
+    for (int64_t i = 0; i < nsl; ++i) {
+        int64_t lo, len;
+        range(r, i, lo, len);
+        if (t0) wait_credit();
+        if (!sync_ok()) return;
+        move_slice<T>(act ? M_SCALE : M_ZERO, s, buf + lo, nullptr,
+                      reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), nullptr, len);
+        __syncthreads();
+        if (t0) st_release(&nxf->rs_ready, prodJ + 1);
+        ++prodJ;
+    }
+    // RS hops 1..P−2: chunk (r−k) mod P, y = fma(s, g, recv)
+    for (int k = 1; k <= P - 2; ++k) {
+        const int c = (r - k + P) % P;
+        for (int64_t i = 0; i < nsl; ++i) {
+            int64_t lo, len;
+            range(c, i, lo, len);
+            if (t0) { wait_ready(); if (!sh.err) wait_credit(); }
+            if (!sync_ok()) return;
+            move_slice<T>(act ? M_FMA : M_COPY, s, buf + lo, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
+                          reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), nullptr, len);
+            __syncthreads();
+            if (t0) {
+                st_release(&pvf->rs_credit, consJ + 1);
+                st_release(&nxf->rs_ready, prodJ + 1);
+            }
+            ++consJ;
+            ++prodJ;
+        }
+    }
+    // last RS hop: chunk (r+1) mod P is complete here; store it locally and send it on (AG hop 0)
+    if (P >= 2) {
+        const int c = (r + 1) % P;
+        for (int64_t i = 0; i < nsl; ++i) {
+            int64_t lo, len;
+            range(c, i, lo, len);
+            if (t0) { wait_ready(); if (!sh.err && !direct) wait_credit(); }
+            if (!sync_ok()) return;
+            T* out2 = direct ? nbuf + lo : reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ));
+            move_slice<T>(act ? M_FMA : M_COPY, s, buf + lo, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
+                          buf + lo, out2, len);
+            __syncthreads();
+            if (t0) {
+                st_release(&pvf->rs_credit, consJ + 1);
+                if (direct) st_release(&nxf->ag_ready, agP + 1);
+                else st_release(&nxf->rs_ready, prodJ + 1);
+            }
+            ++consJ;
+            if (direct) ++agP; else ++prodJ;
+        }
+    }
+    // AG hops 1..P−2: forward chunk (r+1−k) mod P received at hop k−1
+    for (int k = 1; k <= P - 2; ++k) {
+        const int c = (r + 1 - k + P) % P;
+        for (int64_t i = 0; i < nsl; ++i) {
+            int64_t lo, len;
+            range(c, i, lo, len);
+            if (direct) {
+                if (t0 && !wait_ge(&myf->ag_ready, agC + 1, deadline)) fail();
+                if (!sync_ok()) return;
+                move_slice<T>(M_COPY, s, nullptr, buf + lo, nbuf + lo, nullptr, len);
+                __syncthreads();
+                if (t0) st_release(&nxf->ag_ready, agP + 1);
+                ++agC;
+                ++agP;
+            } else {
+                if (t0) { wait_ready(); if (!sh.err) wait_credit(); }
+                if (!sync_ok()) return;
+                move_slice<T>(M_COPY, s, nullptr, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)), buf + lo,
+                              reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), len);
+                __syncthreads();
+                if (t0) {
+                    st_release(&pvf->rs_credit, consJ + 1);
+                    st_release(&nxf->rs_ready, prodJ + 1);
+                }
+                ++consJ;
+                ++prodJ;
+            }
+        }
+    }
+    // AG receive of hop P−2: chunk (r+2) mod P — not forwarded
+    if (P >= 2) {
+        const int c = (r + 2) % P;
+        for (int64_t i = 0; i < nsl; ++i) {
+            int64_t lo, len;
+            range(c, i, lo, len);
+            if (direct) {
+                if (t0 && !wait_ge(&myf->ag_ready, agC + 1, deadline)) fail();
+                ++agC;
+                if (!sync_ok()) return;
+            } else {
+                if (t0) wait_ready();
+                if (!sync_ok()) return;
+                move_slice<T>(M_COPY, s, nullptr, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)), buf + lo,
+                              nullptr, len);
+                __syncthreads();
+                if (t0) st_release(&pvf->rs_credit, consJ + 1);
+                ++consJ;
+            }
+        }
+    }
+    if (t0) {
+        st->slot_base = consJ;   // == prodJ: every rank produces and consumes the same number of slices
+        st->ag_base = agC;       // == agP
+        if (ch == 0) tab->stamps[2] = (long long)gtimer();
+    }
+}
+
+__global__ void allgather_f64_kernel(const DevTable* tab, unsigned long long seq, double v, double* out) {
+    if (threadIdx.x != 0) return;
+    const int r = tab->rank, P = tab->P;
+    const int par = (int)(seq & 1ull);
+    unsigned long long deadline = ~0ull;
+    if (tab->watchdog_ns > 0) deadline = gtimer() + (unsigned long long)tab->watchdog_ns;
+    for (int q = 0; q < P; ++q) {
+        AgEntry* e = reinterpret_cast<AgEntry*>(tab->win[q] + tab->off_ag) + par * P + r;
+        st_relaxed_s64(&e->v, __double_as_longlong(v));
+        st_release(&e->seq, seq);
+    }
+    for (int q = 0; q < P; ++q) {
+        AgEntry* e = reinterpret_cast<AgEntry*>(tab->win[r] + tab->off_ag) + par * P + q;
+        if (!wait_ge(&e->seq, seq, deadline)) { latch(tab, PR_ERR_PEER_TIMEOUT); return; }
+        out[q] = __longlong_as_double(ld_relaxed_s64(&e->v));
+    }
+}
+
+}  // namespace
+
+// =====================================================================================================
+// Host side: communicator
+// =====================================================================================================
+
+namespace {
+thread_local std::string g_cuda_err;
+
+struct Reg {
+    uint8_t* base = nullptr;
+    size_t bytes = 0;
+    bool owned = false;
+    std::vector<uint8_t*> peer;   // mapped base of rank q's region (own = base); IPC-opened for q != rank
+};
+
+struct Hello {
+    cudaIpcMemHandle_t handle;
+    int32_t P, rank, device, channels, slots, threads;
+    int64_t slot_bytes, window_bytes;
+    uint64_t bytes;   // registration size
+};
+}  // namespace
+
+void pr_internal_set_cuda_error(cudaError_t e, const char* what) {
+    g_cuda_err = std::string(what) + ": " + cudaGetErrorString(e);
+}
+extern "C" const char* pr_last_cuda_error(void) { return g_cuda_err.c_str(); }
+
+struct pr_comm {
+    int32_t rank = 0, P = 1, device = 0;
+    bool local = false;
+    pr_comm_config cfg{};
+    DevTable tab{};
+    DevTable* d_tab = nullptr;
+    uint8_t* win = nullptr;                 // own window
+    std::vector<uint8_t*> opened;           // IPC-opened peer pointers (to close)
+    int* h_status = nullptr;                // host-mapped status [0], stamps at +64 B
+    long long* h_stamps = nullptr;
+    double* h_ag = nullptr;                 // host-mapped allgather output
+    std::vector<Reg> regs;
+    pr_exchange_fn fn = nullptr;
+    void* ctx = nullptr;
+    unsigned long long ag_seq = 0;
+};
+
+namespace {
+
+pr_comm_config default_config() {
+    pr_comm_config c;
+    c.channels = 16;
+    c.slots = 4;
+    c.threads = 512;
+    c.flags = 0;
+    c.slot_bytes = 128 * 1024;
+    c.watchdog_ns = 10ll * 1000 * 1000 * 1000;
+    return c;
+}
+
+int check_config(const pr_comm_config& c) {
+    if ((c.flags & ~PR_COMM_FLAG_FORCE_STAGED) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
+        c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20))
+        return PR_ERR_INVALID;
+    return PR_OK;
+}
+
+int alloc_common(pr_comm* c) {
+    PR_CUDA_TRY(cudaSetDevice(c->device));
+    DevTable& t = c->tab;
+    t.rank = c->rank;
+    t.P = c->P;
+    t.channels = c->cfg.channels;
+    t.slots = c->cfg.slots;
+    t.slot_bytes = c->cfg.slot_bytes;
+    t.watchdog_ns = c->cfg.watchdog_ns;
+    layout(t);
+    PR_CUDA_TRY(cudaMalloc((void**)&c->win, t.window_bytes));
+    PR_CUDA_TRY(cudaMemset(c->win, 0, t.window_bytes));
+    void* h = nullptr;
+    PR_CUDA_TRY(cudaHostAlloc(&h, 4096, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(h, 0, 4096);
+    c->h_status = reinterpret_cast<int*>(h);
+    c->h_stamps = reinterpret_cast<long long*>((char*)h + 64);
+    c->h_ag = reinterpret_cast<double*>((char*)h + 256);
+    void* d = nullptr;
+    PR_CUDA_TRY(cudaHostGetDevicePointer(&d, h, 0));
+    t.status = reinterpret_cast<volatile int*>(d);
+    t.stamps = reinterpret_cast<volatile long long*>((char*)d + 64);
+    PR_CUDA_TRY(cudaMalloc((void**)&c->d_tab, sizeof(DevTable)));
+    return PR_OK;
+}
+
+int push_table(pr_comm* c) {
+    PR_CUDA_TRY(cudaMemcpy(c->d_tab, &c->tab, sizeof(DevTable), cudaMemcpyHostToDevice));
+    return PR_OK;
+}
+
+int exchange(pr_comm* c, const void* send, size_t len, void* recv) {
+    if (!c->fn) return PR_ERR_INVALID;
+    return c->fn(c->ctx, send, len, recv) == 0 ? PR_OK : PR_ERR_INVALID;
+}
+
+void free_comm(pr_comm* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (auto& rg : c->regs) {
+        for (int q = 0; q < (int)rg.peer.size(); ++q)
+            if (!c->local && q != c->rank && rg.peer[q]) cudaIpcCloseMemHandle(rg.peer[q]);
+        if (rg.owned && rg.base) cudaFree(rg.base);
+    }
+    for (auto* p : c->opened) cudaIpcCloseMemHandle(p);
+    if (c->win) cudaFree(c->win);
+    if (c->d_tab) cudaFree(c->d_tab);
+    if (c->h_status) cudaFreeHost(c->h_status);
+    delete c;
+}
+
+int find_reg(const pr_comm* c, const void* buf, size_t bytes, int32_t* id, int64_t* off) {
+    if (c->cfg.flags & PR_COMM_FLAG_FORCE_STAGED) {
+        *id = -1;
+        *off = 0;
+        return PR_OK;
+    }
+    if (c->local) {   // local group: every pointer is directly addressable; region 0 has base 0
+        *id = 0;
+        *off = (int64_t)(uintptr_t)buf;
+        return PR_OK;
+    }
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(buf);
+    for (size_t i = 0; i < c->regs.size(); ++i) {
+        const Reg& rg = c->regs[i];
+        if (b >= rg.base && b + bytes <= rg.base + rg.bytes) {
+            *id = (int32_t)i;
+            *off = (int64_t)(b - rg.base);
+            return PR_OK;
+        }
+    }
+    *id = -1;
+    *off = 0;
+    return PR_OK;
+}
+
+size_t dtype_size(int32_t dt) { return dt == PR_DTYPE_F32 ? 4 : (dt == PR_DTYPE_BF16 ? 2 : 0); }
+
+int launch_ring(const LaunchArgs& a, int nranks, int32_t threads, int32_t channels, cudaStream_t s, bool coop) {
+    void* fn = (a.dtype == PR_DTYPE_F32) ? (void*)ring_kernel<float> : (void*)ring_kernel<__nv_bfloat16>;
+    void* args[] = {(void*)&a};
+    const dim3 grid((unsigned)channels, (unsigned)nranks), block((unsigned)threads);
+    if (coop) {
+        PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s));
+    } else {
+        PR_CUDA_TRY(cudaLaunchKernel(fn, grid, block, args, 0, s));
+    }
+    return PR_OK;
+}
+
+}  // namespace
+
+extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t device, pr_exchange_fn fn, void* ctx,
+                            const pr_comm_config* cfg) {
+    if (!out || !fn || P < 1 || P > PR_MAX_RANKS || rank < 0 || rank >= P || device < 0) return PR_ERR_INVALID;
+    pr_comm* c = new (std::nothrow) pr_comm();
+    if (!c) return PR_ERR_INTERNAL;
+    c->rank = rank; c->P = P; c->device = device; c->fn = fn; c->ctx = ctx;
+    c->cfg = cfg ? *cfg : default_config();
+    int rc = check_config(c->cfg);
+    if (!rc) rc = alloc_common(c);
+    Hello me;
+    std::memset(&me, 0, sizeof(me));
+    if (!rc) {
+        cudaError_t e = cudaIpcGetMemHandle(&me.handle, c->win);
+        if (e != cudaSuccess) { pr_internal_set_cuda_error(e, "cudaIpcGetMemHandle(window)"); rc = PR_ERR_CUDA; }
+    }
+    me.P = P; me.rank = rank; me.device = device; me.channels = c->cfg.channels; me.slots = c->cfg.slots;
+    me.threads = c->cfg.threads; me.slot_bytes = c->cfg.slot_bytes; me.window_bytes = (int64_t)c->tab.window_bytes;
+    me.bytes = rc ? 1 : 0;   // error flag travels with the hello so every rank fails together
+    std::vector<Hello> all(P);
+    int xrc = exchange(c, &me, sizeof(Hello), all.data());
+    if (xrc) { free_comm(c); return xrc; }
+    for (int q = 0; q < P; ++q) {
+        const Hello& h = all[q];
+        if (h.bytes) rc = rc ? rc : PR_ERR_CUDA;
+        if (h.P != P || h.rank != q || h.channels != me.channels || h.slots != me.slots || h.slot_bytes != me.slot_bytes ||
+            h.threads != me.threads)
+            rc = rc ? rc : PR_ERR_INVALID;
+    }
+    if (rc) { free_comm(c); return rc; }
+    for (int q = 0; q < P; ++q) {
+        if (q == rank) { c->tab.win[q] = c->win; continue; }
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, all[q].handle, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            pr_internal_set_cuda_error(e, "cudaIpcOpenMemHandle(window)");
+            rc = (e == cudaErrorPeerAccessUnsupported || e == cudaErrorInvalidDevice) ? PR_ERR_NO_P2P : PR_ERR_CUDA;
+            break;
+        }
+        c->opened.push_back((uint8_t*)p);
+        c->tab.win[q] = (uint8_t*)p;
+    }
+    if (!rc) rc = push_table(c);
+    // barrier: nobody signals into a window before every rank has mapped every window
+    int flag = rc ? 1 : 0;
+    std::vector<int> flags(P);
+    if (exchange(c, &flag, sizeof(int), flags.data())) rc = rc ? rc : PR_ERR_INVALID;
+    for (int q = 0; q < P; ++q) if (flags[q]) rc = rc ? rc : PR_ERR_CUDA;
+    if (rc) { free_comm(c); return rc; }
+    *out = c;
+    return PR_OK;
+}
+
+extern "C" int pr_comm_init_local(pr_comm** out, int32_t P, int32_t device, const pr_comm_config* cfg) {
+    if (!out || P < 1 || P > PR_MAX_RANKS || device < 0) return PR_ERR_INVALID;
+    const pr_comm_config cf = cfg ? *cfg : default_config();
+    if (int rc = check_config(cf)) return rc;
+    std::vector<pr_comm*> cs(P, nullptr);
+    int rc = PR_OK;
+    for (int r = 0; r < P && !rc; ++r) {
+        cs[r] = new (std::nothrow) pr_comm();
+        if (!cs[r]) { rc = PR_ERR_INTERNAL; break; }
+        cs[r]->rank = r; cs[r]->P = P; cs[r]->device = device; cs[r]->local = true; cs[r]->cfg = cf;
+        rc = alloc_common(cs[r]);
+    }
+    if (!rc) {
+        for (int r = 0; r < P; ++r) {
+            for (int q = 0; q < P; ++q) {
+                cs[r]->tab.win[q] = cs[q]->win;
+                cs[r]->tab.reg[0][q] = nullptr;   // local region 0: the whole address space, base 0
+            }
+            if ((rc = push_table(cs[r]))) break;
+        }
+    }
+    if (rc) {
+        for (auto* c : cs) free_comm(c);
+        return rc;
+    }
+    for (int r = 0; r < P; ++r) out[r] = cs[r];
+    return PR_OK;
+}
+
+extern "C" int pr_comm_register(pr_comm* c, void* d_buf, size_t bytes) {
+    if (!c || !d_buf || bytes == 0) return PR_ERR_INVALID;
+    if (c->local) return PR_OK;
+    if ((int)c->regs.size() >= PR_MAX_REGS) return PR_ERR_CAPACITY;
+    PR_CUDA_TRY(cudaSetDevice(c->device));
+    Hello me;
+    std::memset(&me, 0, sizeof(me));
+    int rc = PR_OK;
+    cudaError_t e = cudaIpcGetMemHandle(&me.handle, d_buf);
+    if (e != cudaSuccess) { pr_internal_set_cuda_error(e, "cudaIpcGetMemHandle(register)"); rc = PR_ERR_CUDA; }
+    me.rank = c->rank;
+    me.bytes = bytes;
+    me.P = rc;   // error travels with the message
+    std::vector<Hello> all(c->P);
+    if (exchange(c, &me, sizeof(Hello), all.data())) return PR_ERR_INVALID;
+    for (auto& h : all) if (h.P) rc = rc ? rc : h.P;
+    if (rc) return rc;
+    Reg rg;
+    rg.base = (uint8_t*)d_buf;
+    rg.bytes = bytes;
+    rg.peer.assign(c->P, nullptr);
+    for (int q = 0; q < c->P && !rc; ++q) {
+        if (q == c->rank) { rg.peer[q] = rg.base; continue; }
+        void* p = nullptr;
+        cudaError_t e2 = cudaIpcOpenMemHandle(&p, all[q].handle, cudaIpcMemLazyEnablePeerAccess);
+        if (e2 != cudaSuccess) { pr_internal_set_cuda_error(e2, "cudaIpcOpenMemHandle(register)"); rc = PR_ERR_CUDA; break; }
+        rg.peer[q] = (uint8_t*)p;
+    }
+    const int id = (int)c->regs.size();
+    c->regs.push_back(rg);
+    if (!rc) {
+        for (int q = 0; q < c->P; ++q) c->tab.reg[id][q] = rg.peer[q];
+        rc = push_table(c);
+    }
+    int flag = rc ? 1 : 0;
+    std::vector<int> flags(c->P);
+    if (exchange(c, &flag, sizeof(int), flags.data())) rc = rc ? rc : PR_ERR_INVALID;
+    for (int f : flags) if (f) rc = rc ? rc : PR_ERR_CUDA;
+    return rc;
+}
+
+extern "C" int pr_comm_alloc(pr_comm* c, size_t bytes, void** d_ptr) {
+    if (!c || !d_ptr || bytes == 0) return PR_ERR_INVALID;
+    PR_CUDA_TRY(cudaSetDevice(c->device));
+    void* p = nullptr;
+    PR_CUDA_TRY(cudaMalloc(&p, bytes));
+    PR_CUDA_TRY(cudaMemset(p, 0, bytes));
+    if (c->local) {
+        Reg rg;
+        rg.base = (uint8_t*)p; rg.bytes = bytes; rg.owned = true;
+        c->regs.push_back(rg);
+        *d_ptr = p;
+        return PR_OK;
+    }
+    int rc = pr_comm_register(c, p, bytes);
+    if (rc) { cudaFree(p); return rc; }
+    c->regs.back().owned = true;
+    *d_ptr = p;
+    return PR_OK;
+}
+
+extern "C" int pr_weighted_allreduce(pr_comm* c, void* d_buf, int64_t count, int32_t dt, int64_t n_local,
+                                     void* stream) {
+    if (!c || count < 0 || n_local < 0 || !dtype_size(dt) || (count > 0 && !d_buf)) return PR_ERR_INVALID;
+    if (((uintptr_t)d_buf & 15)) return PR_ERR_ALIGN;
+    if (int st = *(volatile int*)c->h_status) return st;
+    if (c->P == 1) return n_local > 0 ? PR_OK : PR_ERR_ZERO_SAMPLES;
+    LaunchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.count = count;
+    a.dtype = dt;
+    a.nranks = 1;
+    a.calls[0].tab = c->d_tab;
+    a.calls[0].buf = d_buf;
+    a.calls[0].n_local = n_local;
+    find_reg(c, d_buf, (size_t)count * dtype_size(dt), &a.calls[0].reg_id, &a.calls[0].reg_off);
+    return launch_ring(a, 1, c->cfg.threads, c->cfg.channels, (cudaStream_t)stream, false);
+}
+
+extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d_bufs, int64_t count, int32_t dt,
+                                           const int64_t* n_local, void* stream) {
+    if (!comms || !d_bufs || !n_local || count < 0 || !dtype_size(dt)) return PR_ERR_INVALID;
+    const pr_comm* c0 = comms[0];
+    if (!c0 || !c0->local) return PR_ERR_INVALID;
+    const int P = c0->P;
+    int64_t sumn = 0;
+    for (int r = 0; r < P; ++r) {
+        const pr_comm* c = comms[r];
+        if (!c || !c->local || c->rank != r || c->P != P || c->device != c0->device) return PR_ERR_INVALID;
+        if (n_local[r] < 0 || (count > 0 && !d_bufs[r])) return PR_ERR_INVALID;
+        if ((uintptr_t)d_bufs[r] & 15) return PR_ERR_ALIGN;
+        if (int st = *(volatile int*)c->h_status) return st;
+        sumn += n_local[r];
+    }
+    if (sumn <= 0) return PR_ERR_ZERO_SAMPLES;   // every n is visible here: fail before launching
+    if (P == 1) return PR_OK;
+    LaunchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.count = count;
+    a.dtype = dt;
+    a.nranks = P;
+    for (int r = 0; r < P; ++r) {
+        a.calls[r].tab = comms[r]->d_tab;
+        a.calls[r].buf = d_bufs[r];
+        a.calls[r].n_local = n_local[r];
+        find_reg(comms[r], d_bufs[r], 0, &a.calls[r].reg_id, &a.calls[r].reg_off);
+    }
+    PR_CUDA_TRY(cudaSetDevice(c0->device));
+    return launch_ring(a, P, c0->cfg.threads, c0->cfg.channels, (cudaStream_t)stream, true);
+}
+
+extern "C" int pr_comm_allgather_f64(pr_comm* c, double local, double* out, void* stream) {
+    if (!c || !out || c->local) return PR_ERR_INVALID;
+    if (int st = *(volatile int*)c->h_status) return st;
+    if (c->P == 1) { out[0] = local; return PR_OK; }
+    PR_CUDA_TRY(cudaSetDevice(c->device));
+    double* d_out = nullptr;
+    PR_CUDA_TRY(cudaHostGetDevicePointer((void**)&d_out, c->h_ag, 0));
+    c->ag_seq += 1;
+    allgather_f64_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->d_tab, c->ag_seq, local, d_out);
+    PR_CUDA_TRY(cudaGetLastError());
+    PR_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    if (int st = *(volatile int*)c->h_status) return st;
+    for (int q = 0; q < c->P; ++q) out[q] = ((volatile double*)c->h_ag)[q];
+    return PR_OK;
+}
+
+extern "C" int pr_comm_status(pr_comm* c) {
+    if (!c) return PR_ERR_INVALID;
+    return *(volatile int*)c->h_status;
+}
+
+extern "C" int pr_comm_timestamps(pr_comm* c, int64_t* out) {
+    if (!c || !out) return PR_ERR_INVALID;
+    for (int i = 0; i < 3; ++i) out[i] = ((volatile long long*)c->h_stamps)[i];
+    return PR_OK;
+}
+
+extern "C" int pr_comm_rank(const pr_comm* c, int32_t* rank, int32_t* size) {
+    if (!c) return PR_ERR_INVALID;
+    if (rank) *rank = c->rank;
+    if (size) *size = c->P;
+    return PR_OK;
+}
+
+extern "C" void pr_comm_destroy(pr_comm* c) {
+    if (!c) return;
+    if (!c->local && c->fn && c->P > 1) {   // collective: nobody unmaps while a peer may still signal
+        cudaSetDevice(c->device);
+        cudaDeviceSynchronize();
+        int flag = 0;
+        std::vector<int> flags(c->P);
+        exchange(c, &flag, sizeof(int), flags.data());
+    }
+    free_comm(c);
+}
+
+// ---- misc ABI ----------------------------------------------------------------------------------------
+extern "C" const char* pr_strerror(int code) {
+    switch (code) {
+        case PR_OK: return "ok";
+        case PR_ERR_INVALID: return "invalid argument";
+        case PR_ERR_INFEASIBLE_FLOOR: return "infeasible floor (C < P*floor)";
+        case PR_ERR_DATASET_TOO_SMALL: return "dataset too small (N < g*C)";
+        case PR_ERR_ZERO_TIMING: return "zero/invalid step timing";
+        case PR_ERR_CUDA: return "CUDA error";
+        case PR_ERR_ALIGN: return "misaligned pointer or row size";
+        case PR_ERR_NO_P2P: return "no peer access between GPUs";
+        case PR_ERR_LENGTH_MISMATCH: return "ranks disagree on count/dtype";
+        case PR_ERR_ZERO_SAMPLES: return "sum of n_local is zero";
+        case PR_ERR_PEER_TIMEOUT: return "peer timeout (watchdog)";
+        case PR_ERR_CAPACITY: return "capacity too small";
+        case PR_ERR_INTERNAL: return "internal error";
+        default: return "unknown error";
+    }
+}
+
+extern "C" int pr_version(void) { return PR_VERSION; }

@@ -1,0 +1,180 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/propring.h declares, and its
+host control plane (pr_alloc_*) is bit-exact against the oracle (SURVEY §4 tier T1)."""
+
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2111_08272_b200 as pr
+from paper_2111_08272_b200 import _lib
+from oracle import allocation as A
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "propring.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(pr_[a-z0-9_]+)\s*\(", txt)) - {"pr_exchange_fn"})
+
+
+def test_library_exports_every_declared_symbol():
+    syms = _declared_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(_lib.LIB, s), s
+        assert s in _lib.SIGNATURES, f"binding lacks {s}"
+    assert pr.version() == 10000
+
+
+def test_library_is_built_for_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_strerror_codes():
+    for code in range(0, -13, -1):
+        assert _lib.LIB.pr_strerror(code)
+
+
+def _oracle_view(a):
+    return {"w": a.w, "n": a.n, "len": a.len, "off": a.off, "S": a.S, "B": a.B}
+
+
+def _lib_view(v):
+    return {k: v[k] for k in ("w", "n", "len", "off", "S", "B")}
+
+
+@pytest.mark.parametrize("N,ratios,C,g", [
+    (1000, [1, 3], 4, 25), (50000, [1, 2], 3, 128), (51200, [1, 1, 1, 1], 64, 16),
+    (50000, [1, 1, 1, 1, 2, 2, 4, 4], 64, 16), (50000, [4, 1, 1, 1, 2, 2, 4, 4], 64, 16),
+    (50000, [1, 1, 1, 2, 2, 4, 4], 256, 4), (1281167, [1.0, 2.5, 0.7, 3.3], 1000, 3)])
+def test_init_configs_bit_exact(N, ratios, C, g):
+    o = A.alloc_init(N, ratios, C=C, g=g)
+    l = pr.alloc_init(N, ratios, C=C, g=g).view()
+    assert _lib_view(l) == _oracle_view(o)
+
+
+def test_init_errors_match():
+    with pytest.raises(pr.PropringError) as e:
+        pr.alloc_init(100, [1, 1, 1], C=2)
+    assert e.value.code == pr.PR_ERR_INFEASIBLE_FLOOR
+    with pytest.raises(pr.PropringError) as e:
+        pr.alloc_init(10, [1, 1], C=20)
+    assert e.value.code == pr.PR_ERR_DATASET_TOO_SMALL
+    for bad in ([1, -1], [1, float("nan")], [1, float("inf")]):
+        with pytest.raises(pr.PropringError) as e:
+            pr.alloc_init(10, bad, C=2)
+        assert e.value.code == pr.PR_ERR_INVALID
+    with pytest.raises(pr.PropringError):
+        pr.alloc_init(10, [1.5, 1], C=0)
+
+
+def test_random_init_and_trajectories_bit_exact():
+    """10^4 random (N, P, ratios, C, g, floor) and controller sequences: identical integers."""
+    rng = np.random.Generator(np.random.PCG64(2024))
+    n_cases = 0
+    for case in range(10000):
+        P = int(rng.integers(1, 17))
+        floor = int(rng.integers(0, 3))
+        C = int(rng.integers(max(P * floor, 1), 4 * P + 60))
+        g = int(rng.integers(1, 9))
+        N = int(g * C * rng.integers(1, 40) + rng.integers(0, 1000))
+        kind = case % 3
+        ratios = (rng.integers(1, 9, P).astype(float) if kind == 0 else rng.uniform(0.05, 5.0, P))
+        try:
+            o = A.alloc_init(N, list(ratios), C=C, g=g, floor=floor)
+        except (A.InfeasibleFloor, A.DatasetTooSmall, ValueError):
+            with pytest.raises(pr.PropringError):
+                pr.alloc_init(N, list(ratios), C=C, g=g, floor=floor)
+            continue
+        l = pr.alloc_init(N, list(ratios), C=C, g=g, floor=floor)
+        assert _lib_view(l.view()) == _oracle_view(o), (N, ratios, C, g, floor)
+        if case % 10:
+            continue
+        for ep in range(6):
+            mode = rng.integers(0, 4)
+            if mode == 0:
+                t = rng.uniform(0.1, 10.0, P)
+            elif mode == 1:
+                t = np.full(P, 2.5)                                  # ties
+            elif mode == 2:
+                t = np.array(o.w, dtype=float) * rng.uniform(0.5, 2.0, P)   # linear costs
+            else:
+                t = rng.uniform(0.1, 10.0, P)
+                t[rng.integers(0, P)] = [0.0, -1.0, float("nan"), float("inf")][ep % 4]
+            try:
+                ch_o = A.alloc_update(o, list(t))
+                err_o = None
+            except A.ZeroTiming:
+                err_o = pr.PR_ERR_ZERO_TIMING
+            if err_o is None:
+                ch_l = l.update(list(t))
+                assert ch_l == ch_o
+            else:
+                with pytest.raises(pr.PropringError) as e:
+                    l.update(list(t))
+                assert e.value.code == err_o
+            v = l.view()
+            assert _lib_view(v) == _oracle_view(o) and v["frozen"] == o.frozen and v["epoch"] == o.epoch
+            assert v["hist_len"] == len(o.history)
+        n_cases += 1
+    assert n_cases > 300
+
+
+def test_controller_spec_examples_via_library():
+    a = pr.alloc_init(10 ** 6, [10, 10], C=20)
+    a.update([2.0, 1.0])
+    assert a.view()["w"] == [7, 13]
+    a = pr.alloc_init(10 ** 6, [10, 10, 10], C=30)
+    a.update([1.0, 2.0, 5.0])
+    assert a.view()["w"] == [18, 9, 3]
+
+
+def test_policy_and_ema_match_oracle():
+    rng = np.random.Generator(np.random.PCG64(77))
+    for _ in range(200):
+        P = int(rng.integers(2, 9))
+        o = A.alloc_init(10 ** 6, [1] * P, C=64)
+        l = pr.alloc_init(10 ** 6, [1] * P, C=64)
+        al = float(rng.choice([1.0, 0.5, 0.3]))
+        o.ema_alpha, o.never_freeze, o.window, o.tol = al, True, 3, 0
+        l.set_policy(window=3, tol=0, never_freeze=True, ema_alpha=al)
+        for _ in range(5):
+            t = list(rng.uniform(0.5, 3.0, P))
+            A.alloc_update(o, t)
+            l.update(t)
+            assert l.view()["w"] == o.w
+    with pytest.raises(pr.PropringError):
+        l.set_policy(window=1)
+
+
+def test_save_load_roundtrip_resumes_identically():
+    a = pr.alloc_init(51200, [1, 1, 1, 1], C=64, g=16)
+    a.set_policy(ema_alpha=0.5, never_freeze=True)
+    a.update([2.0, 2.0, 1.0, 1.0])
+    b = pr.Alloc.load(a.save())
+    assert b.view() == a.view()
+    assert [b.history(k) for k in range(2)] == [a.history(k) for k in range(2)]
+    for t in ([2.0, 2.1, 1.0, 0.9], [1.0, 1.0, 1.0, 1.0]):
+        a.update(t)
+        b.update(t)
+        assert a.view() == b.view()
+    with pytest.raises(pr.PropringError):
+        pr.Alloc.load(b"garbage" * 20)
+
+
+def test_frozen_update_is_noop():
+    a = pr.alloc_init(10 ** 6, [10, 10], C=20)
+    cost = [1e-3, 2e-3]
+    for _ in range(5):
+        w = a.view()["w"]
+        a.update([w[0] * cost[0], w[1] * cost[1]])
+    v = a.view()
+    assert v["frozen"] and v["w"] == [13, 7]
+    assert a.update([1.0, 100.0]) is False and a.view() == v

@@ -1,0 +1,256 @@
+"""GPU parity of K3, the sample-count-weighted ring allreduce, through the C ABI.
+
+All P ranks run on the one test GPU (pr_comm_init_local: same kernel, same flag/credit protocol, peer
+memory = local memory).  Checks:
+  * bit-identical to the oracle's ring-order replay (oracle/ring_emu.c) — catches any chunk, offset,
+    order or rounding bug;
+  * within the north-star tolerance of the fp64 weighted mean (1e-5 fp32, 2e-2 bf16), with the
+    cancellation-aware metric of DESIGN.md §3 #16;
+  * equal weights vs torch's mean (library routine); n_r = 0 contributes nothing, even NaN;
+  * back-to-back calls (monotone counters), direct and staged all-gather, error latching.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import gather as OG
+from oracle import wavg as W
+
+pytestmark = pytest.mark.gpu
+pr = pytest.importorskip("paper_2111_08272_b200")
+
+TOL = {"f32": 1e-5, "bf16": 2e-2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+_GROUPS = {}
+
+
+def group(P, **cfg):
+    key = (P, tuple(sorted(cfg.items())))
+    if key not in _GROUPS:
+        _GROUPS[key] = pr.comm_init_local(P, 0, pr.comm_config(watchdog_ns=5_000_000_000, **cfg))
+    return _GROUPS[key]
+
+
+def _inputs(P, L, dtype, kind="gaussian", seed=0):
+    g32 = synth.gradients(P, L, seed_base=1000 + seed, kind=kind)
+    if dtype == "bf16":
+        host = OG.f32_to_bf16_bits(g32)
+        dev = [torch.from_numpy(host[r].view(np.int16).copy()).cuda().view(torch.bfloat16) for r in range(P)]
+    else:
+        host = g32
+        dev = [torch.from_numpy(g32[r].copy()).cuda() for r in range(P)]
+    return host, dev
+
+
+def _result_host(t, dtype):
+    return t.view(torch.int16).cpu().numpy().view(np.uint16) if dtype == "bf16" else t.cpu().numpy()
+
+
+def _check(P, L, dtype, n, comms, kind="gaussian", seed=0, stream=None):
+    host, dev = _inputs(P, L, dtype, kind, seed)
+    pr.weighted_allreduce_local(comms, dev, n, stream=stream)
+    torch.cuda.synchronize()
+    for c in comms:
+        assert c.status() == 0
+    emu = W.ring_emulate(host, n, dtype)
+    ref, den = W.weighted_average(W.as_f64(host, dtype), n)
+    outs = [_result_host(d, dtype) for d in dev]
+    for r in range(P):
+        assert np.array_equal(outs[r].view(np.uint8), emu.view(np.uint8)), f"rank {r} differs from ring replay"
+    err, zb = W.error_metric(W.as_f64(outs[0], dtype), ref, den)
+    assert zb == 0 and err <= TOL[dtype], err
+    return outs
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 7, 8])
+def test_counts_and_weights(P, dtype):
+    comms = group(P)
+    rng = np.random.Generator(np.random.PCG64(P))
+    for L in (1, 7, P, P + 1, 1000, 4099, 2 ** 20 + 3):
+        for wkind in ("equal", "skewed", "zero"):
+            if wkind == "equal":
+                n = [256] * P
+            elif wkind == "skewed":
+                n = [int(x) * 64 for x in rng.integers(1, 9, P)]
+            else:
+                n = [int(x) * 16 for x in rng.integers(1, 5, P)]
+                n[int(rng.integers(0, P))] = 0
+            _check(P, L, dtype, n, comms, kind="mixed" if L % 2 else "gaussian", seed=L)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_large_buffer_64MiB(P):
+    comms = group(P)
+    L = 64 * 2 ** 20 // 4
+    n = [int(x) for x in [64, 64, 64, 64, 128, 128, 256, 256][:P]]
+    _check(P, L, "f32", n, comms)
+
+
+def test_resnet18_size_sampled_parity_against_oracle():
+    """Full-size C2/C4 gradient (11,689,512 fp32) at P=8: ring replay on every element."""
+    P = 8
+    comms = group(P)
+    _check(P, 11_689_512, "f32", [64, 64, 64, 64, 128, 128, 256, 256], comms)
+
+
+def test_equal_weights_match_torch_mean():
+    P, L = 4, 100_003
+    comms = group(P)
+    host, dev = _inputs(P, L, "f32")
+    mean = torch.stack(dev).double().mean(0)
+    pr.weighted_allreduce_local(comms, dev, [32] * P)
+    torch.cuda.synchronize()
+    den = torch.stack(dev).double().abs().sum(0) / P + 1e-300
+    assert float(((dev[0].double() - mean).abs() / den).max()) <= 1e-5
+
+
+def test_power_of_two_equal_weights_is_scaled_sum_bit_exact():
+    P, L = 8, 333_333
+    comms = group(P)
+    host, dev = _inputs(P, L, "f32", seed=5)
+    pr.weighted_allreduce_local(comms, dev, [10] * P)
+    torch.cuda.synchronize()
+    cs = W.chunk_elems(L, P, 4)
+    plain = np.zeros(L, dtype=np.float32)
+    for c in range(P):
+        lo, hi = c * cs, min((c + 1) * cs, L)
+        acc = host[c, lo:hi].copy()
+        for h in range(1, P):
+            acc = (acc + host[(c + h) % P, lo:hi]).astype(np.float32)
+        plain[lo:hi] = acc
+    assert np.array_equal(dev[3].cpu().numpy(), plain * np.float32(1 / 8))
+
+
+def test_zero_sample_rank_with_nan_does_not_propagate():
+    P, L = 4, 10_000
+    comms = group(P)
+    host, dev = _inputs(P, L, "f32")
+    dev[2].fill_(float("nan"))
+    host[2, :] = np.nan
+    n = [10, 20, 0, 30]
+    pr.weighted_allreduce_local(comms, dev, n)
+    torch.cuda.synchronize()
+    out = dev[2].cpu().numpy()
+    assert np.all(np.isfinite(out))
+    assert np.array_equal(out, W.ring_emulate(host, n, "f32"))
+
+
+def test_identity_P1_and_zero_samples_error():
+    comms = group(1)
+    x = torch.randn(1000, device="cuda")
+    y = x.clone()
+    pr.weighted_allreduce_local(comms, [x], [5])
+    assert torch.equal(x, y)
+    with pytest.raises(pr.PropringError) as e:
+        pr.weighted_allreduce_local(comms, [x], [0])
+    assert e.value.code == pr.PR_ERR_ZERO_SAMPLES
+
+
+def test_all_zero_samples_latches_error_and_leaves_buffers():
+    comms = pr.comm_init_local(3, 0, pr.comm_config(watchdog_ns=2_000_000_000))
+    host, dev = _inputs(3, 5000, "f32")
+    before = [d.clone() for d in dev]
+    with pytest.raises(pr.PropringError):
+        pr.weighted_allreduce_local(comms, dev, [0, 0, 0])   # host-side check
+    for c in comms:
+        c.destroy()
+
+
+def test_back_to_back_calls_and_streams():
+    """Many calls in a row (monotone counters, parity-double-buffered handshake), different sizes."""
+    P = 5
+    comms = group(P)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for it, L in enumerate([10, 100_000, 3, 77_777, 1_000_000, 5, 12_345]):
+            _check(P, L, "f32" if it % 2 else "bf16", [it + 1, 2, 3, 4 * it, 5], comms, seed=it, stream=s)
+
+
+def test_staged_allgather_path():
+    for P in (2, 3, 8):
+        comms = group(P, force_staged=True)
+        for L in (5, 4099, 2 ** 20 + 3):
+            _check(P, L, "f32", [1 + r for r in range(P)], comms, seed=L)
+            _check(P, L, "bf16", [3] * P, comms, seed=L)
+
+
+@pytest.mark.parametrize("cfg", [dict(channels=1, slots=2, slot_bytes=256), dict(channels=3, slots=3, slot_bytes=4096),
+                                 dict(channels=32, slots=8, slot_bytes=65536, threads=256)])
+def test_config_variants(cfg):
+    for P in (2, 5):
+        comms = group(P, **cfg)
+        for L in (1, 999, 300_001):
+            _check(P, L, "f32", [7] * (P - 1) + [1], comms, seed=L)
+
+
+def test_cuda_graph_replay():
+    """Device-resident counters make the call capturable: replaying the graph gives the same result."""
+    P, L = 4, 50_000
+    comms = group(P)
+    host, dev = _inputs(P, L, "f32", seed=9)
+    src = [d.clone() for d in dev]
+    n = [1, 2, 3, 4]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        pr.weighted_allreduce_local(comms, dev, n, stream=s)   # warm-up outside capture
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            pr.weighted_allreduce_local(comms, dev, n, stream=s)
+    emu = W.ring_emulate(host, n, "f32")
+    for _ in range(3):
+        for d, s0 in zip(dev, src):
+            d.copy_(s0)
+        g.replay()
+        torch.cuda.synchronize()
+        for d in dev:
+            assert np.array_equal(d.cpu().numpy(), emu)
+
+
+def test_length_mismatch_and_timeout_latch():
+    """Per-rank launches of a local group on separate streams: count mismatch -> LENGTH_MISMATCH on
+    every rank with buffers untouched; a missing peer -> PEER_TIMEOUT."""
+    P = 2
+    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, watchdog_ns=1_000_000_000))
+    a = torch.randn(1000, device="cuda")
+    b = torch.randn(1000, device="cuda")
+    a0, b0 = a.clone(), b.clone()
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    pr.weighted_allreduce(comms[0], a, 1, stream=s0, count=1000)
+    pr.weighted_allreduce(comms[1], b, 1, stream=s1, count=999)
+    torch.cuda.synchronize()
+    assert comms[0].status() == pr.PR_ERR_LENGTH_MISMATCH and comms[1].status() == pr.PR_ERR_LENGTH_MISMATCH
+    assert torch.equal(a, a0) and torch.equal(b, b0)
+    for c in comms:
+        c.destroy()
+    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, watchdog_ns=300_000_000))
+    pr.weighted_allreduce(comms[0], a, 1, stream=s0)
+    torch.cuda.synchronize()
+    assert comms[0].status() == pr.PR_ERR_PEER_TIMEOUT
+    with pytest.raises(pr.PropringError) as e:
+        pr.weighted_allreduce(comms[0], a, 1, stream=s0)
+    assert e.value.code == pr.PR_ERR_PEER_TIMEOUT
+    for c in comms:
+        c.destroy()
+
+
+def test_timestamps_and_status():
+    P = 3
+    comms = group(P)
+    host, dev = _inputs(P, 1 << 20, "f32")
+    pr.weighted_allreduce_local(comms, dev, [1, 2, 3])
+    torch.cuda.synchronize()
+    for c in comms:
+        t = c.timestamps()
+        assert 0 < t[0] <= t[1] <= t[2]

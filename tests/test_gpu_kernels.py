@@ -1,0 +1,188 @@
+"""GPU parity: K1 sharder, K2 gather, K4 spin, called through the C ABI, against the CPU oracle.
+
+Bar: bit-exact for indices and gathered bytes (integer / byte work, and the affine
+conversion whose definition fixes every rounding).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import allocation as A
+from oracle import gather as OG
+from oracle import permutation as PM
+
+pytestmark = pytest.mark.gpu
+
+pr = pytest.importorskip("paper_2111_08272_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+# ---------------------------------------------------------------- K1 ----------------------------
+
+def test_philox_device_matches_kat_oracle_and_curand():
+    rng = np.random.Generator(np.random.PCG64(1))
+    ctr = rng.integers(0, 2 ** 32, (4096, 4), dtype=np.uint64).astype(np.uint32)
+    ctr[0] = 0
+    ctr[1] = 0xFFFFFFFF
+    ctr[2] = [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344]
+    for key in (0, 0xFFFFFFFFFFFFFFFF, 0x299F31D0A4093822, 1234567):
+        d = _dev(ctr.view(np.int32))
+        mine = torch.empty(ctr.size, dtype=torch.int32, device="cuda")
+        cur = torch.empty_like(mine)
+        pr.test_philox(d, key, False, mine)
+        pr.test_philox(d, key, True, cur)
+        torch.cuda.synchronize()
+        m = mine.cpu().numpy().view(np.uint32).reshape(-1, 4)
+        c = cur.cpu().numpy().view(np.uint32).reshape(-1, 4)
+        assert np.array_equal(m, c)                           # library routine (cuRAND)
+        o = np.stack(PM.philox4x32_10(tuple(ctr[:, j] for j in range(4)), (key & 0xFFFFFFFF, key >> 32)), 1)
+        assert np.array_equal(m, o)                           # oracle
+    # published KAT through the device function
+    d = _dev(np.array([[0, 0, 0, 0]], dtype=np.uint32).view(np.int32))
+    out = torch.empty(4, dtype=torch.int32, device="cuda")
+    pr.test_philox(d, 0, False, out)
+    assert out.cpu().numpy().view(np.uint32).tolist() == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 10, 1000, 50000, 1281167, 2 ** 24])
+def test_permute_bit_exact(N):
+    rng = np.random.Generator(np.random.PCG64(N))
+    for _ in range(3 if N < 2 ** 20 else 1):
+        seed = int(rng.integers(0, 2 ** 63)) * 2 + int(rng.integers(0, 2))
+        ep = int(rng.integers(0, 2 ** 40))
+        out = torch.empty(N, dtype=torch.int64, device="cuda")
+        pr.permute(N, seed, ep, 0, N, out)
+        got = out.cpu().numpy()
+        if N <= 2 ** 21:
+            assert np.array_equal(got, PM.permute(np.arange(N), N, seed, ep))
+        else:   # full size: sampled positions one by one + the bijection property
+            pos = rng.integers(0, N, 20000)
+            assert np.array_equal(got[pos], PM.permute(pos, N, seed, ep))
+        assert np.array_equal(np.sort(got), np.arange(N))
+
+
+def test_permute_subrange_and_edges():
+    N = 12345
+    full = torch.empty(N, dtype=torch.int64, device="cuda")
+    pr.permute(N, 9, 4, 0, N, full)
+    part = torch.empty(1000, dtype=torch.int64, device="cuda")
+    pr.permute(N, 9, 4, 11345, 1000, part)
+    assert torch.equal(full[11345:], part)
+    pr.permute(N, 9, 4, 5, 0, part)          # empty range: no-op
+    with pytest.raises(pr.PropringError):
+        pr.permute(N, 9, 4, 12000, 1000, part)
+
+
+@pytest.mark.parametrize("N,ratios,C,g", [(1000, [1, 3], 4, 25), (50000, [1, 2], 3, 128),
+                                          (51200, [1, 1, 1, 1], 64, 16), (50000, [1, 1, 1, 1, 2, 2, 4, 4], 64, 16),
+                                          (1281167, [3, 1, 4, 1, 5], 14, 2)])
+def test_shard_indices_bit_exact(N, ratios, C, g):
+    a = pr.alloc_init(N, ratios, C=C, g=g)
+    o = A.alloc_init(N, ratios, C=C, g=g)
+    for epoch in (0, 1, 7):
+        seen = []
+        for r in range(len(ratios)):
+            out = torch.empty(o.len[r], dtype=torch.int64, device="cuda")
+            pr.shard_indices(a, r, epoch, 1234, out)
+            got = out.cpu().numpy()
+            assert np.array_equal(got, PM.shard_indices(N, o.off[r], o.len[r], 1234, epoch))
+            seen.append(got)
+        allv = np.concatenate(seen)
+        assert np.array_equal(np.sort(allv), np.arange(N))
+    small = torch.empty(o.len[0] - 1, dtype=torch.int64, device="cuda")
+    with pytest.raises(pr.PropringError) as e:
+        pr.shard_indices(a, 0, 0, 1, small)
+    assert e.value.code == pr.PR_ERR_CAPACITY
+
+
+# ---------------------------------------------------------------- K2 ----------------------------
+
+MEAN = [123.675, 116.28, 103.53]
+STD = [58.395, 57.12, 57.375]
+
+
+@pytest.mark.parametrize("row_bytes,plane", [(16, 16), (48, 16), (48, 8), (3072, 1024), (150528, 50176)])
+@pytest.mark.parametrize("n", [0, 1, 31, 32, 33, 4096])
+def test_gather_bit_exact(row_bytes, plane, n):
+    if row_bytes == 150528 and n == 4096:
+        n = 300
+    nsrc = max(64, n // 2)
+    channels = row_bytes // plane
+    rng = np.random.Generator(np.random.PCG64(row_bytes + n))
+    X = rng.integers(0, 256, (nsrc, row_bytes), dtype=np.uint8)
+    Y = rng.integers(0, 1000, nsrc, dtype=np.int64)
+    idx = rng.integers(0, nsrc, n, dtype=np.int64)
+    scale = np.array([1.0 / STD[c % 3] for c in range(channels)], dtype=np.float32)
+    shift = np.array([MEAN[c % 3] for c in range(channels)], dtype=np.float32)
+    dX, dY, didx = _dev(X), _dev(Y), _dev(idx)
+    for op in (pr.GATHER_COPY, pr.GATHER_U8_TO_F32_AFFINE, pr.GATHER_U8_TO_BF16_AFFINE):
+        width = {0: 1, 1: 4, 2: 2}[op]
+        out = torch.full((max(n, 1) * row_bytes * width,), 0x5A, dtype=torch.uint8, device="cuda")
+        lab = torch.full((max(n, 1),), -7, dtype=torch.int64, device="cuda")
+        gop = pr.make_gather_op(op, scale, shift, plane)
+        pr.gather_rows(dX, nsrc, row_bytes, didx, n, out, gop, dY, lab)
+        torch.cuda.synchronize()
+        if n == 0:
+            assert int((out != 0x5A).sum()) == 0
+            continue
+        ref, rlab = OG.gather_rows(X, idx, op, scale, shift, plane, Y=Y)
+        assert np.array_equal(out.cpu().numpy(), np.ascontiguousarray(ref).view(np.uint8).reshape(-1))
+        assert np.array_equal(lab.cpu().numpy(), rlab)
+
+
+def test_gather_step_slices_of_a_shard_and_alignment_errors():
+    X = synth.images_u8(2000, seed=0).reshape(2000, -1)
+    a = pr.alloc_init(2000, [1, 2], C=3, g=16)
+    v = a.view()
+    idx = torch.empty(v["len"][1], dtype=torch.int64, device="cuda")
+    pr.shard_indices(a, 1, 3, 99, idx)
+    dX = _dev(X)
+    n = v["n"][1]
+    out = torch.empty((n, 3072), dtype=torch.bfloat16, device="cuda")
+    scale = [1 / s for s in STD]
+    gop = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE, scale, MEAN, 1024)
+    for s in range(v["S"]):
+        pr.gather_rows(dX, 2000, 3072, idx[s * n:], n, out, gop)
+        ref, _ = OG.step_gather(X, idx.cpu().numpy(), s, n, op=OG.U8_TO_BF16_AFFINE,
+                                scale=np.float32(scale), shift=np.float32(MEAN), plane=1024)
+        assert np.array_equal(out.view(torch.int16).cpu().numpy().view(np.uint16), ref)
+    with pytest.raises(pr.PropringError) as e:
+        pr.gather_rows(dX, 2000, 3000, idx, 1, out)
+    assert e.value.code == pr.PR_ERR_ALIGN
+
+
+def test_gather_from_mapped_host_memory():
+    """The e2e path: rows read straight from pinned host memory over PCIe."""
+    X = synth.images_u8(512, seed=5).reshape(512, -1)
+    hX = torch.from_numpy(X).pin_memory()
+    idx = torch.randint(0, 512, (100,), dtype=torch.int64).cuda()
+    out = torch.empty((100, 3072), dtype=torch.uint8, device="cuda")
+    ptr = hX.data_ptr()   # UVA: pinned host memory is addressable from the device
+    pr.gather_rows(ptr, 512, 3072, idx, 100, out)
+    assert torch.equal(out.cpu(), hX[idx.cpu()])
+
+
+# ---------------------------------------------------------------- K4 ----------------------------
+
+def test_spin_duration():
+    torch.cuda.synchronize()
+    for ns in (50_000, 1_000_000):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        pr.spin(ns)
+        e.record()
+        e.synchronize()
+        ms = s.elapsed_time(e)
+        assert ns / 1e6 * 0.99 <= ms <= ns / 1e6 * 1.10 + 0.02

@@ -1,0 +1,131 @@
+"""World-size-2 tests of the N>1 path.
+
+CPU (gloo, runs here): the replicated control plane — every rank computes the same allocation from the
+same t_s allgather, shards are disjoint and cover the data set, and the byte-exchange callback that
+bootstraps pr_comm_init (CUDA-IPC handle allgather) is a correct rank-ordered allgather.
+GPU (marked): two processes on the one test GPU bootstrap a real pr_comm_init over CUDA IPC and run
+the weighted allreduce (needs the two contexts to be co-resident; skipped if the box cannot).
+"""
+
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _cpu_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2111_08272_b200 as pr
+        from oracle import allocation as A
+        from oracle import permutation as PM
+
+        # exchange callback = rank-ordered byte allgather
+        fn = pr.torch_exchange()
+        send = (b"rank%d-" % rank) * 3
+        recv = ctypes.create_string_buffer(len(send) * world)
+        rc = fn(None, ctypes.cast(ctypes.c_char_p(send), ctypes.c_void_p), len(send), ctypes.addressof(recv))
+        assert rc == 0
+        assert recv.raw == b"".join((b"rank%d-" % r) * 3 for r in range(world))
+
+        # replicated controller: per-rank measured times -> allgather -> identical update everywhere
+        a = pr.alloc_init(51200, [1] * world, C=64, g=16)
+        speeds = [1000.0, 2000.0]
+        for epoch in range(6):
+            v = a.view()
+            t_local = torch.tensor([v["S"] * v["n"][rank] / speeds[rank] + 0.01], dtype=torch.float64)
+            allt = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(allt, t_local)
+            a.update([float(x) for x in allt])
+        w = torch.tensor(a.view()["w"])
+        ws = [torch.zeros_like(w) for _ in range(world)]
+        dist.all_gather(ws, w)
+        assert all(torch.equal(ws[0], x) for x in ws)
+        v = a.view()
+        assert sum(v["w"]) == 64 and v["w"][1] > v["w"][0]
+        # each rank derives only its own shard; together they partition the data set
+        mine = PM.shard_indices(v["N"], v["off"][rank], v["len"][rank], 7, 3)
+        parts = [None] * world
+        dist.all_gather_object(parts, mine.tolist())
+        allv = np.concatenate([np.asarray(p, dtype=np.int64) for p in parts])
+        assert np.array_equal(np.sort(allv), np.arange(v["N"]))
+        q.put((rank, "ok"))
+    except Exception as e:  # report to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_control_plane():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_cpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in ps)
+    for p in ps:
+        p.join(60)
+    assert res == {0: "ok", 1: "ok"}, res
+
+
+def _gpu_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2111_08272_b200 as pr
+        import synth
+        from oracle import wavg as W
+
+        torch.cuda.set_device(0)
+        comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=2, watchdog_ns=30_000_000_000))
+        L = 4099
+        g = synth.gradients(world, L, seed_base=11)
+        buf = comm.alloc(L * 4, dtype=torch.float32)
+        buf.copy_(torch.from_numpy(g[rank]))
+        n = [3, 5]
+        pr.weighted_allreduce(comm, buf, n[rank])
+        torch.cuda.synchronize()
+        st = comm.status()
+        ok = st == 0 and np.array_equal(buf.cpu().numpy(), W.ring_emulate(g, n, "f32"))
+        t = comm.allgather_f64(1.5 + rank)
+        ok = ok and t == [1.5, 2.5]
+        dist.barrier()
+        comm.destroy()
+        q.put((rank, "ok" if ok else f"bad status={st}"))
+    except Exception as e:
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_ipc_two_processes_one_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(60)
+    assert res == {0: "ok", 1: "ok"}, res
