@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the proportional-allocation + weighted-ring-allreduce training path (arXiv 2111.08272).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N ...
+
+A "step" is ONE EPOCH of Algorithm 1 — the unit at which the paper re-allocates and the
+unit of the metric "epoch time at 1/2/4/8 B200" (BASELINE.json) — and it runs every row of
+SURVEY §8(a): controller update + allgather of t_s (a10, a5), per-epoch shard (a2, K1), then S
+aggregation steps of gather (a3, K2) -> ResNet-18 forward/backward with gradient accumulation (a4)
+-> weighted ring allreduce of the 11,689,512-element fp32 gradient (a6-a8, K3; identity at N=1) ->
+SGD (a9).  Workload: CIFAR-10-shaped synthetic data 50,000×3×32×32 u8 resident in HBM (153.6 MB >
+L2 126 MB, so every epoch streams it from HBM), global batch B = 1024 (g = 16, C = 64) split by the
+allocation; strong scaling across N.
+
+value   = whole-job samples/s over the K timed epochs (device time, CUDA events, max over ranks)
+e2e     = the same with the data set in pinned HOST memory: the gather reads every sampled row over
+          PCIe inside the timed region, and every step's loss is read back to the host
+roofline= the library's dominant kernel in the timed region (K2 at N=1, K3 at N>1), achieved
+          algorithmic bytes / live CUDA-event duration vs the measured peak
+cpu_baseline / --impl reference: the CPU oracle (oracle/) + a torch-CPU forward/backward on a bounded
+          sample of one aggregation step, on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "epoch throughput (samples/s; epoch time = S·B/value) of the proportional-allocation + weighted-ring-allreduce training step"
+N_DATA, G_UNIT, C_UNITS = 50_000, 16, 64
+ROW_BYTES = 3 * 32 * 32
+L_RESNET18 = 11_689_512
+NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction (900 nominal)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-epochs", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-colocated", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.lines = device, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2111_08272_b200 as pr
+    from paper_2111_08272_b200.trainer import RunConfig, Worker
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = pr.comm_init(rank, world, local) if world > 1 else None
+    cfg = RunConfig(N=N_DATA, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024)
+    wk = Worker(cfg, rank, world, local, comm)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def epoch(record=False, loss_to_host=False, w=wk):
+        if w.epoch > 0:                          # a10 + a5 allgather (Algorithm 1 steps 1-3)
+            ts = comm.allgather_f64(w.last_ts) if comm is not None else [w.last_ts]
+            w.launches += 1 if comm is not None else 0
+            if cfg.adaptive:
+                w.alloc.update(ts)
+        rec = w.run_epoch(record=record, loss_to_host=loss_to_host)
+        w.last_ts = rec["t_s"]
+        return rec
+
+    for _ in range(args.warmup):
+        epoch()
+    torch.cuda.synchronize()
+    barrier()
+    wk.launches = 0
+    wk.gather_events.clear()
+    wk.ar_events.clear()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    samples = 0
+    recs = []
+    for _ in range(args.steps):
+        rec = epoch(record=True)
+        recs.append(rec)
+        samples += rec["S"] * wk.alloc.view()["B"]
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    launches = wk.launches
+    ms_epoch = ms / args.steps
+    value = samples / (ms / 1e3)
+
+    # ---- roofline of the library's dominant kernel (live CUDA events in the timed region) ----------
+    hbm, peak_kind = peaks()
+    g_ms = [a.elapsed_time(b) for a, b, _ in wk.gather_events]
+    g_rows = [n for _, _, n in wk.gather_events]
+    g_bytes = statistics.mean(g_rows) * (ROW_BYTES + 2 * ROW_BYTES + 8 + 8 + 8)
+    g_avg = statistics.mean(g_ms) if g_ms else float("nan")
+    gather_roof = {"kernel": "gather_kernel<U8_TO_BF16_AFFINE> (K2)", "bound": "hbm",
+                   "achieved": g_bytes / (g_avg * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                   "peak_kind": peak_kind, "launches": len(g_ms), "avg_us": g_avg * 1e3,
+                   "bytes_per_launch": g_bytes, "total_ms": sum(g_ms)}
+    gather_roof["frac"] = gather_roof["achieved"] / hbm
+    gather_roof["traffic"] = traffic_from_profiles("gather")
+    roof = gather_roof
+    allreduce = None
+    if world > 1 and wk.ar_events:
+        a_ms = [a.elapsed_time(b) for a, b in wk.ar_events]
+        a_avg = statistics.mean(a_ms)
+        Z = wk.L * 4
+        bus = Z * 2 * (world - 1) / world / (a_avg * 1e-3) / 1e9
+        allreduce = {"kernel": "ring_kernel<float> (K3)", "bound": "nvlink", "achieved": bus, "peak": NVLINK_PEER_GBS,
+                     "unit": "GB/s", "peak_kind": "B200_PROFILING.md measured peer copy per direction",
+                     "frac": bus / NVLINK_PEER_GBS, "avg_us": a_avg * 1e3, "bytes": Z, "launches": len(a_ms),
+                     "frac_of_900_nominal": bus / 900.0, "total_ms": sum(a_ms), "traffic": None}
+        if allreduce["total_ms"] > gather_roof["total_ms"]:
+            roof = allreduce
+
+    # ---- e2e: host-resident data set, per-step loss read back --------------------------------------
+    e2e = None
+    if args.e2e_epochs > 0:
+        cfg_h = RunConfig(N=N_DATA, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024,
+                          host_data=True)
+        wk_h = Worker(cfg_h, rank, world, local, comm, data=wk.X.cpu(), labels=wk.Y.cpu())
+        wk_h.model.load_state_dict(wk.model.state_dict())
+        epoch(w=wk_h)                                      # warm-up
+        torch.cuda.synchronize()
+        barrier()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record()
+        hs = 0
+        for _ in range(args.e2e_epochs):
+            r = epoch(w=wk_h, loss_to_host=True)
+            hs += r["S"] * wk_h.alloc.view()["B"]
+        h1.record()
+        torch.cuda.synchronize()
+        barrier()
+        hms = h0.elapsed_time(h1)
+        if world > 1:
+            t = torch.tensor([hms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            hms = float(t)
+        v = wk_h.alloc.view()
+        e2e = {"value": hs / (hms / 1e3), "unit": "samples/s",
+               "h2d_bytes_per_step": v["S"] * v["n"][rank] * (ROW_BYTES + 8),
+               "d2h_bytes_per_step": v["S"] * 4,
+               "note": "data set in pinned host memory; rows gathered over PCIe by K2 inside the timed region; "
+                       "per-step loss copied to host"}
+
+    # ---- co-located ring (1 GPU): all P ranks of K3 on this GPU, HBM-bound proxy of the NVLink path --
+    colocated = None
+    if world == 1 and not args.no_colocated:
+        colocated = colocated_allreduce(hbm, peak_kind)
+
+    if rank == 0:
+        cpu = None if args.no_cpu_baseline else cpu_baseline(world)
+        out = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_epoch, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "resnet18-cifar10-shaped-50k, global batch 1024 (g=16, C=64), equal start, "
+                                   "self-adaptive allocation, fp32 gradients (11,689,512), bf16 autocast compute",
+                       "model": "resnet18 (1000-class head, random init)", "global_batch": 1024,
+                       "seq_len": None, "parallelism": f"dp{world}", "step": "one epoch (S=48 aggregations)",
+                       "l2": "inputs larger than L2 (153.6 MB data set streamed every epoch)"},
+            "epoch_time_s": ms_epoch / 1e3,
+            "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+            "roofline_detail": roof,
+            "gather": gather_roof,
+            "allreduce": allreduce,
+            "allreduce_colocated": colocated,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "cpu_baseline": cpu,
+            "alloc_w": wk.alloc.view()["w"],
+            "loss_last_epoch": recs[-1]["loss"],
+        }
+        print(json.dumps(out))
+    if comm is not None:
+        comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def traffic_from_profiles(kind):
+    """dram bytes per launch from the committed ncu --set full capture (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kind, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def colocated_allreduce(hbm, peak_kind, P=8, reps=20):
+    import torch
+
+    import paper_2111_08272_b200 as pr
+
+    comms = pr.comm_init_local(P, torch.cuda.current_device(), pr.comm_config())
+    L = L_RESNET18
+    bufs = [torch.randn(L, device="cuda") for _ in range(P)]
+    n = [64, 64, 64, 64, 128, 128, 256, 256][:P]
+    for _ in range(5):
+        pr.weighted_allreduce_local(comms, bufs, n)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        pr.weighted_allreduce_local(comms, bufs, n)
+    b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / reps
+    Z = L * 4
+    # algorithmic HBM bytes of one call, all P ranks (direct all-gather): per rank
+    # hop0 2·Z/P, P−2 middle hops 3·Z/P, last hop 4·Z/P, P−2 forwards 2·Z/P  => (6 + 5(P−2))·Z/P
+    byts = P * (6 + 5 * (P - 2)) * Z / P
+    for c in comms:
+        c.destroy()
+    return {"kernel": "ring_kernel<float> (K3), all ranks on one GPU", "P": P, "bytes_per_rank": Z,
+            "n_local": n, "avg_us": t * 1e3, "bound": "hbm", "achieved": byts / (t * 1e-3) / 1e9, "peak": hbm,
+            "unit": "GB/s", "frac": byts / (t * 1e-3) / 1e9 / hbm, "peak_kind": peak_kind,
+            "algorithmic_bytes_per_call": byts,
+            "note": "P virtual ranks co-resident on one GPU exercise the same kernel and protocol; peer stores "
+                    "land in local HBM, so this is an HBM roofline, not an NVLink number"}
+
+
+# ---------------------------------------------------------------------------------------------------
+def oracle_step(P, sample_rows, X, Y, grads, model, rank=0, a=None, epoch=0):
+    """One aggregation step of the CPU reference: oracle shard slice + gather + torch-CPU fwd/bwd on a
+    bounded sample + oracle fp64 weighted average of P gradient buffers + controller update."""
+    import numpy as np
+    import torch
+    import torch.nn.functional as F
+
+    from oracle import allocation as OA
+    from oracle import gather as OG
+    from oracle import permutation as OP
+    from oracle import wavg as OW
+
+    if a is None:
+        a = OA.alloc_init(N_DATA, [1] * P, C=C_UNITS, g=G_UNIT)
+    n_r = a.n[rank]
+    idx = OP.shard_indices(N_DATA, a.off[rank] + 0, min(a.len[rank], n_r), 1234, epoch)
+    xb, yb = OG.gather_rows(X, idx[:sample_rows], OG.U8_TO_F32_AFFINE, scale=np.float32([1 / 51.5865, 1 / 50.847, 1 / 51.255]),
+                            shift=np.float32([125.307, 122.961, 113.8575]), plane=1024, Y=Y)
+    x = torch.from_numpy(xb).view(-1, 3, 32, 32)
+    loss = F.cross_entropy(model(x), torch.from_numpy(yb))
+    model.zero_grad()
+    loss.backward()
+    ref, _ = OW.weighted_average(grads, a.n)
+    OA.alloc_update(a, [1.0] * P) if not a.frozen else None
+    return float(loss), ref.shape[0]
+
+
+def cpu_reference_setup(P):
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2111_08272_b200.trainer import build_model
+
+    X = synth.images_u8(N_DATA, seed=0).reshape(N_DATA, -1)
+    Y = synth.labels(N_DATA, 10, seed=1)
+    grads = synth.gradients(max(P, 1), L_RESNET18, seed_base=1000).astype(np.float64)
+    model = build_model("resnet18", 1000)
+    return X, Y, grads, model, torch.get_num_threads()
+
+
+def cpu_baseline(P, sample_rows=16, steps=2):
+    X, Y, grads, model, cores = cpu_reference_setup(P)
+    oracle_step(P, sample_rows, X, Y, grads, model)          # warm-up
+    t0 = time.perf_counter()
+    for s in range(steps):
+        oracle_step(P, sample_rows, X, Y, grads, model, epoch=s)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": sample_rows / dt, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "sample": f"{steps} aggregation steps, each: oracle shard slice + oracle gather of {sample_rows} rows + "
+                      f"torch-CPU fp32 ResNet-18 fwd/bwd on those rows + oracle fp64 weighted average of "
+                      f"{max(P, 1)}×{L_RESNET18} gradients + controller; samples/s = rows/step time"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    X, Y, grads, model, cores = cpu_reference_setup(args.gpus)
+    sample_rows = 16
+    for w in range(args.warmup):
+        oracle_step(args.gpus, sample_rows, X, Y, grads, model, epoch=w)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        oracle_step(args.gpus, sample_rows, X, Y, grads, model, epoch=s)
+    dt = time.perf_counter() - t0
+    value = args.steps * sample_rows / dt
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "resnet18-cifar10-shaped-50k, global batch 1024 (g=16, C=64)",
+                      "step": f"bounded sample: one aggregation step on {sample_rows} rows"},
+           "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "oracle",
+                            "sample": f"{sample_rows} rows per step (oracle path + torch-CPU ResNet-18 fwd/bwd)"},
+           "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -379,105 +379,100 @@ __global__ void __launch_bounds__(512, 1) ring_kernel(const __grid_constant__ La
         if (!wait_ge(&myf->rs_ready, consJ + 1, deadline)) fail();
     };
 
-    // RS hop 0: chunk r, y = s·g (or 0 if this rank has no samples)
-    for (int64_t i = 0; i < nsl; ++i) {
-        int64_t lo, len;
-        range(r, i, lo, len);
-        if (t0) wait_credit();
-        if (!sync_ok()) return;
-        move_slice<T>(act ? M_SCALE : M_ZERO, s, buf + lo, nullptr,
-                      reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), nullptr, len);
-        __syncthreads();
-        if (t0) st_release(&nxf->rs_ready, prodJ + 1);
-        ++prodJ;
-    }
-    // RS hops 1..P−2: chunk (r−k) mod P, y = fma(s, g, recv)
-    for (int k = 1; k <= P - 2; ++k) {
-        const int c = (r - k + P) % P;
-        for (int64_t i = 0; i < nsl; ++i) {
-            int64_t lo, len;
-            range(c, i, lo, len);
-            if (t0) { wait_ready(); if (!sh.err) wait_credit(); }
-            if (!sync_ok()) return;
-            move_slice<T>(act ? M_FMA : M_COPY, s, buf + lo, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
-                          reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), nullptr, len);
-            __syncthreads();
-            if (t0) {
-                st_release(&pvf->rs_credit, consJ + 1);
-                st_release(&nxf->rs_ready, prodJ + 1);
-            }
-            ++consJ;
-            ++prodJ;
-        }
-    }
-    // last RS hop: chunk (r+1) mod P is complete here; store it locally and send it on (AG hop 0)
-    if (P >= 2) {
-        const int c = (r + 1) % P;
-        for (int64_t i = 0; i < nsl; ++i) {
-            int64_t lo, len;
-            range(c, i, lo, len);
-            if (t0) { wait_ready(); if (!sh.err && !direct) wait_credit(); }
-            if (!sync_ok()) return;
-            T* out2 = direct ? nbuf + lo : reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ));
-            move_slice<T>(act ? M_FMA : M_COPY, s, buf + lo, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
-                          buf + lo, out2, len);
-            __syncthreads();
-            if (t0) {
-                st_release(&pvf->rs_credit, consJ + 1);
-                if (direct) st_release(&nxf->ag_ready, agP + 1);
-                else st_release(&nxf->rs_ready, prodJ + 1);
-            }
-            ++consJ;
-            if (direct) ++agP; else ++prodJ;
-        }
-    }
-    // AG hops 1..P−2: forward chunk (r+1−k) mod P received at hop k−1
-    for (int k = 1; k <= P - 2; ++k) {
-        const int c = (r + 1 - k + P) % P;
-        for (int64_t i = 0; i < nsl; ++i) {
-            int64_t lo, len;
-            range(c, i, lo, len);
-            if (direct) {
-                if (t0 && !wait_ge(&myf->ag_ready, agC + 1, deadline)) fail();
-                if (!sync_ok()) return;
-                move_slice<T>(M_COPY, s, nullptr, buf + lo, nbuf + lo, nullptr, len);
-                __syncthreads();
-                if (t0) st_release(&nxf->ag_ready, agP + 1);
-                ++agC;
-                ++agP;
-            } else {
-                if (t0) { wait_ready(); if (!sh.err) wait_credit(); }
-                if (!sync_ok()) return;
-                move_slice<T>(M_COPY, s, nullptr, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)), buf + lo,
-                              reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), len);
-                __syncthreads();
-                if (t0) {
-                    st_release(&pvf->rs_credit, consJ + 1);
-                    st_release(&nxf->rs_ready, prodJ + 1);
+    // The buffer is processed in ROUNDS of G = K/2 slices per chunk; each round walks all 2P−1 phases:
+    //   phase 0             RS hop 0     chunk r            y = s·g                 -> next's slot
+    //   phase h, 1..P−2     RS hop h     chunk (r−h) mod P  y = fma(s, g, recv)     -> next's slot
+    //   phase P−1           last RS hop  chunk (r+1) mod P  y = fma(s, g, recv)     -> own buf + next (AG hop 0)
+    //   phase P−1+k, k≥1    AG hop k     chunk (r+1−k)      forward                 -> next
+    //   phase 2P−2          AG receive   chunk (r+2) mod P  (staged: slot -> own buf)
+    // G <= K/2 keeps the schedule deadlock-free (a producer never needs a credit its consumer can only
+    // return after its own blocked production) and leaves G−1 slices of slack per hop to hide the flag
+    // latency.  Every rank executes the same (round, phase, slice) sequence, so slot numbers match.
+    const int64_t G = (int64_t)(K / 2);
+    const int nphase = 2 * P - 1;
+    for (int64_t i0 = 0; i0 < nsl; i0 += G) {
+        const int64_t gend = min(i0 + G, nsl);
+        for (int h = 0; h < nphase; ++h) {
+            for (int64_t i = i0; i < gend; ++i) {
+                int64_t lo, len;
+                if (h == 0) {                                   // RS hop 0
+                    range(r, i, lo, len);
+                    if (t0) wait_credit();
+                    if (!sync_ok()) return;
+                    move_slice<T>(act ? M_SCALE : M_ZERO, s, buf + lo, nullptr,
+                                  reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), nullptr, len);
+                    __syncthreads();
+                    if (t0) st_release(&nxf->rs_ready, prodJ + 1);
+                    ++prodJ;
+                } else if (h <= P - 2) {                        // RS hops 1..P−2
+                    range((r - h + P) % P, i, lo, len);
+                    if (t0) { wait_ready(); if (!sh.err) wait_credit(); }
+                    if (!sync_ok()) return;
+                    move_slice<T>(act ? M_FMA : M_COPY, s, buf + lo,
+                                  reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
+                                  reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), nullptr, len);
+                    __syncthreads();
+                    if (t0) {
+                        st_release(&pvf->rs_credit, consJ + 1);
+                        st_release(&nxf->rs_ready, prodJ + 1);
+                    }
+                    ++consJ;
+                    ++prodJ;
+                } else if (h == P - 1) {                        // last RS hop = AG hop 0
+                    range((r + 1) % P, i, lo, len);
+                    if (t0) { wait_ready(); if (!sh.err && !direct) wait_credit(); }
+                    if (!sync_ok()) return;
+                    T* out2 = direct ? nbuf + lo : reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ));
+                    move_slice<T>(act ? M_FMA : M_COPY, s, buf + lo,
+                                  reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)), buf + lo, out2, len);
+                    __syncthreads();
+                    if (t0) {
+                        st_release(&pvf->rs_credit, consJ + 1);
+                        if (direct) st_release(&nxf->ag_ready, agP + 1);
+                        else st_release(&nxf->rs_ready, prodJ + 1);
+                    }
+                    ++consJ;
+                    if (direct) ++agP; else ++prodJ;
+                } else if (h <= 2 * P - 3) {                    // AG hops 1..P−2
+                    const int k = h - (P - 1);
+                    range((r + 1 - k + P) % P, i, lo, len);
+                    if (direct) {
+                        if (t0 && !wait_ge(&myf->ag_ready, agC + 1, deadline)) fail();
+                        if (!sync_ok()) return;
+                        move_slice<T>(M_COPY, s, nullptr, buf + lo, nbuf + lo, nullptr, len);
+                        __syncthreads();
+                        if (t0) st_release(&nxf->ag_ready, agP + 1);
+                        ++agC;
+                        ++agP;
+                    } else {
+                        if (t0) { wait_ready(); if (!sh.err) wait_credit(); }
+                        if (!sync_ok()) return;
+                        move_slice<T>(M_COPY, s, nullptr, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
+                                      buf + lo, reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), len);
+                        __syncthreads();
+                        if (t0) {
+                            st_release(&pvf->rs_credit, consJ + 1);
+                            st_release(&nxf->rs_ready, prodJ + 1);
+                        }
+                        ++consJ;
+                        ++prodJ;
+                    }
+                } else {                                        // AG receive of hop P−2 (not forwarded)
+                    range((r + 2) % P, i, lo, len);
+                    if (direct) {
+                        if (t0 && !wait_ge(&myf->ag_ready, agC + 1, deadline)) fail();
+                        ++agC;
+                        if (!sync_ok()) return;
+                    } else {
+                        if (t0) wait_ready();
+                        if (!sync_ok()) return;
+                        move_slice<T>(M_COPY, s, nullptr, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
+                                      buf + lo, nullptr, len);
+                        __syncthreads();
+                        if (t0) st_release(&pvf->rs_credit, consJ + 1);
+                        ++consJ;
+                    }
                 }
-                ++consJ;
-                ++prodJ;
-            }
-        }
-    }
-    // AG receive of hop P−2: chunk (r+2) mod P — not forwarded
-    if (P >= 2) {
-        const int c = (r + 2) % P;
-        for (int64_t i = 0; i < nsl; ++i) {
-            int64_t lo, len;
-            range(c, i, lo, len);
-            if (direct) {
-                if (t0 && !wait_ge(&myf->ag_ready, agC + 1, deadline)) fail();
-                ++agC;
-                if (!sync_ok()) return;
-            } else {
-                if (t0) wait_ready();
-                if (!sync_ok()) return;
-                move_slice<T>(M_COPY, s, nullptr, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)), buf + lo,
-                              nullptr, len);
-                __syncthreads();
-                if (t0) st_release(&pvf->rs_credit, consJ + 1);
-                ++consJ;
             }
         }
     }

@@ -1,0 +1,227 @@
+"""Training harness around the library: Algorithm 1 on one rank of a P-rank job.
+
+Rows of SURVEY §8(a) handled here (the rest are library calls):
+  a4  local compute + gradient accumulation: "accumulate gradients without back propagation [= without
+      a parameter update] ... until w_i samples are transferred" (P:69 steps (1)-(3)).  The rank's n_r
+      samples are processed in microbatches of at most `micro` rows; each microbatch loss is scaled by
+      mb/n_r so the flat gradient buffer ends up holding the LOCAL MEAN gradient (DESIGN.md §3 #11).
+      Emulated heterogeneity: after the backward pass a K4 spin of (σ_r − 1)·c0·n_r ns (c0 = calibrated
+      seconds per sample at σ = 1) slows rank r by the factor σ_r.
+  a5  t_s capture: CUDA events around gather + compute + spin, summed over the epoch (
+      DESIGN.md §3 #4-#5); one event synchronisation per epoch, not per step.
+  a9  SGD update, Eq. 1 with weight decay: torch.optim.SGD on the reduced buffer.
+Library rows: a1/a10 alloc_init / Alloc.update, a2 shard_indices, a3 gather_rows, a6-a8 weighted_allreduce.
+
+Parameters' .grad are views into one flat fp32 buffer allocated by the communicator (CUDA-IPC registered),
+so backward() accumulates straight into the buffer the ring reduces in place — no bucketing copies.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import torch
+import torch.nn.functional as F
+
+import paper_2111_08272_b200 as pr
+
+CIFAR_MEAN = [125.307, 122.961, 113.8575]
+CIFAR_STD = [51.5865, 50.847, 51.255]
+
+
+@dataclass
+class RunConfig:
+    N: int = 50_000
+    shape: tuple = (3, 32, 32)
+    classes: int = 10
+    model: str = "resnet18"
+    num_classes: int = 1000                 # head size of the gradient buffer (DESIGN.md §3 #31)
+    ratios: list = field(default_factory=lambda: [1])
+    C: int = 0
+    g: int = 128
+    floor: int = 1
+    seed: int = 1234
+    lr: float = 1e-2
+    wd: float = 1e-4
+    micro: int = 512                        # max rows per microbatch
+    slowdown: list | None = None            # σ_r per rank (emulated heterogeneity)
+    adaptive: bool = False                  # Algorithm 1 self-adaptive allocation
+    host_data: bool = False                 # e2e: dataset in pinned host memory, gathered over PCIe
+    bf16_compute: bool = True               # autocast for the model's forward/backward
+
+
+def build_model(name: str, num_classes: int):
+    import torchvision
+
+    if name == "resnet18":
+        return torchvision.models.resnet18(num_classes=num_classes)
+    if name == "vgg16":
+        return torchvision.models.vgg16(num_classes=num_classes)
+    if name == "logreg":
+        return torch.nn.Linear(1024, 1, bias=False)
+    raise ValueError(name)
+
+
+class Worker:
+    """One rank: owns the data set copy, the model, the flat gradient buffer and the communicator."""
+
+    def __init__(self, cfg: RunConfig, rank: int = 0, world: int = 1, device: int = 0, comm=None,
+                 data=None, labels=None):
+        self.cfg, self.rank, self.P = cfg, rank, world
+        self.dev = torch.device("cuda", device)
+        torch.cuda.set_device(self.dev)
+        self.comm = comm
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.alloc = pr.alloc_init(cfg.N, cfg.ratios, C=cfg.C, g=cfg.g, floor=cfg.floor)
+        if not cfg.adaptive:
+            self.alloc.set_policy(never_freeze=False)
+        self.row_bytes = int(torch.tensor(cfg.shape).prod())
+        # data set (synthetic, replicated per rank): u8 CHW rows + int64 labels
+        if data is None:
+            import synth
+
+            data = torch.from_numpy(synth.images_u8(cfg.N, *cfg.shape, seed=0).reshape(cfg.N, -1))
+            labels = torch.from_numpy(synth.labels(cfg.N, cfg.classes, seed=1))
+        if cfg.host_data:
+            self.X = data.pin_memory()
+            self.Y = labels.to(self.dev)
+        else:
+            self.X = data.to(self.dev)
+            self.Y = labels.to(self.dev)
+        C, H, W = cfg.shape
+        self.gop = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE if cfg.bf16_compute else pr.GATHER_U8_TO_F32_AFFINE,
+                                     [1.0 / s for s in CIFAR_STD[:C]], CIFAR_MEAN[:C], H * W)
+        self.model = build_model(cfg.model, cfg.num_classes).to(self.dev)
+        torch.manual_seed(cfg.seed)
+        for p in self.model.parameters():          # identical initial weights on every rank
+            with torch.no_grad():
+                p.copy_(torch.randn_like(p) * 0.02 if p.dim() > 1 else torch.zeros_like(p))
+        params = [p for p in self.model.parameters()]
+        self.L = sum(p.numel() for p in params)
+        if comm is not None:
+            self.flat = comm.alloc(self.L * 4, dtype=torch.float32)
+        else:
+            self.flat = torch.zeros(self.L, dtype=torch.float32, device=self.dev)
+        off = 0
+        for p in params:
+            p.grad = self.flat[off:off + p.numel()].view_as(p)
+            off += p.numel()
+        self.opt = torch.optim.SGD(params, lr=cfg.lr, weight_decay=cfg.wd)
+        v = self.alloc.view()
+        self.idx = torch.empty(max(v["len"]) + cfg.N // max(1, v["P"]) + 16, dtype=torch.int64, device=self.dev)
+        self.c0_ns = 0.0                               # calibrated per-sample compute time (ns) at σ = 1
+        self.launches = 0                              # library kernels launched (for the bench)
+        self.ar_events = []
+        self.gather_events = []
+        self.epoch = 0
+
+    # ---- one aggregation step (Algorithm 1 steps 4-6) ------------------------------------
+    def step(self, s: int, n_r: int, xbuf, ybuf, record=False):
+        cfg = self.cfg
+        C, H, W = cfg.shape
+        if n_r > 0:
+            if record:
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                g0.record(self.stream)
+            src = self.X.data_ptr()
+            pr.gather_rows(src, cfg.N, self.row_bytes, self.idx[s * n_r:], n_r, xbuf, self.gop, self.Y, ybuf,
+                           stream=self.stream)
+            self.launches += 1
+            if record:
+                g1.record(self.stream)
+                self.gather_events.append((g0, g1, n_r))
+            x = xbuf[:n_r].view(n_r, C, H, W)
+            y = ybuf[:n_r]
+            losses = []
+            for m0 in range(0, n_r, cfg.micro):
+                xm, ym = x[m0:m0 + cfg.micro], y[m0:m0 + cfg.micro]
+                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.bf16_compute):
+                    out = self.model(xm)
+                    loss = F.cross_entropy(out.float(), ym)
+                (loss * (xm.shape[0] / n_r)).backward()       # local mean over n_r (DESIGN §3 #11)
+                losses.append(loss.detach() * xm.shape[0])
+            sigma = cfg.slowdown[self.rank] if cfg.slowdown else 1.0
+            if sigma > 1.0 and self.c0_ns > 0:
+                pr.spin(int((sigma - 1.0) * self.c0_ns * n_r), stream=self.stream)
+                self.launches += 1
+            return torch.stack(losses).sum() / n_r
+        return torch.zeros((), device=self.dev)
+
+    def allreduce_and_update(self, n_r: int, record=False):
+        if self.P > 1:
+            if record:
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(self.stream)
+            pr.weighted_allreduce(self.comm, self.flat, n_r, stream=self.stream)
+            self.launches += 1
+            if record:
+                a1.record(self.stream)
+                self.ar_events.append((a0, a1))
+        self.opt.step()
+        self.flat.zero_()
+
+    # ---- one epoch (Algorithm 1 outer loop) ---------------------------------------------------------
+    def run_epoch(self, record=False, loss_to_host=False):
+        cfg = self.cfg
+        v = self.alloc.view()
+        n_r, S = v["n"][self.rank], v["S"]
+        pr.shard_indices(self.alloc, self.rank, self.epoch, cfg.seed, self.idx, stream=self.stream)   # a2
+        self.launches += 1
+        width = 2 if cfg.bf16_compute else 4
+        xbuf = torch.empty((max(n_r, 1), self.row_bytes * width // (2 if cfg.bf16_compute else 4)),
+                           dtype=torch.bfloat16 if cfg.bf16_compute else torch.float32, device=self.dev)
+        ybuf = torch.empty(max(n_r, 1), dtype=torch.int64, device=self.dev)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
+        losses = []
+        host_losses = []
+        for s in range(S):
+            ev[s][0].record(self.stream)
+            loss = self.step(s, n_r, xbuf, ybuf, record)
+            ev[s][1].record(self.stream)
+            self.allreduce_and_update(n_r, record)
+            losses.append(loss)
+            if loss_to_host:
+                host_losses.append(float(loss))          # D2H of the step's result (e2e contract)
+        ev[-1][1].synchronize()
+        t_s = sum(a.elapsed_time(b) for a, b in ev) / 1e3   # seconds (a5)
+        self.epoch += 1
+        return {"t_s": t_s, "loss": float(torch.stack(losses).mean()), "S": S, "n_r": n_r, "w": v["w"]}
+
+    def boundary(self, t_s: float):
+        """Algorithm 1 steps 1-3: allgather t_s, Eq. 10 + rounding, redistribute."""
+        if not self.cfg.adaptive:
+            return False
+        if self.P > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([t_s], dtype=torch.float64, device=self.dev)
+            allt = [torch.zeros_like(t) for _ in range(self.P)]
+            dist.all_gather(allt, t)
+            ts = [float(x) for x in allt]
+        else:
+            ts = [t_s]
+        return self.alloc.update(ts)
+
+    def calibrate(self, steps: int = 3):
+        """c0 = seconds per sample of this rank's compute at σ = 1 (for the K4 spin)."""
+        v = self.alloc.view()
+        n_r = v["n"][self.rank]
+        pr.shard_indices(self.alloc, self.rank, 0, self.cfg.seed, self.idx, stream=self.stream)
+        C, H, W = self.cfg.shape
+        xbuf = torch.empty((n_r, C * H * W), dtype=torch.bfloat16, device=self.dev)
+        ybuf = torch.empty(n_r, dtype=torch.int64, device=self.dev)
+        save = self.cfg.slowdown
+        self.cfg.slowdown = None
+        for _ in range(2):
+            self.step(0, n_r, xbuf, ybuf)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(self.stream)
+        for s in range(steps):
+            self.step(s, n_r, xbuf, ybuf)
+        b.record(self.stream)
+        b.synchronize()
+        self.flat.zero_()
+        self.cfg.slowdown = save
+        self.c0_ns = a.elapsed_time(b) * 1e6 / (steps * n_r)
+        return self.c0_ns

@@ -107,10 +107,10 @@ def test_equal_weights_match_torch_mean():
     P, L = 4, 100_003
     comms = group(P)
     host, dev = _inputs(P, L, "f32")
-    mean = torch.stack(dev).double().mean(0)
+    mean = torch.stack(dev).double().mean(0)                      # library routine
+    den = torch.stack(dev).double().abs().sum(0) / P + 1e-300     # Σ|s·g| (before the in-place reduce)
     pr.weighted_allreduce_local(comms, dev, [32] * P)
     torch.cuda.synchronize()
-    den = torch.stack(dev).double().abs().sum(0) / P + 1e-300
     assert float(((dev[0].double() - mean).abs() / den).max()) <= 1e-5
 
 
@@ -185,12 +185,15 @@ def test_staged_allgather_path():
 
 
 @pytest.mark.parametrize("cfg", [dict(channels=1, slots=2, slot_bytes=256), dict(channels=3, slots=3, slot_bytes=4096),
-                                 dict(channels=32, slots=8, slot_bytes=65536, threads=256)])
+                                 dict(channels=32, slots=8, slot_bytes=65536, threads=256),
+                                 dict(channels=3, slots=4, slot_bytes=1024, force_staged=True),
+                                 dict(channels=2, slots=5, slot_bytes=512, threads=64)])
 def test_config_variants(cfg):
     for P in (2, 5):
         comms = group(P, **cfg)
         for L in (1, 999, 300_001):
             _check(P, L, "f32", [7] * (P - 1) + [1], comms, seed=L)
+            _check(P, L, "bf16", [2] * P, comms, seed=L)
 
 
 def test_cuda_graph_replay():

@@ -177,6 +177,7 @@ def test_gather_from_mapped_host_memory():
 # ---------------------------------------------------------------- K4 ----------------------------
 
 def test_spin_duration():
+    pr.spin(1000)                     # first launch pays the lazy module load
     torch.cuda.synchronize()
     for ns in (50_000, 1_000_000):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -185,4 +186,4 @@ def test_spin_duration():
         e.record()
         e.synchronize()
         ms = s.elapsed_time(e)
-        assert ns / 1e6 * 0.99 <= ms <= ns / 1e6 * 1.10 + 0.02
+        assert ns / 1e6 * 0.99 <= ms <= ns / 1e6 * 1.02 + 0.015    # + launch latency
