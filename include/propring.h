@@ -167,11 +167,13 @@ typedef struct pr_comm pr_comm;
 
 typedef struct {
     int32_t channels;     /* ring channels = CTAs per rank (default 16)                               */
-    int32_t slots;        /* staging slots per channel (pipeline depth, default 4)                    */
-    int32_t threads;      /* threads per CTA, <= 512 (default 512)                                         */
+    int32_t slots;        /* staging slots per channel, >= 2 (default 8)                    */
+    int32_t threads;      /* consumer threads per CTA, <= 512 (default 512)                                         */
     int32_t flags;        /* PR_COMM_FLAG_* (default 0)                                                */
-    int64_t slot_bytes;   /* bytes per staging slot, multiple of 16 (default 131072)                  */
+    int64_t slot_bytes;   /* bytes per staging slot, multiple of 256 (default 262144)                 */
     int64_t watchdog_ns;  /* spin-wait deadline per call (default 10 s); <= 0 disables               */
+    int32_t stages;       /* TMA smem pipeline depth per CTA, 2..16 (default 6)                       */
+    int32_t tile_bytes;   /* bytes per input per pipeline stage, multiple of 16, <= 32768 (default 16384) */
 } pr_comm_config;
 
 /* Byte allgather supplied by the caller (e.g. over a torch process group): every rank passes `len`

@@ -209,11 +209,12 @@ def test_philox(ctr, key: int, use_curand: bool, out, stream=None):
 COMM_FLAG_FORCE_STAGED = 1
 
 
-def comm_config(channels=16, slots=4, threads=512, slot_bytes=128 * 1024, watchdog_ns=10_000_000_000,
-                force_staged=False):
+def comm_config(channels=16, slots=8, threads=512, slot_bytes=256 * 1024, watchdog_ns=10_000_000_000,
+                force_staged=False, stages=6, tile_bytes=16384):
+    """K3 launch/pipeline configuration; the defaults are the best of tools/sweep_ring.py on B200."""
     return CommConfig(channels=channels, slots=slots, threads=threads,
                       flags=COMM_FLAG_FORCE_STAGED if force_staged else 0, slot_bytes=slot_bytes,
-                      watchdog_ns=watchdog_ns)
+                      watchdog_ns=watchdog_ns, stages=stages, tile_bytes=tile_bytes)
 
 
 class _DeviceBuffer:

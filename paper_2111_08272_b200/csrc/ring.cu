@@ -35,12 +35,11 @@
 
 namespace {
 
-constexpr int kUnroll = 4;
 
 // ---- window layout (one cudaMalloc per rank, CUDA-IPC exported) ------------------------------------
 struct ChanFlags {          // written by peers, polled locally
-    unsigned long long rs_ready;   uint64_t p0[15];   // by prev: slot-slices produced into my staging
-    unsigned long long rs_credit;  uint64_t p1[15];   // by next: my slot-slices it has consumed
+    unsigned long long rs_ready;   uint64_t p0[15];   // by prev: slices it has stored into my staging slots
+    unsigned long long rs_credit;  uint64_t p1[15];   // by next: my slot-slices it has consumed (slot reuse)
     unsigned long long ag_ready;   uint64_t p2[15];   // by prev: direct all-gather slices written into my buf
 };
 struct HsEntry {            // handshake entry, written by rank q into every peer's page (slot [parity][q])
@@ -52,8 +51,10 @@ struct HsEntry {            // handshake entry, written by rank q into every pee
     int64_t offset;
     uint64_t pad[3];
 };
-struct ChanState {          // local only
-    unsigned long long seq, slot_base, ag_base;
+struct ChanState {          // local only: cumulative counters carried across calls
+    unsigned long long seq;         // handshake sequence number
+    unsigned long long slot_base;   // staging-slot slices produced (= consumed: uniform slicing)
+    unsigned long long ag_base;     // direct all-gather slices sent (= received)
     uint64_t pad[13];
 };
 struct AgEntry {
@@ -66,6 +67,7 @@ static_assert(sizeof(ChanState) == 128, "state");
 
 struct DevTable {
     int32_t rank, P, channels, slots;
+    int32_t stages, tile_bytes;     // TMA pipeline: depth, bytes per input per stage
     int64_t slot_bytes;
     int64_t watchdog_ns;
     uint64_t off_flags, off_hs, off_state, off_ag, off_staging, window_bytes;
@@ -121,6 +123,9 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ long long ld_relaxed_s64(const void* p) {
     long long v;
     asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -128,11 +133,6 @@ __device__ __forceinline__ long long ld_relaxed_s64(const void* p) {
 }
 __device__ __forceinline__ void st_relaxed_s64(void* p, long long v) {
     asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    return r;
 }
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -213,47 +213,41 @@ template <> struct Vec<__nv_bfloat16> {
     }
 };
 
-// Move one slice: out1[e] (and out2[e]) = f(g[e], in[e]) for e < len.  All threads of the CTA.
-template <typename T>
-__device__ __forceinline__ void move_slice(int mode, float s, const T* g, const T* in, T* out1, T* out2, int64_t len) {
-    constexpr int V = Vec<T>::V;
-    const int64_t nv = len / V;
-    const int64_t nt = blockDim.x;
-    const bool need_g = (mode == M_SCALE || mode == M_FMA), need_in = (mode == M_FMA || mode == M_COPY);
-    for (int64_t base = threadIdx.x; base < nv; base += nt * kUnroll) {
-        uint4 a[kUnroll], b[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const int64_t v = base + u * nt;
-            a[u] = make_uint4(0, 0, 0, 0);
-            b[u] = make_uint4(0, 0, 0, 0);
-            if (v < nv) {
-                if (need_g) a[u] = ld_cg_v4(g + v * V);
-                if (need_in) b[u] = ld_cg_v4(in + v * V);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const int64_t v = base + u * nt;
-            if (v < nv) {
-                const uint4 y = Vec<T>::op(mode, s, a[u], b[u]);
-                st_v4(out1 + v * V, y);
-                if (out2) st_v4(out2 + v * V, y);
-            }
-        }
-    }
-    for (int64_t e = nv * V + threadIdx.x; e < len; e += nt) {   // ragged tail (end of the buffer only)
-        const float gv = need_g ? Vec<T>::to_f(Vec<T>::ld(g + e)) : 0.0f;
-        const float iv = need_in ? Vec<T>::to_f(Vec<T>::ld(in + e)) : 0.0f;
-        float r;
-        if (mode == M_SCALE) r = __fmul_rn(s, gv);
-        else if (mode == M_FMA) r = __fmaf_rn(s, gv, iv);
-        else if (mode == M_COPY) r = iv;
-        else r = 0.0f;
-        const T y = (mode == M_COPY) ? Vec<T>::ld(in + e) : Vec<T>::from_f(r);
-        Vec<T>::st(out1 + e, y);
-        if (out2) Vec<T>::st(out2 + e, y);
-    }
+// ---- TMA (bulk copy) + mbarrier helpers ------------------------------------------------------------
+constexpr int kMaxStages = 16;      // smem pipeline depth limit (tiles in flight per CTA)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n"
+        "DONE:\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+// TMA bulk copy global -> shared, completion counted in bytes on `bar` (SASS: UBLKCP)
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// generic-proxy writes (peer stores observed through an acquire) -> visible to the async proxy (TMA)
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 struct Shared {
@@ -261,6 +255,11 @@ struct Shared {
     int direct;
     long long sumn;
     void* next_buf;
+    unsigned long long fin_slot, fin_ag;   // producer's final counters, for the epilogue
+    uint64_t full[kMaxStages];             // producer -> consumers: tile landed in smem (TMA tx bytes)
+    uint64_t stored[kMaxStages];           // consumers -> signal warp: tile's stores issued
+    uint64_t empty[kMaxStages];            // consumers + signal warp -> producer: stage reusable
+    int tile_ok[kMaxStages];
 };
 
 __device__ __forceinline__ void latch(const DevTable* t, int code) {
@@ -276,8 +275,28 @@ __device__ __forceinline__ bool wait_ge(const unsigned long long* p, unsigned lo
     return true;
 }
 
+enum Kind { K_FIRST = 0, K_MID = 1, K_LAST = 2, K_AGMID = 3, K_AGLAST = 4 };
+
+// The schedule: rounds of G slices; each round walks the 2P−1 phases (see the comment in ring_kernel).
+template <typename F>
+__device__ __forceinline__ void for_each_step(int P, int r, int64_t nsl, int64_t G, F&& f) {
+    for (int64_t i0 = 0; i0 < nsl; i0 += G) {
+        const int64_t gend = min(i0 + G, nsl);
+        for (int h = 0; h < 2 * P - 1; ++h) {
+            int kind, c;
+            if (h == 0) { kind = K_FIRST; c = r; }
+            else if (h <= P - 2) { kind = K_MID; c = (r - h + P) % P; }
+            else if (h == P - 1) { kind = K_LAST; c = (r + 1) % P; }
+            else if (h <= 2 * P - 3) { kind = K_AGMID; c = (r + 1 - (h - (P - 1)) + P) % P; }
+            else { kind = K_AGLAST; c = (r + 2) % P; }
+            for (int64_t i = i0; i < gend; ++i) f(kind, c, i);
+        }
+    }
+}
+
 template <typename T>
-__global__ void __launch_bounds__(512, 1) ring_kernel(const __grid_constant__ LaunchArgs A) {
+__global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ LaunchArgs A) {
+    extern __shared__ __align__(128) uint8_t smem[];   // [stages][2][tile_bytes]: g tile, recv tile
     __shared__ Shared sh;
     const RankCall& rc = A.calls[blockIdx.y];
     const DevTable* tab = rc.tab;
@@ -290,6 +309,9 @@ __global__ void __launch_bounds__(512, 1) ring_kernel(const __grid_constant__ La
     ChanFlags* nxf = flags_of(tab->win[next], tab, ch);
     ChanFlags* pvf = flags_of(tab->win[prev], tab, ch);
     const bool t0 = threadIdx.x == 0;
+    const int nc = blockDim.x - 64;                 // consumer threads (warps 2..): warp 0 producer, warp 1 signal
+    const int kStages = tab->stages;
+    const int kTileBytes = tab->tile_bytes;
     unsigned long long deadline = ~0ull;
 
     // ---- handshake = the barrier; its duration is t_w ---------------------------------
@@ -297,6 +319,12 @@ __global__ void __launch_bounds__(512, 1) ring_kernel(const __grid_constant__ La
         const unsigned long long start = gtimer();
         if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
         if (ch == 0) tab->stamps[0] = (long long)start;
+        for (int k = 0; k < kStages; ++k) {
+            mbar_init(&sh.full[k], 1);
+            mbar_init(&sh.stored[k], (uint32_t)(nc / 32));
+            mbar_init(&sh.empty[k], (uint32_t)(nc / 32 + 1));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const unsigned long long seq = st->seq + 1;
         const int par = (int)(seq & 1ull);
         for (int q = 0; q < P; ++q) {
@@ -340,46 +368,22 @@ __global__ void __launch_bounds__(512, 1) ring_kernel(const __grid_constant__ La
 
     // ---- geometry (DESIGN.md §3 #14) ----------------------------------------------------------------
     constexpr int V = Vec<T>::V;
+    const int64_t TE = kTileBytes / (int64_t)sizeof(T);          // tile elements
     const int64_t count = A.count;
     const int64_t per = (count + P - 1) / P;
     const int64_t cs = (per + V - 1) / V * V;                      // chunk elements
     const int64_t subp = (cs + tab->channels - 1) / tab->channels;
     const int64_t sub = (subp + V - 1) / V * V;                   // this channel's share of a chunk
-    const int64_t sl = tab->slot_bytes / (int64_t)sizeof(T);       // slice elements
+    const int64_t sl = tab->slot_bytes / (int64_t)sizeof(T);       // slice elements (one staging slot)
+    const int64_t te = min(TE, sl);
     const int64_t nsl = sub > 0 ? (sub + sl - 1) / sl : 0;
     const float s = (float)((double)rc.n_local / (double)sh.sumn);  // n_r/Σn: fp64 division, fp32 weight
     const bool act = rc.n_local > 0;
     const bool direct = sh.direct != 0;
     T* buf = reinterpret_cast<T*>(rc.buf);
     T* nbuf = reinterpret_cast<T*>(sh.next_buf);
-    unsigned long long prodJ = st->slot_base, consJ = st->slot_base, agP = st->ag_base, agC = st->ag_base;
     const unsigned long long K = (unsigned long long)tab->slots;
-
-    auto range = [&](int c, int64_t i, int64_t& lo, int64_t& len) {
-        const int64_t clo = (int64_t)c * cs;
-        const int64_t chi = min(clo + cs, count);
-        const int64_t a = clo + (int64_t)ch * sub + i * sl;
-        const int64_t b = min(min(a + sl, clo + min((int64_t)(ch + 1) * sub, cs)), chi);
-        lo = a;
-        len = b > a ? b - a : 0;
-    };
-    // thread 0 waits, then the CTA proceeds together; false = abort (watchdog)
-    auto sync_ok = [&]() -> bool {
-        __syncthreads();
-        return sh.err == 0;
-    };
-    auto fail = [&]() {
-        sh.err = PR_ERR_PEER_TIMEOUT;
-        latch(tab, PR_ERR_PEER_TIMEOUT);
-    };
-    auto wait_credit = [&]() {   // slot prodJ % K in next's staging is free once next consumed prodJ − K
-        if (prodJ + 1 > K && !wait_ge(&myf->rs_credit, prodJ + 1 - K, deadline)) fail();
-    };
-    auto wait_ready = [&]() {
-        if (!wait_ge(&myf->rs_ready, consJ + 1, deadline)) fail();
-    };
-
-    // The buffer is processed in ROUNDS of G = K/2 slices per chunk; each round walks all 2P−1 phases:
+    // Rounds of G = K/2 slices per chunk walk all 2P−1 phases:
     //   phase 0             RS hop 0     chunk r            y = s·g                 -> next's slot
     //   phase h, 1..P−2     RS hop h     chunk (r−h) mod P  y = fma(s, g, recv)     -> next's slot
     //   phase P−1           last RS hop  chunk (r+1) mod P  y = fma(s, g, recv)     -> own buf + next (AG hop 0)
@@ -389,96 +393,186 @@ __global__ void __launch_bounds__(512, 1) ring_kernel(const __grid_constant__ La
     // return after its own blocked production) and leaves G−1 slices of slack per hop to hide the flag
     // latency.  Every rank executes the same (round, phase, slice) sequence, so slot numbers match.
     const int64_t G = (int64_t)(K / 2);
-    const int nphase = 2 * P - 1;
-    for (int64_t i0 = 0; i0 < nsl; i0 += G) {
-        const int64_t gend = min(i0 + G, nsl);
-        for (int h = 0; h < nphase; ++h) {
-            for (int64_t i = i0; i < gend; ++i) {
+
+    auto range = [&](int c, int64_t i, int64_t& lo, int64_t& len) {
+        const int64_t clo = (int64_t)c * cs;
+        const int64_t chi = min(clo + cs, count);
+        const int64_t a = clo + (int64_t)ch * sub + i * sl;
+        const int64_t b = min(min(a + sl, clo + min((int64_t)(ch + 1) * sub, cs)), chi);
+        lo = a;
+        len = b > a ? b - a : 0;
+    };
+    auto reads_slot = [&](int k) { return k == K_MID || k == K_LAST || (!direct && (k == K_AGMID || k == K_AGLAST)); };
+    auto writes_slot = [&](int k) { return k == K_FIRST || k == K_MID || (!direct && (k == K_LAST || k == K_AGMID)); };
+    auto waits_ag = [&](int k) { return direct && (k == K_AGMID || k == K_AGLAST); };
+    auto sends_ag = [&](int k) { return direct && (k == K_LAST || k == K_AGMID); };
+    auto needs_g = [&](int k) { return act && (k == K_FIRST || k == K_MID || k == K_LAST); };
+    auto needs_in = [&](int k) { return k != K_FIRST && !(direct && k == K_AGLAST); };
+    auto ntiles = [&](int k, int64_t len) -> int64_t {
+        if (direct && k == K_AGLAST) return 0;
+        return (len + te - 1) / te;
+    };
+    auto mode_of = [&](int k) -> int {
+        if (k == K_FIRST) return act ? M_SCALE : M_ZERO;
+        if (k == K_MID || k == K_LAST) return act ? M_FMA : M_COPY;
+        return M_COPY;
+    };
+
+    if (threadIdx.x < 32) {
+        // ================= producer: flags -> TMA bulk loads into the smem ring =======================
+        if (t0) {
+            unsigned long long prodJ = st->slot_base, consJ = st->slot_base, agC = st->ag_base;
+            uint32_t tc = 0;
+            bool bad = false;
+            for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
                 int64_t lo, len;
-                if (h == 0) {                                   // RS hop 0
-                    range(r, i, lo, len);
-                    if (t0) wait_credit();
-                    if (!sync_ok()) return;
-                    move_slice<T>(act ? M_SCALE : M_ZERO, s, buf + lo, nullptr,
-                                  reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), nullptr, len);
-                    __syncthreads();
-                    if (t0) st_release(&nxf->rs_ready, prodJ + 1);
-                    ++prodJ;
-                } else if (h <= P - 2) {                        // RS hops 1..P−2
-                    range((r - h + P) % P, i, lo, len);
-                    if (t0) { wait_ready(); if (!sh.err) wait_credit(); }
-                    if (!sync_ok()) return;
-                    move_slice<T>(act ? M_FMA : M_COPY, s, buf + lo,
-                                  reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
-                                  reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), nullptr, len);
-                    __syncthreads();
-                    if (t0) {
-                        st_release(&pvf->rs_credit, consJ + 1);
-                        st_release(&nxf->rs_ready, prodJ + 1);
+                range(c, i, lo, len);
+                if (!bad) {
+                    bool ok = true;
+                    if (reads_slot(kind)) ok = wait_ge(&myf->rs_ready, consJ + 1, deadline);
+                    if (ok && waits_ag(kind)) ok = wait_ge(&myf->ag_ready, agC + 1, deadline);
+                    if (ok && writes_slot(kind) && prodJ + 1 > K) ok = wait_ge(&myf->rs_credit, prodJ + 1 - K, deadline);
+                    if (!ok) {
+                        bad = true;
+                        *(volatile int*)&sh.err = PR_ERR_PEER_TIMEOUT;
+                        latch(tab, PR_ERR_PEER_TIMEOUT);
                     }
-                    ++consJ;
-                    ++prodJ;
-                } else if (h == P - 1) {                        // last RS hop = AG hop 0
-                    range((r + 1) % P, i, lo, len);
-                    if (t0) { wait_ready(); if (!sh.err && !direct) wait_credit(); }
-                    if (!sync_ok()) return;
-                    T* out2 = direct ? nbuf + lo : reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ));
-                    move_slice<T>(act ? M_FMA : M_COPY, s, buf + lo,
-                                  reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)), buf + lo, out2, len);
-                    __syncthreads();
-                    if (t0) {
-                        st_release(&pvf->rs_credit, consJ + 1);
-                        if (direct) st_release(&nxf->ag_ready, agP + 1);
-                        else st_release(&nxf->rs_ready, prodJ + 1);
+                    if (reads_slot(kind) || waits_ag(kind)) fence_proxy_async_global();
+                }
+                const int64_t nt = ntiles(kind, len);
+                const T* gsrc = buf + lo;
+                const T* isrc = (kind == K_AGMID && direct) ? buf + lo
+                                                            : reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ));
+                for (int64_t t = 0; t < nt; ++t, ++tc) {
+                    const int stg = (int)(tc % (uint32_t)kStages);
+                    if (tc >= (uint32_t)kStages) mbar_wait(&sh.empty[stg], ((tc / (uint32_t)kStages) - 1) & 1);
+                    const int64_t e0 = t * te;
+                    const int64_t ne = min(te, len - e0);
+                    const uint32_t vb = (uint32_t)((ne * (int64_t)sizeof(T)) & ~15ll);   // whole 16 B vectors
+                    uint8_t* gs = smem + (size_t)stg * 2 * kTileBytes;
+                    uint8_t* is = gs + kTileBytes;
+                    uint32_t tx = 0;
+                    if (!bad && vb) {
+                        if (needs_g(kind)) tx += vb;
+                        if (needs_in(kind)) tx += vb;
                     }
-                    ++consJ;
-                    if (direct) ++agP; else ++prodJ;
-                } else if (h <= 2 * P - 3) {                    // AG hops 1..P−2
-                    const int k = h - (P - 1);
-                    range((r + 1 - k + P) % P, i, lo, len);
-                    if (direct) {
-                        if (t0 && !wait_ge(&myf->ag_ready, agC + 1, deadline)) fail();
-                        if (!sync_ok()) return;
-                        move_slice<T>(M_COPY, s, nullptr, buf + lo, nbuf + lo, nullptr, len);
-                        __syncthreads();
-                        if (t0) st_release(&nxf->ag_ready, agP + 1);
-                        ++agC;
-                        ++agP;
-                    } else {
-                        if (t0) { wait_ready(); if (!sh.err) wait_credit(); }
-                        if (!sync_ok()) return;
-                        move_slice<T>(M_COPY, s, nullptr, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
-                                      buf + lo, reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ)), len);
-                        __syncthreads();
-                        if (t0) {
-                            st_release(&pvf->rs_credit, consJ + 1);
-                            st_release(&nxf->rs_ready, prodJ + 1);
-                        }
-                        ++consJ;
-                        ++prodJ;
-                    }
-                } else {                                        // AG receive of hop P−2 (not forwarded)
-                    range((r + 2) % P, i, lo, len);
-                    if (direct) {
-                        if (t0 && !wait_ge(&myf->ag_ready, agC + 1, deadline)) fail();
-                        ++agC;
-                        if (!sync_ok()) return;
-                    } else {
-                        if (t0) wait_ready();
-                        if (!sync_ok()) return;
-                        move_slice<T>(M_COPY, s, nullptr, reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ)),
-                                      buf + lo, nullptr, len);
-                        __syncthreads();
-                        if (t0) st_release(&pvf->rs_credit, consJ + 1);
-                        ++consJ;
+                    sh.tile_ok[stg] = bad ? 0 : 1;
+                    mbar_arrive_expect_tx(&sh.full[stg], tx);
+                    if (!bad && vb) {
+                        if (needs_g(kind)) tma_load(gs, gsrc + e0, vb, &sh.full[stg]);
+                        if (needs_in(kind)) tma_load(is, isrc + e0, vb, &sh.full[stg]);
                     }
                 }
-            }
+                if (reads_slot(kind)) ++consJ;
+                if (writes_slot(kind)) ++prodJ;
+                if (waits_ag(kind)) ++agC;
+            });
+            sh.fin_slot = consJ;                   // hand the final counters to the epilogue
+            sh.fin_ag = agC;
         }
+    } else if (threadIdx.x < 64) {
+        // ================= signal warp: per-slice release of ready flags, off the data path ===========
+        // Waits until the consumers' stores of a slice's tiles are issued (stored barrier, release.cta by
+        // every consumer warp), then one sys-scope release makes the whole slice visible to the peer.
+        if (threadIdx.x == 32) {
+            unsigned long long prodJ = st->slot_base, agP = st->ag_base;
+            uint32_t tc = 0;
+            for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
+                int64_t lo, len;
+                range(c, i, lo, len);
+                const int64_t nt = ntiles(kind, len);
+                const bool sends = sends_ag(kind) || writes_slot(kind);
+                bool ok = true;
+                for (int64_t t = 0; t < nt; ++t, ++tc) {
+                    const int stg = (int)(tc % (uint32_t)kStages);
+                    if (sends) mbar_wait(&sh.stored[stg], (tc / (uint32_t)kStages) & 1);
+                    ok = ok && sh.tile_ok[stg] != 0;
+                    if (t == nt - 1 && sends && ok) {
+                        if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1);
+                        else st_release(&nxf->rs_ready, prodJ + 1);
+                    }
+                    mbar_arrive(&sh.empty[stg]);
+                }
+                if (nt == 0 && sends && !*(volatile int*)&sh.err) {   // empty slice: nothing to wait for
+                    if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1);
+                    else st_release(&nxf->rs_ready, prodJ + 1);
+                }
+                if (sends_ag(kind)) ++agP;
+                else if (writes_slot(kind)) ++prodJ;
+            });
+        }
+    } else {
+        // ================= consumers: smem -> fp32 math -> 16 B stores to local + peer memory ==========
+        const int cid = threadIdx.x - 64;
+        const int lane = threadIdx.x & 31;
+        unsigned long long prodJ = st->slot_base, consJ = st->slot_base;
+        uint32_t tc = 0;
+        for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
+            int64_t lo, len;
+            range(c, i, lo, len);
+            const int64_t nt = ntiles(kind, len);
+            const int mode = mode_of(kind);
+            T* out1;
+            T* out2 = nullptr;
+            T* nslot = reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ));
+            if (kind == K_FIRST || kind == K_MID) out1 = nslot;
+            else if (kind == K_LAST) { out1 = buf + lo; out2 = direct ? nbuf + lo : nslot; }
+            else if (kind == K_AGMID) { if (direct) out1 = nbuf + lo; else { out1 = buf + lo; out2 = nslot; } }
+            else out1 = buf + lo;                                   // K_AGLAST (staged)
+            const T* gsrc = buf + lo;
+            const T* isrc = (kind == K_AGMID && direct) ? buf + lo
+                                                        : reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ));
+            const bool ng = needs_g(kind), ni = needs_in(kind);
+            bool ok = true;
+            for (int64_t t = 0; t < nt; ++t, ++tc) {
+                const int stg = (int)(tc % (uint32_t)kStages);
+                mbar_wait(&sh.full[stg], (tc / (uint32_t)kStages) & 1);
+                ok = sh.tile_ok[stg] != 0;
+                if (ok && t == nt - 1 && reads_slot(kind) && cid == 0)   // slot landed in smem: hand it back
+                    st_relaxed_u64(&pvf->rs_credit, consJ + 1);     // (ordered after the TMA reads by the wait)
+                const int64_t e0 = t * te;
+                const int64_t ne = min(te, len - e0);
+                const int64_t nv = (ne * (int64_t)sizeof(T)) / 16;
+                const uint4* gs = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes);
+                const uint4* is = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes + kTileBytes);
+                if (ok) {
+                    for (int64_t v = cid; v < nv; v += nc) {
+                        const uint4 a = ng ? gs[v] : make_uint4(0, 0, 0, 0);
+                        const uint4 b = ni ? is[v] : make_uint4(0, 0, 0, 0);
+                        const uint4 y = Vec<T>::op(mode, s, a, b);
+                        st_v4(out1 + e0 + v * V, y);
+                        if (out2) st_v4(out2 + e0 + v * V, y);
+                    }
+                    for (int64_t e = nv * V + cid; e < ne; e += nc) {   // ragged tail: end of the buffer only
+                        const float gv = ng ? Vec<T>::to_f(Vec<T>::ld(gsrc + e0 + e)) : 0.0f;
+                        const float iv = ni ? Vec<T>::to_f(Vec<T>::ld(isrc + e0 + e)) : 0.0f;
+                        float rr;
+                        if (mode == M_SCALE) rr = __fmul_rn(s, gv);
+                        else if (mode == M_FMA) rr = __fmaf_rn(s, gv, iv);
+                        else rr = (mode == M_COPY) ? iv : 0.0f;
+                        const T y = (mode == M_COPY) ? Vec<T>::ld(isrc + e0 + e) : Vec<T>::from_f(rr);
+                        Vec<T>::st(out1 + e0 + e, y);
+                        if (out2) Vec<T>::st(out2 + e0 + e, y);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sh.stored[stg]);                   // release.cta: this warp's stores precede
+                    mbar_arrive(&sh.empty[stg]);
+                }
+            }
+            const bool err = *(volatile int*)&sh.err != 0;
+            if (nt == 0 && reads_slot(kind) && cid == 0 && !err) st_relaxed_u64(&pvf->rs_credit, consJ + 1);
+            if (reads_slot(kind)) ++consJ;
+            if (writes_slot(kind)) ++prodJ;
+        });
     }
+    __syncthreads();
     if (t0) {
-        st->slot_base = consJ;   // == prodJ: every rank produces and consumes the same number of slices
-        st->ag_base = agC;       // == agP
+        if (!*(volatile int*)&sh.err) {
+            st->slot_base = sh.fin_slot;   // == prodJ: all ranks produce/consume equally
+            st->ag_base = sh.fin_ag;
+        }
         if (ch == 0) tab->stamps[2] = (long long)gtimer();
     }
 }
@@ -519,7 +613,7 @@ struct Reg {
 
 struct Hello {
     cudaIpcMemHandle_t handle;
-    int32_t P, rank, device, channels, slots, threads;
+    int32_t P, rank, device, channels, slots, threads, stages, tile_bytes;
     int64_t slot_bytes, window_bytes;
     uint64_t bytes;   // registration size
 };
@@ -552,17 +646,21 @@ namespace {
 pr_comm_config default_config() {
     pr_comm_config c;
     c.channels = 16;
-    c.slots = 4;
+    c.slots = 8;
     c.threads = 512;
     c.flags = 0;
-    c.slot_bytes = 128 * 1024;
+    c.slot_bytes = 256 * 1024;
     c.watchdog_ns = 10ll * 1000 * 1000 * 1000;
+    c.stages = 6;
+    c.tile_bytes = 16384;
     return c;
 }
 
 int check_config(const pr_comm_config& c) {
     if ((c.flags & ~PR_COMM_FLAG_FORCE_STAGED) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
-        c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20))
+        c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
+        c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
+        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024)
         return PR_ERR_INVALID;
     return PR_OK;
 }
@@ -576,6 +674,8 @@ int alloc_common(pr_comm* c) {
     t.slots = c->cfg.slots;
     t.slot_bytes = c->cfg.slot_bytes;
     t.watchdog_ns = c->cfg.watchdog_ns;
+    t.stages = c->cfg.stages;
+    t.tile_bytes = c->cfg.tile_bytes;
     layout(t);
     PR_CUDA_TRY(cudaMalloc((void**)&c->win, t.window_bytes));
     PR_CUDA_TRY(cudaMemset(c->win, 0, t.window_bytes));
@@ -645,14 +745,23 @@ int find_reg(const pr_comm* c, const void* buf, size_t bytes, int32_t* id, int64
 
 size_t dtype_size(int32_t dt) { return dt == PR_DTYPE_F32 ? 4 : (dt == PR_DTYPE_BF16 ? 2 : 0); }
 
-int launch_ring(const LaunchArgs& a, int nranks, int32_t threads, int32_t channels, cudaStream_t s, bool coop) {
+int launch_ring(const LaunchArgs& a, int nranks, const pr_comm_config& cfg, cudaStream_t s, bool coop) {
+    const int32_t threads = cfg.threads, channels = cfg.channels;
     void* fn = (a.dtype == PR_DTYPE_F32) ? (void*)ring_kernel<float> : (void*)ring_kernel<__nv_bfloat16>;
+    const size_t smem = (size_t)cfg.stages * 2 * cfg.tile_bytes;
+    static size_t attr_set[2] = {0, 0};
+    const int di = a.dtype == PR_DTYPE_F32 ? 0 : 1;
+    if (attr_set[di] < smem) {
+        PR_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set[di] = smem;
+    }
     void* args[] = {(void*)&a};
-    const dim3 grid((unsigned)channels, (unsigned)nranks), block((unsigned)threads);
+    // producer warp + signal warp + `threads` consumer threads per channel CTA
+    const dim3 grid((unsigned)channels, (unsigned)nranks), block((unsigned)(threads + 64));
     if (coop) {
-        PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s));
+        PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, s));
     } else {
-        PR_CUDA_TRY(cudaLaunchKernel(fn, grid, block, args, 0, s));
+        PR_CUDA_TRY(cudaLaunchKernel(fn, grid, block, args, smem, s));
     }
     return PR_OK;
 }
@@ -676,6 +785,7 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
     }
     me.P = P; me.rank = rank; me.device = device; me.channels = c->cfg.channels; me.slots = c->cfg.slots;
     me.threads = c->cfg.threads; me.slot_bytes = c->cfg.slot_bytes; me.window_bytes = (int64_t)c->tab.window_bytes;
+    me.stages = c->cfg.stages; me.tile_bytes = c->cfg.tile_bytes;
     me.bytes = rc ? 1 : 0;   // error flag travels with the hello so every rank fails together
     std::vector<Hello> all(P);
     int xrc = exchange(c, &me, sizeof(Hello), all.data());
@@ -684,7 +794,7 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
         const Hello& h = all[q];
         if (h.bytes) rc = rc ? rc : PR_ERR_CUDA;
         if (h.P != P || h.rank != q || h.channels != me.channels || h.slots != me.slots || h.slot_bytes != me.slot_bytes ||
-            h.threads != me.threads)
+            h.threads != me.threads || h.stages != me.stages || h.tile_bytes != me.tile_bytes)
             rc = rc ? rc : PR_ERR_INVALID;
     }
     if (rc) { free_comm(c); return rc; }
@@ -816,7 +926,7 @@ extern "C" int pr_weighted_allreduce(pr_comm* c, void* d_buf, int64_t count, int
     a.calls[0].buf = d_buf;
     a.calls[0].n_local = n_local;
     find_reg(c, d_buf, (size_t)count * dtype_size(dt), &a.calls[0].reg_id, &a.calls[0].reg_off);
-    return launch_ring(a, 1, c->cfg.threads, c->cfg.channels, (cudaStream_t)stream, false);
+    return launch_ring(a, 1, c->cfg, (cudaStream_t)stream, false);
 }
 
 extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d_bufs, int64_t count, int32_t dt,
@@ -848,7 +958,7 @@ extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d
         find_reg(comms[r], d_bufs[r], 0, &a.calls[r].reg_id, &a.calls[r].reg_off);
     }
     PR_CUDA_TRY(cudaSetDevice(c0->device));
-    return launch_ring(a, P, c0->cfg.threads, c0->cfg.channels, (cudaStream_t)stream, true);
+    return launch_ring(a, P, c0->cfg, (cudaStream_t)stream, true);
 }
 
 extern "C" int pr_comm_allgather_f64(pr_comm* c, double local, double* out, void* stream) {

@@ -184,8 +184,8 @@ def test_staged_allgather_path():
             _check(P, L, "bf16", [3] * P, comms, seed=L)
 
 
-@pytest.mark.parametrize("cfg", [dict(channels=1, slots=2, slot_bytes=256), dict(channels=3, slots=3, slot_bytes=4096),
-                                 dict(channels=32, slots=8, slot_bytes=65536, threads=256),
+@pytest.mark.parametrize("cfg", [dict(channels=1, slots=2, slot_bytes=256, stages=2, tile_bytes=256), dict(channels=3, slots=3, slot_bytes=4096),
+                                 dict(channels=32, slots=8, slot_bytes=65536, threads=256, stages=4, tile_bytes=8192),
                                  dict(channels=3, slots=4, slot_bytes=1024, force_staged=True),
                                  dict(channels=2, slots=5, slot_bytes=512, threads=64)])
 def test_config_variants(cfg):

@@ -186,4 +186,4 @@ def test_spin_duration():
         e.record()
         e.synchronize()
         ms = s.elapsed_time(e)
-        assert ns / 1e6 * 0.99 <= ms <= ns / 1e6 * 1.02 + 0.015    # + launch latency
+        assert ns / 1e6 * 0.99 <= ms <= ns / 1e6 * 1.02 + 0.025    # + launch latency

@@ -1,0 +1,74 @@
+"""Run each library kernel in isolation at bench sizes (target for `ncu --set full`, one GPU).
+
+    python tools/profile_kernels.py [gather|gather_imagenet|shard|ring|all] [reps]
+
+gather          K2 at the bench step size: 1024 CIFAR rows (3,072 B u8 -> 6,144 B bf16)
+gather_imagenet K2 at the C3 fast-rank size: 336 ImageNet-shaped rows (150,528 B -> 301,056 B)
+shard           K1 over N = 1,281,167 (whole permutation)
+ring            K3, 8 ranks co-located on this GPU, 11,689,512 fp32 each (ResNet-18 gradients)
+Also prints CUDA-event timings (outside ncu these are the kernel's live durations).
+"""
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2111_08272_b200 as pr  # noqa: E402
+
+
+def timed(fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps * 1e3   # us
+
+
+def gather(rows, row_bytes, nsrc, reps, plane):
+    X = torch.randint(0, 256, (nsrc, row_bytes), dtype=torch.uint8, device="cuda")
+    Y = torch.randint(0, 10, (nsrc,), dtype=torch.int64, device="cuda")
+    idx = torch.randperm(nsrc, device="cuda")[:rows].contiguous()
+    out = torch.empty((rows, row_bytes), dtype=torch.bfloat16, device="cuda")
+    lab = torch.empty(rows, dtype=torch.int64, device="cuda")
+    op = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE, [0.02, 0.02, 0.02], [120.0, 120.0, 110.0], plane)
+    us = timed(lambda: pr.gather_rows(X, nsrc, row_bytes, idx, rows, out, op, Y, lab), reps)
+    byts = rows * (3 * row_bytes + 24)
+    print(f"gather rows={rows} row_bytes={row_bytes}: {us:.2f} us, {byts / us / 1e3:.1f} GB/s algorithmic")
+
+
+def shard(reps):
+    N = 1281167
+    out = torch.empty(N, dtype=torch.int64, device="cuda")
+    us = timed(lambda: pr.permute(N, 1234, 3, 0, N, out), reps)
+    print(f"permute N={N}: {us:.2f} us, {N / us:.1f} M indices/s")
+
+
+def ring(reps, P=8, L=11_689_512):
+    comms = pr.comm_init_local(P, 0, pr.comm_config())
+    bufs = [torch.randn(L, device="cuda") for _ in range(P)]
+    n = [64, 64, 64, 64, 128, 128, 256, 256][:P]
+    us = timed(lambda: pr.weighted_allreduce_local(comms, bufs, n), reps)
+    byts = (6 + 5 * (P - 2)) * L * 4
+    print(f"ring P={P} L={L}: {us:.1f} us, {byts / us / 1e3:.1f} GB/s algorithmic HBM (all ranks)")
+    for c in comms:
+        c.destroy()
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    if what in ("gather", "all"):
+        gather(1024, 3072, 50000, reps, 1024)
+    if what in ("gather_imagenet", "all"):
+        gather(336, 150528, 2000, reps, 50176)
+    if what in ("shard", "all"):
+        shard(reps)
+    if what in ("ring", "all"):
+        ring(reps)
