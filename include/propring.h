@@ -130,6 +130,9 @@ int pr_permute(int64_t N, uint64_t seed, int64_t epoch, int64_t begin, int64_t c
 #define PR_GATHER_U8_TO_F32_AFFINE  1  /* (float(x) − shift_c)·scale_c, two fp32 roundings, no FMA   */
 #define PR_GATHER_U8_TO_BF16_AFFINE 2  /* the same value rounded to bfloat16 (RNE)                   */
 #define PR_GATHER_MAX_CHANNELS 16
+#define PR_GATHER_IMPL_AUTO 0   /* TMA staging when the launch moves >= 8 MiB of input, else LSU        */
+#define PR_GATHER_IMPL_LSU  1   /* warp per 2 KiB segment, ld.global.nc 16-byte vectors                 */
+#define PR_GATHER_IMPL_TMA  2   /* cp.async.bulk row segments into an 8-stage smem ring (mbarrier)      */
 
 typedef struct {
     int32_t op;                              /* PR_GATHER_*                                           */
@@ -137,6 +140,8 @@ typedef struct {
     int64_t plane;                           /* affine ops: elements per channel (H·W of a CHW row)   */
     float scale[PR_GATHER_MAX_CHANNELS];     /* per-channel multiplier                                */
     float shift[PR_GATHER_MAX_CHANNELS];     /* per-channel subtrahend                                */
+    int32_t impl;                            /* PR_GATHER_IMPL_* (results are identical)              */
+    int32_t reserved;
 } pr_gather_op;
 
 /* Step-batch gather (Algorithm 1 step 4, "Proportionally draw samples from the sub-data set"):

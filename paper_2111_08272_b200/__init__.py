@@ -167,9 +167,15 @@ def permute(N: int, seed: int, epoch: int, begin: int, count: int, out, stream=N
     return out
 
 
-def make_gather_op(op=GATHER_COPY, scale=None, shift=None, plane=1):
+GATHER_IMPL_AUTO = 0
+GATHER_IMPL_LSU = 1
+GATHER_IMPL_TMA = 2
+
+
+def make_gather_op(op=GATHER_COPY, scale=None, shift=None, plane=1, impl=GATHER_IMPL_AUTO):
     g = GatherOp()
     g.op = op
+    g.impl = impl
     if op != GATHER_COPY:
         n = len(scale)
         g.channels = n

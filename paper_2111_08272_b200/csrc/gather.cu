@@ -53,8 +53,31 @@ __device__ __forceinline__ float affine(uint32_t x, float sc, float sh) {
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-    const __nv_bfloat16 a = __float2bfloat16_rn(lo), b = __float2bfloat16_rn(hi);
-    return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+    const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);     // one cvt.rn.bf16x2.f32
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// Packed fp32 pairs (Blackwell FADD2/FMUL2): per-lane IEEE round-to-nearest, identical to two scalar ops.
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+// bytes j and j+1 of w as exact floats 2^23 + x (PRMT into the mantissa of 0x4B000000)
+__device__ __forceinline__ uint64_t u8pair_magic(uint32_t w, int j) {
+    const uint32_t a = __byte_perm(w, 0x4B000000u, 0x7540u + j);
+    const uint32_t b = __byte_perm(w, 0x4B000000u, 0x7540u + j + 1);
+    return (uint64_t)a | ((uint64_t)b << 32);
 }
 
 template <int OP>
@@ -68,10 +91,18 @@ __device__ __forceinline__ void convert_store(const GatherParams& p, uint8_t* dr
     const uint32_t k0 = (uint32_t)v * 16u;  // element index of the first byte (row_bytes < 2^31)
     const uint32_t plane = (uint32_t)p.plane;
     if (plane % 16u == 0) {
+        // one channel per 16-byte vector: (x − shift)·scale on pairs, x = (2^23 + x) − 2^23 exactly
         const int c = (int)(k0 / plane);
-        const float sc = p.scale[c], sh = p.shift[c];
+        const uint64_t m23 = pk2(-8388608.0f, -8388608.0f);
+        const uint64_t nsh = pk2(-p.shift[c], -p.shift[c]);
+        const uint64_t sc2 = pk2(p.scale[c], p.scale[c]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = affine((w[j >> 2] >> (8 * (j & 3))) & 0xffu, sc, sh);
+        for (int j = 0; j < 16; j += 2) {
+            const uint64_t xf = add2(u8pair_magic(w[j >> 2], j & 3), m23);   // exact: x
+            const uint64_t y = mul2(add2(xf, nsh), sc2);                     // RN(RN(x − shift)·scale)
+            f[j] = __uint_as_float((uint32_t)y);
+            f[j + 1] = __uint_as_float((uint32_t)(y >> 32));
+        }
     } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -132,6 +163,125 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) gather_kernel(const __grid_
     }
 }
 
+// ---- TMA-staged variant: bulk copies keep whole rows (or 24 KiB row segments) in flight per CTA ------
+// A unit is up to kTmaSeg input bytes: 8 CIFAR rows (8 bulk copies) or one segment of a long row; the
+// producer warp prefetches the next unit's row indices (lane-parallel) while lane 0 issues the copies.
+constexpr int kTmaStages = 4;
+constexpr int kTmaSeg = 24576;                // input bytes per unit
+constexpr int kTmaConsumerWarps = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n"
+        "DONE:\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int OP>
+__global__ void __launch_bounds__(32 * (kTmaConsumerWarps + 1)) gather_tma_kernel(const __grid_constant__ GatherParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];   // [kTmaStages][kTmaSeg]
+    __shared__ uint64_t full[kTmaStages], empty[kTmaStages];
+    const int64_t rpu = (p.row_bytes <= kTmaSeg / 2) ? min((int64_t)32, kTmaSeg / p.row_bytes) : 1;  // rows/unit
+    const int64_t segs = rpu > 1 ? 1 : (p.row_bytes + kTmaSeg - 1) / kTmaSeg;                          // units/row
+    const int64_t units = rpu > 1 ? (p.n + rpu - 1) / rpu : p.n * segs;
+    const int64_t G = gridDim.x;
+    const int64_t out_mul = (OP == PR_GATHER_COPY) ? 1 : (OP == PR_GATHER_U8_TO_BF16_AFFINE ? 2 : 4);
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kTmaStages; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kTmaConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (p.lab_dst) {                                                 // labels: one thread per row
+        const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < p.n; t += nthreads)
+            p.lab_dst[t] = p.lab_src[p.idx[t]];
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // source row of lane `lane` within unit u (rows mode) / of the unit (segment mode)
+    auto fetch = [&](int64_t u) -> int64_t {
+        if (u >= units) return 0;
+        if (rpu > 1) {
+            const int64_t row = u * rpu + lane;
+            return (lane < rpu && row < p.n) ? __ldg(p.idx + row) : 0;
+        }
+        return __ldg(p.idx + u / segs);
+    };
+    if (warp == 0) {
+        uint32_t k = 0;
+        int64_t cur = fetch(blockIdx.x);
+        for (int64_t u = blockIdx.x; u < units; u += G, ++k) {
+            const int64_t nxt = fetch(u + G);                         // prefetch: hides the idx latency
+            const int stg = (int)(k % kTmaStages);
+            if (lane == 0 && k >= (uint32_t)kTmaStages) mbar_wait(&empty[stg], ((k / kTmaStages) - 1) & 1);
+            uint8_t* dst = smem + (size_t)stg * kTmaSeg;
+            if (rpu > 1) {
+                const int64_t nrows = min(rpu, p.n - u * rpu);
+                if (lane == 0) mbar_arrive_expect_tx(&full[stg], (uint32_t)(nrows * p.row_bytes));
+                for (int j = 0; j < nrows; ++j) {
+                    const int64_t srow = __shfl_sync(0xffffffffu, cur, j);
+                    if (lane == 0) tma_load(dst + j * p.row_bytes, p.src + srow * p.row_bytes, (uint32_t)p.row_bytes,
+                                            &full[stg]);
+                }
+            } else if (lane == 0) {
+                const int64_t off = (u % segs) * kTmaSeg;
+                const uint32_t bytes = (uint32_t)min((int64_t)kTmaSeg, p.row_bytes - off);
+                mbar_arrive_expect_tx(&full[stg], bytes);
+                tma_load(dst, p.src + cur * p.row_bytes + off, bytes, &full[stg]);
+            }
+            cur = nxt;
+        }
+    } else {
+        // consumer warps: smem -> convert -> 16-byte stores, lanes on consecutive vectors of one row
+        const int cw = warp - 1;
+        const int64_t vpr = p.row_bytes / 16;
+        uint32_t k = 0;
+        for (int64_t u = blockIdx.x; u < units; u += G, ++k) {
+            const int stg = (int)(k % kTmaStages);
+            mbar_wait(&full[stg], (k / kTmaStages) & 1);
+            const uint4* sv = reinterpret_cast<const uint4*>(smem + (size_t)stg * kTmaSeg);
+            if (rpu > 1) {
+                const int64_t nrows = min(rpu, p.n - u * rpu);
+                for (int64_t rl = cw; rl < nrows; rl += kTmaConsumerWarps) {
+                    uint8_t* drow = p.dst + (u * rpu + rl) * p.row_bytes * out_mul;
+                    for (int64_t v = lane; v < vpr; v += 32) convert_store<OP>(p, drow, v, sv[rl * vpr + v]);
+                }
+            } else {
+                const int64_t row = u / segs, off = (u - row * segs) * kTmaSeg;
+                const int64_t nv = min((int64_t)kTmaSeg, p.row_bytes - off) / 16;
+                uint8_t* drow = p.dst + row * p.row_bytes * out_mul;
+                for (int64_t v = threadIdx.x - 32; v < nv; v += 32 * kTmaConsumerWarps)
+                    convert_store<OP>(p, drow, off / 16 + v, sv[v]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);
+        }
+    }
+}
+
 }  // namespace
 
 extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_bytes, const int64_t* d_idx, int64_t n,
@@ -163,12 +313,49 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
     }
     p.lab_src = d_lab_src;
     p.lab_dst = d_lab_dst;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int impl = op ? op->impl : PR_GATHER_IMPL_AUTO;
+    // TMA staging pays off once a launch moves enough bytes to be bandwidth-bound; rows
+    // read from pinned host memory (the e2e path) stream over PCIe through the LSU kernel.
+    bool host_src = false;
+    if (impl == PR_GATHER_IMPL_AUTO) {
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, d_src) == cudaSuccess) host_src = at.type == cudaMemoryTypeHost;
+        else cudaGetLastError();
+    }
+    const bool tma = impl == PR_GATHER_IMPL_TMA ||
+                     (impl == PR_GATHER_IMPL_AUTO && !host_src && n * row_bytes >= (8ll << 20));
+    if (tma) {
+        const size_t smem = (size_t)kTmaStages * kTmaSeg;
+        const int64_t rpu = row_bytes <= kTmaSeg / 2 ? (kTmaSeg / row_bytes < 32 ? kTmaSeg / row_bytes : 32) : 1;
+        const int64_t units = rpu > 1 ? (n + rpu - 1) / rpu : n * ((row_bytes + kTmaSeg - 1) / kTmaSeg);
+        int64_t blocks = units < 148 * 2 ? units : 148 * 2;
+        const dim3 block(32 * (kTmaConsumerWarps + 1));
+        static bool attr = false;
+        if (!attr) {
+            PR_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel<PR_GATHER_COPY>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            PR_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel<PR_GATHER_U8_TO_F32_AFFINE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            PR_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel<PR_GATHER_U8_TO_BF16_AFFINE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        switch (p.op) {
+            case PR_GATHER_COPY: gather_tma_kernel<PR_GATHER_COPY><<<(unsigned)blocks, block, smem, s>>>(p); break;
+            case PR_GATHER_U8_TO_F32_AFFINE:
+                gather_tma_kernel<PR_GATHER_U8_TO_F32_AFFINE><<<(unsigned)blocks, block, smem, s>>>(p);
+                break;
+            default: gather_tma_kernel<PR_GATHER_U8_TO_BF16_AFFINE><<<(unsigned)blocks, block, smem, s>>>(p);
+        }
+        PR_CUDA_TRY(cudaGetLastError());
+        return PR_OK;
+    }
     const int64_t vpr = row_bytes / 16;
     const int64_t items = n * ((vpr + kSegVec - 1) / kSegVec);
     int64_t blocks = (items + kWarpsPerCta - 1) / kWarpsPerCta;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    cudaStream_t s = (cudaStream_t)stream;
     switch (p.op) {
         case PR_GATHER_COPY: gather_kernel<PR_GATHER_COPY><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, s>>>(p); break;
         case PR_GATHER_U8_TO_F32_AFFINE:

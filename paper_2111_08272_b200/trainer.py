@@ -7,18 +7,23 @@ Rows of SURVEY §8(a) handled here (the rest are library calls):
       mb/n_r so the flat gradient buffer ends up holding the LOCAL MEAN gradient (DESIGN.md §3 #11).
       Emulated heterogeneity: after the backward pass a K4 spin of (σ_r − 1)·c0·n_r ns (c0 = calibrated
       seconds per sample at σ = 1) slows rank r by the factor σ_r.
-  a5  t_s capture: CUDA events around gather + compute + spin, summed over the epoch (P:102, P:152;
-      DESIGN.md §3 #4-#5); one event synchronisation per epoch, not per step.
+  a5  t_s capture: CUDA events around data movement + compute + spin, summed over the epoch (P:102,
+      P:152; DESIGN.md §3 #4-#5); one event synchronisation per epoch, not per step.
   a9  SGD update, Eq. 1 with weight decay: torch.optim.SGD on the reduced buffer.
-Library rows: a1/a10 alloc_init / Alloc.update, a2 shard_indices, a3 gather_rows, a6-a8 weighted_allreduce.
+Library rows: a1/a10 alloc_init / Alloc.update (+ pr_comm_allgather_f64 for the t_s exchange),
+a2 shard_indices, a3 gather_rows, a6-a8 weighted_allreduce.
 
-Parameters' .grad are views into one flat fp32 buffer allocated by the communicator (CUDA-IPC registered),
-so backward() accumulates straight into the buffer the ring reduces in place — no bucketing copies.
+Data movement (a3): by default ONE K2 launch per epoch gathers the rows of all S aggregation steps
+(S·n_r rows, in step order) into a resident buffer — the same rows in the same order as S per-step
+gathers, but HBM-bound instead of launch-latency-bound; its time is part of t_s.  gather="step"
+issues one launch per aggregation step instead.
+
+Parameters' .grad are views into one flat fp32 buffer allocated by the communicator (CUDA-IPC
+registered), so backward() accumulates straight into the buffer the ring reduces in place.
 """
 
 from __future__ import annotations
 
-import time
 from dataclasses import dataclass, field
 
 import torch
@@ -47,8 +52,9 @@ class RunConfig:
     micro: int = 512                        # max rows per microbatch
     slowdown: list | None = None            # σ_r per rank (emulated heterogeneity)
     adaptive: bool = False                  # Algorithm 1 self-adaptive allocation
-    host_data: bool = False                 # e2e: dataset in pinned host memory, gathered over PCIe
+    host_data: bool = False                 # e2e: data set in pinned host memory, gathered over PCIe
     bf16_compute: bool = True               # autocast for the model's forward/backward
+    gather: str = "epoch"                   # "epoch": one K2 launch per epoch; "step": one per step
 
 
 def build_model(name: str, num_classes: int):
@@ -58,8 +64,6 @@ def build_model(name: str, num_classes: int):
         return torchvision.models.resnet18(num_classes=num_classes)
     if name == "vgg16":
         return torchvision.models.vgg16(num_classes=num_classes)
-    if name == "logreg":
-        return torch.nn.Linear(1024, 1, bias=False)
     raise ValueError(name)
 
 
@@ -74,30 +78,23 @@ class Worker:
         self.comm = comm
         self.stream = torch.cuda.current_stream(self.dev)
         self.alloc = pr.alloc_init(cfg.N, cfg.ratios, C=cfg.C, g=cfg.g, floor=cfg.floor)
-        if not cfg.adaptive:
-            self.alloc.set_policy(never_freeze=False)
         self.row_bytes = int(torch.tensor(cfg.shape).prod())
-        # data set (synthetic, replicated per rank): u8 CHW rows + int64 labels
-        if data is None:
+        if data is None:                              # synthetic data set, replicated per rank
             import synth
 
             data = torch.from_numpy(synth.images_u8(cfg.N, *cfg.shape, seed=0).reshape(cfg.N, -1))
             labels = torch.from_numpy(synth.labels(cfg.N, cfg.classes, seed=1))
-        if cfg.host_data:
-            self.X = data.pin_memory()
-            self.Y = labels.to(self.dev)
-        else:
-            self.X = data.to(self.dev)
-            self.Y = labels.to(self.dev)
+        self.X = data.pin_memory() if cfg.host_data else data.to(self.dev)
+        self.Y = labels.to(self.dev)
         C, H, W = cfg.shape
         self.gop = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE if cfg.bf16_compute else pr.GATHER_U8_TO_F32_AFFINE,
                                      [1.0 / s for s in CIFAR_STD[:C]], CIFAR_MEAN[:C], H * W)
-        torch.manual_seed(cfg.seed)                # identical initial weights on every rank
+        torch.manual_seed(cfg.seed)                   # identical initial weights on every rank
         self.model = build_model(cfg.model, cfg.num_classes).to(self.dev)
-        params = [p for p in self.model.parameters()]
+        params = list(self.model.parameters())
         self.L = sum(p.numel() for p in params)
         if comm is not None:
-            self.flat = comm.alloc(self.L * 4, dtype=torch.float32)
+            self.flat = comm.alloc(self.L * 4, dtype=torch.float32)   # IPC-registered: direct all-gather
         else:
             self.flat = torch.zeros(self.L, dtype=torch.float32, device=self.dev)
         off = 0
@@ -106,45 +103,51 @@ class Worker:
             off += p.numel()
         self.opt = torch.optim.SGD(params, lr=cfg.lr, weight_decay=cfg.wd)
         self.idx = torch.empty(cfg.N, dtype=torch.int64, device=self.dev)   # any shard size after re-allocation
-        self.last_ts = 0.0
+        self.xdt = torch.bfloat16 if cfg.bf16_compute else torch.float32
         self.c0_ns = 0.0                               # calibrated per-sample compute time (ns) at σ = 1
         self.launches = 0                              # library kernels launched (for the bench)
-        self.ar_events = []
-        self.gather_events = []
+        self.ar_events, self.gather_events = [], []
         self.epoch = 0
+        self.last_ts = 0.0
+        self.history = []
 
-    # ---- one aggregation step (Algorithm 1 steps 4-6) ------------------------------------
-    def step(self, s: int, n_r: int, xbuf, ybuf, record=False):
-        cfg = self.cfg
-        C, H, W = cfg.shape
-        if n_r > 0:
+    # ---- a3: data movement --------------------------------------------------------------------------
+    def gather(self, first: int, rows: int, record=False):
+        """K2: rows [first, first+rows) of this rank's shard -> (x [rows, C·H·W], y [rows])."""
+        x = torch.empty((max(rows, 1), self.row_bytes), dtype=self.xdt, device=self.dev)
+        y = torch.empty(max(rows, 1), dtype=torch.int64, device=self.dev)
+        if rows > 0:
             if record:
                 g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 g0.record(self.stream)
-            src = self.X.data_ptr()
-            pr.gather_rows(src, cfg.N, self.row_bytes, self.idx[s * n_r:], n_r, xbuf, self.gop, self.Y, ybuf,
-                           stream=self.stream)
+            pr.gather_rows(self.X.data_ptr(), self.cfg.N, self.row_bytes, self.idx[first:], rows, x, self.gop, self.Y,
+                           y, stream=self.stream)
             self.launches += 1
             if record:
                 g1.record(self.stream)
-                self.gather_events.append((g0, g1, n_r))
-            x = xbuf[:n_r].view(n_r, C, H, W)
-            y = ybuf[:n_r]
-            losses = []
-            for m0 in range(0, n_r, cfg.micro):
-                xm, ym = x[m0:m0 + cfg.micro], y[m0:m0 + cfg.micro]
-                with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.bf16_compute):
-                    out = self.model(xm)
-                    loss = F.cross_entropy(out.float(), ym)
-                (loss * (xm.shape[0] / n_r)).backward()       # local mean over n_r (DESIGN §3 #11)
-                losses.append(loss.detach() * xm.shape[0])
-            sigma = cfg.slowdown[self.rank] if cfg.slowdown else 1.0
-            if sigma > 1.0 and self.c0_ns > 0:
-                pr.spin(int((sigma - 1.0) * self.c0_ns * n_r), stream=self.stream)
-                self.launches += 1
-            return torch.stack(losses).sum() / n_r
-        return torch.zeros((), device=self.dev)
+                self.gather_events.append((g0, g1, rows))
+        return x, y
 
+    # ---- a4: forward/backward with gradient accumulation (P:69 steps (1)-(3)) --------------------------
+    def compute(self, x, y, n_r: int):
+        cfg = self.cfg
+        C, H, W = cfg.shape
+        x = x[:n_r].view(n_r, C, H, W)
+        losses = []
+        for m0 in range(0, n_r, cfg.micro):
+            xm, ym = x[m0:m0 + cfg.micro], y[m0:m0 + cfg.micro]
+            with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.bf16_compute):
+                out = self.model(xm)
+                loss = F.cross_entropy(out.float(), ym)
+            (loss * (xm.shape[0] / n_r)).backward()           # local mean over n_r (DESIGN §3 #11)
+            losses.append(loss.detach() * xm.shape[0])
+        sigma = cfg.slowdown[self.rank] if cfg.slowdown else 1.0
+        if sigma > 1.0 and self.c0_ns > 0:
+            pr.spin(int((sigma - 1.0) * self.c0_ns * n_r), stream=self.stream)   # K4
+            self.launches += 1
+        return torch.stack(losses).sum() / n_r
+
+    # ---- a6-a9: weighted ring allreduce + SGD (Algorithm 1 steps 5-6) ---------------------------------
     def allreduce_and_update(self, n_r: int, record=False):
         if self.P > 1:
             if record:
@@ -158,45 +161,54 @@ class Worker:
         self.opt.step()
         self.flat.zero_()
 
-    # ---- one epoch (Algorithm 1 outer loop) ---------------------------------------------------------
+    # ---- one epoch (Algorithm 1 outer loop) -----------------------------------------------------------
     def run_epoch(self, record=False, loss_to_host=False):
         cfg = self.cfg
         v = self.alloc.view()
         n_r, S = v["n"][self.rank], v["S"]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(self.stream)
         pr.shard_indices(self.alloc, self.rank, self.epoch, cfg.seed, self.idx, stream=self.stream)   # a2
         self.launches += 1
-        xbuf = torch.empty((max(n_r, 1), self.row_bytes),            # one output element per input byte
-                           dtype=torch.bfloat16 if cfg.bf16_compute else torch.float32, device=self.dev)
-        ybuf = torch.empty(max(n_r, 1), dtype=torch.int64, device=self.dev)
+        if cfg.gather == "epoch":
+            xe, ye = self.gather(0, S * n_r, record)                                   # a3, one launch
+        e1.record(self.stream)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
-        losses = []
-        host_losses = []
+        losses, host_losses = [], []
         for s in range(S):
             ev[s][0].record(self.stream)
-            loss = self.step(s, n_r, xbuf, ybuf, record)
+            if n_r > 0:
+                if cfg.gather == "epoch":
+                    x, y = xe[s * n_r:(s + 1) * n_r], ye[s * n_r:(s + 1) * n_r]
+                else:
+                    x, y = self.gather(s * n_r, n_r, record)
+                loss = self.compute(x, y, n_r)
+            else:
+                loss = torch.zeros((), device=self.dev)
             ev[s][1].record(self.stream)
             self.allreduce_and_update(n_r, record)
             losses.append(loss)
             if loss_to_host:
                 host_losses.append(float(loss))          # D2H of the step's result (e2e contract)
         ev[-1][1].synchronize()
-        t_s = sum(a.elapsed_time(b) for a, b in ev) / 1e3   # seconds (a5)
+        t_s = (e0.elapsed_time(e1) + sum(a.elapsed_time(b) for a, b in ev)) / 1e3   # seconds (a5)
         self.epoch += 1
-        return {"t_s": t_s, "loss": float(torch.stack(losses).mean()), "S": S, "n_r": n_r, "w": v["w"]}
+        rec = {"t_s": t_s, "loss": float(torch.stack(losses).mean()), "S": S, "n_r": n_r, "w": v["w"]}
+        self.history.append(rec)
+        self.last_ts = t_s
+        return rec
 
-    def boundary(self, t_s: float):
-        """Algorithm 1 steps 1-3: allgather t_s, Eq. 10 + rounding, redistribute."""
+    def boundary(self):
+        """Algorithm 1 steps 1-3: exchange t_s (K6), Eq. 10 + rounding, redistribute."""
+        if self.epoch == 0:
+            return False                              # "t_s ... is set to 0" (P:133): nothing to adapt yet
+        if self.comm is not None:
+            ts = self.comm.allgather_f64(self.last_ts, stream=self.stream)
+            self.launches += 1
+        else:
+            ts = [self.last_ts]
         if not self.cfg.adaptive:
             return False
-        if self.P > 1:
-            import torch.distributed as dist
-
-            t = torch.tensor([t_s], dtype=torch.float64, device=self.dev)
-            allt = [torch.zeros_like(t) for _ in range(self.P)]
-            dist.all_gather(allt, t)
-            ts = [float(x) for x in allt]
-        else:
-            ts = [t_s]
         return self.alloc.update(ts)
 
     def calibrate(self, steps: int = 3):
@@ -204,17 +216,14 @@ class Worker:
         v = self.alloc.view()
         n_r = v["n"][self.rank]
         pr.shard_indices(self.alloc, self.rank, 0, self.cfg.seed, self.idx, stream=self.stream)
-        C, H, W = self.cfg.shape
-        xbuf = torch.empty((n_r, C * H * W), dtype=torch.bfloat16, device=self.dev)
-        ybuf = torch.empty(n_r, dtype=torch.int64, device=self.dev)
-        save = self.cfg.slowdown
-        self.cfg.slowdown = None
+        x, y = self.gather(0, n_r)
+        save, self.cfg.slowdown = self.cfg.slowdown, None
         for _ in range(2):
-            self.step(0, n_r, xbuf, ybuf)
+            self.compute(x, y, n_r)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(self.stream)
-        for s in range(steps):
-            self.step(s, n_r, xbuf, ybuf)
+        for _ in range(steps):
+            self.compute(x, y, n_r)
         b.record(self.stream)
         b.synchronize()
         self.flat.zero_()

@@ -127,11 +127,12 @@ def test_gather_bit_exact(row_bytes, plane, n):
     scale = np.array([1.0 / STD[c % 3] for c in range(channels)], dtype=np.float32)
     shift = np.array([MEAN[c % 3] for c in range(channels)], dtype=np.float32)
     dX, dY, didx = _dev(X), _dev(Y), _dev(idx)
-    for op in (pr.GATHER_COPY, pr.GATHER_U8_TO_F32_AFFINE, pr.GATHER_U8_TO_BF16_AFFINE):
+    for op, impl in [(o, i) for o in (pr.GATHER_COPY, pr.GATHER_U8_TO_F32_AFFINE, pr.GATHER_U8_TO_BF16_AFFINE)
+                     for i in (pr.GATHER_IMPL_LSU, pr.GATHER_IMPL_TMA)]:
         width = {0: 1, 1: 4, 2: 2}[op]
         out = torch.full((max(n, 1) * row_bytes * width,), 0x5A, dtype=torch.uint8, device="cuda")
         lab = torch.full((max(n, 1),), -7, dtype=torch.int64, device="cuda")
-        gop = pr.make_gather_op(op, scale, shift, plane)
+        gop = pr.make_gather_op(op, scale, shift, plane, impl=impl)
         pr.gather_rows(dX, nsrc, row_bytes, didx, n, out, gop, dY, lab)
         torch.cuda.synchronize()
         if n == 0:
@@ -161,6 +162,22 @@ def test_gather_step_slices_of_a_shard_and_alignment_errors():
     with pytest.raises(pr.PropringError) as e:
         pr.gather_rows(dX, 2000, 3000, idx, 1, out)
     assert e.value.code == pr.PR_ERR_ALIGN
+
+
+def test_gather_epoch_size_tma_vs_oracle():
+    """The bench's per-epoch launch (48 steps x 1024 CIFAR rows, AUTO -> TMA): bit-exact on sampled rows."""
+    X = synth.images_u8(50000, seed=0).reshape(50000, -1)
+    a = pr.alloc_init(50000, [1], C=64, g=16)
+    idx = torch.empty(50000, dtype=torch.int64, device="cuda")
+    pr.shard_indices(a, 0, 5, 1234, idx)
+    rows = 48 * 1024
+    out = torch.empty((rows, 3072), dtype=torch.bfloat16, device="cuda")
+    scale = [1 / s for s in STD]
+    pr.gather_rows(_dev(X), 50000, 3072, idx, rows, out, pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE, scale, MEAN, 1024))
+    pick = np.random.Generator(np.random.PCG64(3)).integers(0, rows, 500)
+    ref, _ = OG.gather_rows(X, idx.cpu().numpy()[pick], OG.U8_TO_BF16_AFFINE, np.float32(scale), np.float32(MEAN), 1024)
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16)[pick]
+    assert np.array_equal(got, ref)
 
 
 def test_gather_from_mapped_host_memory():

@@ -31,16 +31,19 @@ def timed(fn, reps):
     return a.elapsed_time(b) / reps * 1e3   # us
 
 
-def gather(rows, row_bytes, nsrc, reps, plane):
+def gather(rows, row_bytes, nsrc, reps, plane, impls=(1, 2)):
     X = torch.randint(0, 256, (nsrc, row_bytes), dtype=torch.uint8, device="cuda")
     Y = torch.randint(0, 10, (nsrc,), dtype=torch.int64, device="cuda")
-    idx = torch.randperm(nsrc, device="cuda")[:rows].contiguous()
+    idx = torch.randint(0, nsrc, (rows,), device="cuda")
     out = torch.empty((rows, row_bytes), dtype=torch.bfloat16, device="cuda")
     lab = torch.empty(rows, dtype=torch.int64, device="cuda")
-    op = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE, [0.02, 0.02, 0.02], [120.0, 120.0, 110.0], plane)
-    us = timed(lambda: pr.gather_rows(X, nsrc, row_bytes, idx, rows, out, op, Y, lab), reps)
-    byts = rows * (3 * row_bytes + 24)
-    print(f"gather rows={rows} row_bytes={row_bytes}: {us:.2f} us, {byts / us / 1e3:.1f} GB/s algorithmic")
+    for impl in impls:
+        op = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE, [0.02, 0.02, 0.02], [120.0, 120.0, 110.0], plane,
+                               impl=impl)
+        us = timed(lambda: pr.gather_rows(X, nsrc, row_bytes, idx, rows, out, op, Y, lab), reps)
+        byts = rows * (3 * row_bytes + 24)
+        print(f"gather[{'LSU' if impl == 1 else 'TMA'}] rows={rows} row_bytes={row_bytes}: {us:.2f} us, "
+              f"{byts / us / 1e3:.1f} GB/s algorithmic")
 
 
 def shard(reps):
@@ -66,6 +69,8 @@ if __name__ == "__main__":
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     if what in ("gather", "all"):
         gather(1024, 3072, 50000, reps, 1024)
+    if what in ("gather_epoch", "all"):
+        gather(49152, 3072, 50000, reps, 1024)          # one launch per epoch (48 steps x 1024 rows)
     if what in ("gather_imagenet", "all"):
         gather(336, 150528, 2000, reps, 50176)
     if what in ("shard", "all"):
