@@ -126,9 +126,18 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    # PR_BENCH_SHARED_GPU=1: every rank on cuda:0 with a gloo group — a functional check of the N>1 path
+    # on a one-GPU box (timings are then meaningless: the ranks time-share one GPU)
+    shared = os.environ.get("PR_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
+    tdev = "cpu" if shared else "cuda"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = pr.comm_init(rank, world, local) if world > 1 else None
     cfg = RunConfig(N=N_DATA, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024)
     wk = Worker(cfg, rank, world, local, comm)
@@ -165,7 +174,7 @@ def run_ours(args):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t)
     launches = wk.launches
@@ -219,7 +228,7 @@ def run_ours(args):
         barrier()
         hms = h0.elapsed_time(h1)
         if world > 1:
-            t = torch.tensor([hms], device="cuda")
+            t = torch.tensor([hms], device=tdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             hms = float(t)
         v = wk_h.alloc.view()
