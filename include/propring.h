@@ -132,7 +132,10 @@ int pr_permute(int64_t N, uint64_t seed, int64_t epoch, int64_t begin, int64_t c
 #define PR_GATHER_MAX_CHANNELS 16
 #define PR_GATHER_IMPL_AUTO 0   /* TMA staging when the launch moves >= 8 MiB of input, else LSU        */
 #define PR_GATHER_IMPL_LSU  1   /* warp per 2 KiB segment, ld.global.nc 16-byte vectors                 */
-#define PR_GATHER_IMPL_TMA  2   /* cp.async.bulk row segments into an 8-stage smem ring (mbarrier)      */
+#define PR_GATHER_IMPL_TMA  2   /* cp.async.bulk rows / segments into a 4-stage smem ring (mbarrier)    */
+#define PR_GATHER_LAYOUT_CHW 0  /* output row in the input's channel-major order                        */
+#define PR_GATHER_LAYOUT_HWC 1  /* channels-last output: element (c, p) at p·channels + c; needs
+                                   channels <= 4 and plane % 16 == 0 (both kernels)                     */
 
 typedef struct {
     int32_t op;                              /* PR_GATHER_*                                           */
@@ -141,7 +144,7 @@ typedef struct {
     float scale[PR_GATHER_MAX_CHANNELS];     /* per-channel multiplier                                */
     float shift[PR_GATHER_MAX_CHANNELS];     /* per-channel subtrahend                                */
     int32_t impl;                            /* PR_GATHER_IMPL_* (results are identical)              */
-    int32_t reserved;
+    int32_t layout;                          /* PR_GATHER_LAYOUT_* of the output row (affine ops)     */
 } pr_gather_op;
 
 /* Step-batch gather (Algorithm 1 step 4, "Proportionally draw samples from the sub-data set"):

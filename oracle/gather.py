@@ -10,6 +10,7 @@ data-plane details, so the operation is build-defined (DESIGN.md §3 #38, SURVEY
   U8_TO_F32_AFFINE   (float32(x) − shift_c) · scale_c, two separately rounded fp32 operations (no FMA)
   U8_TO_BF16_AFFINE  the same fp32 value, then round-to-nearest-even to bfloat16
   channel c = k // plane for element k of a CHW row (plane = H·W)
+  layout "hwc" (channels-last output): element (c, p) of the row is stored at p·C + c
 
 Pins: COPY is the identity on bytes; the affine value is within 0.5 ulp(fp32) of each rounding of the
 exact fp64 value; RNE-to-bf16 agrees with torch's CPU float32->bfloat16 conversion (a library routine).
@@ -44,8 +45,9 @@ def bf16_bits_to_f32(bits):
     return (np.asarray(bits, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
 
 
-def gather_rows(X, idx, op: int = COPY, scale=None, shift=None, plane: int = 1, Y=None):
-    """Gather rows X[idx] and apply `op`.  X: [N, R] (uint8 for the affine ops).  Returns (out, lab)."""
+def gather_rows(X, idx, op: int = COPY, scale=None, shift=None, plane: int = 1, Y=None, layout: str = "chw"):
+    """Gather rows X[idx] and apply `op`.  X: [N, R] (uint8 for the affine ops).  Returns (out, lab).
+    layout="hwc": the affine output row is stored channels-last (element (c, p) at p·C + c)."""
     X = np.asarray(X)
     idx = np.asarray(idx, dtype=np.int64)
     rows = X.reshape(X.shape[0], -1)[idx]
@@ -61,6 +63,11 @@ def gather_rows(X, idx, op: int = COPY, scale=None, shift=None, plane: int = 1, 
     v = rows.astype(np.float32)
     v = np.subtract(v, sh, dtype=np.float32)      # first fp32 rounding
     v = np.multiply(v, sc, dtype=np.float32)      # second fp32 rounding
+    if layout == "hwc":                           # channels-last: element (c, p) -> position p·C + c
+        C = rows.shape[1] // plane
+        v = np.ascontiguousarray(v.reshape(v.shape[0], C, plane).transpose(0, 2, 1)).reshape(v.shape[0], -1)
+    elif layout != "chw":
+        raise ValueError(layout)
     if op == U8_TO_F32_AFFINE:
         return v, lab
     if op == U8_TO_BF16_AFFINE:

@@ -170,12 +170,17 @@ def permute(N: int, seed: int, epoch: int, begin: int, count: int, out, stream=N
 GATHER_IMPL_AUTO = 0
 GATHER_IMPL_LSU = 1
 GATHER_IMPL_TMA = 2
+GATHER_LAYOUT_CHW = 0
+GATHER_LAYOUT_HWC = 1
 
 
-def make_gather_op(op=GATHER_COPY, scale=None, shift=None, plane=1, impl=GATHER_IMPL_AUTO):
+def make_gather_op(op=GATHER_COPY, scale=None, shift=None, plane=1, impl=GATHER_IMPL_AUTO,
+                   layout=GATHER_LAYOUT_CHW):
+    """pr_gather_op: per-channel affine (channels = len(scale), plane = H·W), kernel choice, output layout."""
     g = GatherOp()
     g.op = op
     g.impl = impl
+    g.layout = layout
     if op != GATHER_COPY:
         n = len(scale)
         g.channels = n

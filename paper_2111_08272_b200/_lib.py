@@ -33,7 +33,7 @@ class AllocPolicy(ctypes.Structure):
 class GatherOp(ctypes.Structure):
     _fields_ = [("op", c_i32), ("channels", c_i32), ("plane", c_i64),
                 ("scale", ctypes.c_float * PR_GATHER_MAX_CHANNELS), ("shift", ctypes.c_float * PR_GATHER_MAX_CHANNELS),
-                ("impl", c_i32), ("reserved", c_i32)]
+                ("impl", c_i32), ("layout", c_i32)]
 
 
 class CommConfig(ctypes.Structure):

@@ -1,14 +1,20 @@
-// K2 — step-batch gather of sampled rows into the local batch, with the u8 -> f32/bf16 affine fused.
+// K2 — step-batch gather of sampled rows into the local batch, with the u8 -> f32/bf16 affine fused
+// (and optionally the CHW -> HWC "channels-last" layout change the model's tensor-core convs want).
 //
 // Paper: Algorithm 1 step 4, "Proportionally draw samples from the sub-data set for training";
 // static allocation, "Worker i draws w_i samples from subdataset".  Data-plane definition is
-// build-defined (DESIGN.md §3 #38): dst[t,:] = op(src[idx[t],:]), lab_dst[t] = lab_src[idx[t]].
+// build-defined (DESIGN.md §3 #38, #41): dst[t,:] = op(src[idx[t],:]), lab_dst[t] = lab_src[idx[t]];
+// with PR_GATHER_LAYOUT_HWC the output element (c, p) of a CHW row is stored at p·C + c.
 //
-// HBM-bound: per row, row_bytes read + out_bytes written (+8 B index, +16 B label).  Layout: work item =
-// (row, 2 KiB segment of the input row); one warp per work item; every lane issues its 16-byte loads
-// (ld.global.nc.L1::no_allocate — the dataset is read-only and streamed) before any store (MLP 4 per
-// lane), converts in registers and stores 16-byte vectors (2 per input vector for bf16, 4 for f32).
-// Grid = 148 SMs × 8 CTAs × 8 warps, grid-stride over work items.
+// HBM-bound: per row, row_bytes read + out_bytes written (+8 B index, +16 B label).  Two kernels with
+// identical results:
+//   gather_tma_kernel  persistent CTAs; a producer warp prefetches row indices and issues cp.async.bulk
+//                      copies (whole rows, 24 KiB segments, or per-channel pixel blocks) into a 4-stage
+//                      mbarrier ring; 8 consumer warps convert from smem and store 16-byte vectors.
+//   gather_kernel      (LSU) a warp per 2 KiB segment, 4 ld.global.nc 16-byte loads in flight per lane;
+//                      chosen for small launches and host-memory sources (the e2e path).
+// Conversion: u8 -> exact float via PRMT into 0x4B000000 then −2^23, (x − shift)·scale with packed
+// FADD2/FMUL2 (per-lane IEEE RN, identical to the scalar two-op definition), cvt.rn.bf16x2.f32.
 #include <cuda_bf16.h>
 
 #include "common.h"
@@ -18,6 +24,7 @@ namespace {
 constexpr int kWarpsPerCta = 8;
 constexpr int kVecPerLane = 4;                            // 16-byte input vectors per lane per work item
 constexpr int kSegVec = 32 * kVecPerLane;                 // input vectors per work item (2 KiB)
+constexpr int kMaxHwcChannels = 4;
 
 struct GatherParams {
     const uint8_t* src;
@@ -32,6 +39,7 @@ struct GatherParams {
     float shift[PR_GATHER_MAX_CHANNELS];
     const int64_t* lab_src;
     int64_t* lab_dst;
+    int32_t hwc;          // 1: channels-last output
 };
 
 __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
@@ -79,6 +87,20 @@ __device__ __forceinline__ uint64_t u8pair_magic(uint32_t w, int j) {
     const uint32_t b = __byte_perm(w, 0x4B000000u, 0x7540u + j + 1);
     return (uint64_t)a | ((uint64_t)b << 32);
 }
+// f[0..2k) = (x − shift)·scale for the 4·k bytes of w[0..k), one channel
+template <int K>
+__device__ __forceinline__ void affine_words(const uint32_t* w, float sc, float sh, float* f) {
+    const uint64_t m23 = pk2(-8388608.0f, -8388608.0f);
+    const uint64_t nsh = pk2(-sh, -sh);
+    const uint64_t sc2 = pk2(sc, sc);
+#pragma unroll
+    for (int j = 0; j < 4 * K; j += 2) {
+        const uint64_t xf = add2(u8pair_magic(w[j >> 2], j & 3), m23);   // exact: x
+        const uint64_t y = mul2(add2(xf, nsh), sc2);                     // RN(RN(x − shift)·scale)
+        f[j] = __uint_as_float((uint32_t)y);
+        f[j + 1] = __uint_as_float((uint32_t)(y >> 32));
+    }
+}
 
 template <int OP>
 __device__ __forceinline__ void convert_store(const GatherParams& p, uint8_t* drow, int64_t v, uint4 x) {
@@ -90,19 +112,9 @@ __device__ __forceinline__ void convert_store(const GatherParams& p, uint8_t* dr
     float f[16];
     const uint32_t k0 = (uint32_t)v * 16u;  // element index of the first byte (row_bytes < 2^31)
     const uint32_t plane = (uint32_t)p.plane;
-    if (plane % 16u == 0) {
-        // one channel per 16-byte vector: (x − shift)·scale on pairs, x = (2^23 + x) − 2^23 exactly
+    if (plane % 16u == 0) {                 // one channel per 16-byte vector
         const int c = (int)(k0 / plane);
-        const uint64_t m23 = pk2(-8388608.0f, -8388608.0f);
-        const uint64_t nsh = pk2(-p.shift[c], -p.shift[c]);
-        const uint64_t sc2 = pk2(p.scale[c], p.scale[c]);
-#pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-            const uint64_t xf = add2(u8pair_magic(w[j >> 2], j & 3), m23);   // exact: x
-            const uint64_t y = mul2(add2(xf, nsh), sc2);                     // RN(RN(x − shift)·scale)
-            f[j] = __uint_as_float((uint32_t)y);
-            f[j + 1] = __uint_as_float((uint32_t)(y >> 32));
-        }
+        affine_words<4>(w, p.scale[c], p.shift[c], f);
     } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -125,6 +137,57 @@ __device__ __forceinline__ void convert_store(const GatherParams& p, uint8_t* dr
     }
 }
 
+// Channels-last: 8 consecutive pixels of all C channels (8 bytes per plane in smem, plane stride ps) ->
+// 8·C interleaved outputs at pixel pix0 of the HWC output row: C (bf16) or 2C (f32) 16-byte stores.
+template <int OP, int C>
+__device__ __forceinline__ void hwc_store(const GatherParams& p, uint8_t* drow, int64_t pix0, const uint8_t* s,
+                                          int64_t ps) {
+    float f[C][8];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        const uint2 w = *reinterpret_cast<const uint2*>(s + c * ps);
+        const uint32_t ww[2] = {w.x, w.y};
+        affine_words<2>(ww, p.scale[c], p.shift[c], f[c]);
+    }
+    // interleaved value k = pixel (k / C), channel (k % C)
+    if (OP == PR_GATHER_U8_TO_BF16_AFFINE) {
+        uint8_t* d = drow + pix0 * C * 2;
+#pragma unroll
+        for (int q = 0; q < C; ++q) {
+            uint32_t o[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int k = 8 * q + 2 * h;
+                o[h] = pack_bf16x2(f[k % C][k / C], f[(k + 1) % C][(k + 1) / C]);
+            }
+            st_v4(d + 16 * q, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    } else {
+        uint8_t* d = drow + pix0 * C * 4;
+#pragma unroll
+        for (int q = 0; q < 2 * C; ++q) {
+            uint32_t o[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int k = 4 * q + h;
+                o[h] = __float_as_uint(f[k % C][k / C]);
+            }
+            st_v4(d + 16 * q, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+    }
+}
+
+template <int OP>
+__device__ __forceinline__ void hwc_dispatch(const GatherParams& p, uint8_t* drow, int64_t pix0, const uint8_t* s,
+                                             int64_t ps) {
+    switch (p.channels) {
+        case 1: hwc_store<OP, 1>(p, drow, pix0, s, ps); break;
+        case 2: hwc_store<OP, 2>(p, drow, pix0, s, ps); break;
+        case 3: hwc_store<OP, 3>(p, drow, pix0, s, ps); break;
+        default: hwc_store<OP, 4>(p, drow, pix0, s, ps); break;
+    }
+}
+
 template <int OP>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) gather_kernel(const __grid_constant__ GatherParams p) {
     const int lane = threadIdx.x & 31;
@@ -135,13 +198,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) gather_kernel(const __grid_
     const int64_t out_mul = (OP == PR_GATHER_COPY) ? 1 : (OP == PR_GATHER_U8_TO_BF16_AFFINE ? 2 : 4);
     const int64_t items = p.n * segs;
 
-    // labels: one thread per row
-    if (p.lab_dst) {
+    if (p.lab_dst) {                                            // labels: one thread per row
         const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
         for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < p.n; t += nthreads)
             p.lab_dst[t] = p.lab_src[p.idx[t]];
     }
-
+    if (OP != PR_GATHER_COPY && p.hwc) {
+        // channels-last: a lane takes 8 pixels of every plane (C 8-byte loads, coalesced per plane)
+        const int64_t groups = p.plane / 8, gsegs = (groups + 31) / 32;
+        for (int64_t it = warp; it < p.n * gsegs; it += nwarps) {
+            const int64_t row = it / gsegs, gi = (it - row * gsegs) * 32 + lane;
+            if (gi < groups)
+                hwc_dispatch<OP>(p, p.dst + row * p.row_bytes * out_mul, gi * 8,
+                                 p.src + __ldg(p.idx + row) * p.row_bytes + gi * 8, p.plane);
+        }
+        return;
+    }
     for (int64_t it = warp; it < items; it += nwarps) {
         const int64_t row = it / segs;
         const int64_t seg = it - row * segs;
@@ -163,9 +235,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) gather_kernel(const __grid_
     }
 }
 
-// ---- TMA-staged variant: bulk copies keep whole rows (or 24 KiB row segments) in flight per CTA ------
-// A unit is up to kTmaSeg input bytes: 8 CIFAR rows (8 bulk copies) or one segment of a long row; the
-// producer warp prefetches the next unit's row indices (lane-parallel) while lane 0 issues the copies.
+// ---- TMA-staged variant --------------------------------------------------------------------------------
+// A unit is up to kTmaSeg input bytes: several whole rows (one bulk copy each), one 24 KiB segment of a
+// long row (CHW output), or one pixel block of a long row across all C planes (HWC output, C copies).
+// The producer warp prefetches the next unit's row indices (lane-parallel) while lane 0 issues copies.
 constexpr int kTmaStages = 4;
 constexpr int kTmaSeg = 24576;                // input bytes per unit
 constexpr int kTmaConsumerWarps = 8;
@@ -198,13 +271,37 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
+struct TmaGeom {
+    int64_t rpu;     // rows per unit (> 1: whole rows)
+    int64_t upr;     // units per row (rpu == 1)
+    int64_t pb;      // HWC pixel block (rpu == 1 && hwc), pixels
+    int64_t units;
+};
+
+__host__ __device__ inline TmaGeom tma_geom(int64_t n, int64_t row_bytes, int hwc, int64_t channels, int64_t plane) {
+    TmaGeom g;
+    g.rpu = 1;
+    g.pb = 0;
+    if (row_bytes <= kTmaSeg / 2) {
+        g.rpu = kTmaSeg / row_bytes < 32 ? kTmaSeg / row_bytes : 32;
+        g.upr = 1;
+        g.units = (n + g.rpu - 1) / g.rpu;
+    } else if (hwc) {
+        g.pb = (kTmaSeg / channels) / 16 * 16;
+        g.upr = (plane + g.pb - 1) / g.pb;
+        g.units = n * g.upr;
+    } else {
+        g.upr = (row_bytes + kTmaSeg - 1) / kTmaSeg;
+        g.units = n * g.upr;
+    }
+    return g;
+}
+
 template <int OP>
 __global__ void __launch_bounds__(32 * (kTmaConsumerWarps + 1)) gather_tma_kernel(const __grid_constant__ GatherParams p) {
     extern __shared__ __align__(128) uint8_t smem[];   // [kTmaStages][kTmaSeg]
     __shared__ uint64_t full[kTmaStages], empty[kTmaStages];
-    const int64_t rpu = (p.row_bytes <= kTmaSeg / 2) ? min((int64_t)32, kTmaSeg / p.row_bytes) : 1;  // rows/unit
-    const int64_t segs = rpu > 1 ? 1 : (p.row_bytes + kTmaSeg - 1) / kTmaSeg;                          // units/row
-    const int64_t units = rpu > 1 ? (p.n + rpu - 1) / rpu : p.n * segs;
+    const TmaGeom geo = tma_geom(p.n, p.row_bytes, p.hwc, p.channels, p.plane);
     const int64_t G = gridDim.x;
     const int64_t out_mul = (OP == PR_GATHER_COPY) ? 1 : (OP == PR_GATHER_U8_TO_BF16_AFFINE ? 2 : 4);
     if (threadIdx.x == 0) {
@@ -221,25 +318,24 @@ __global__ void __launch_bounds__(32 * (kTmaConsumerWarps + 1)) gather_tma_kerne
     }
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // source row of lane `lane` within unit u (rows mode) / of the unit (segment mode)
-    auto fetch = [&](int64_t u) -> int64_t {
-        if (u >= units) return 0;
-        if (rpu > 1) {
-            const int64_t row = u * rpu + lane;
-            return (lane < rpu && row < p.n) ? __ldg(p.idx + row) : 0;
+    auto fetch = [&](int64_t u) -> int64_t {          // source row(s) of unit u (lane j: j-th row)
+        if (u >= geo.units) return 0;
+        if (geo.rpu > 1) {
+            const int64_t row = u * geo.rpu + lane;
+            return (lane < geo.rpu && row < p.n) ? __ldg(p.idx + row) : 0;
         }
-        return __ldg(p.idx + u / segs);
+        return __ldg(p.idx + u / geo.upr);
     };
     if (warp == 0) {
         uint32_t k = 0;
         int64_t cur = fetch(blockIdx.x);
-        for (int64_t u = blockIdx.x; u < units; u += G, ++k) {
+        for (int64_t u = blockIdx.x; u < geo.units; u += G, ++k) {
             const int64_t nxt = fetch(u + G);                         // prefetch: hides the idx latency
             const int stg = (int)(k % kTmaStages);
             if (lane == 0 && k >= (uint32_t)kTmaStages) mbar_wait(&empty[stg], ((k / kTmaStages) - 1) & 1);
             uint8_t* dst = smem + (size_t)stg * kTmaSeg;
-            if (rpu > 1) {
-                const int64_t nrows = min(rpu, p.n - u * rpu);
+            if (geo.rpu > 1) {
+                const int64_t nrows = min(geo.rpu, p.n - u * geo.rpu);
                 if (lane == 0) mbar_arrive_expect_tx(&full[stg], (uint32_t)(nrows * p.row_bytes));
                 for (int j = 0; j < nrows; ++j) {
                     const int64_t srow = __shfl_sync(0xffffffffu, cur, j);
@@ -247,34 +343,56 @@ __global__ void __launch_bounds__(32 * (kTmaConsumerWarps + 1)) gather_tma_kerne
                                             &full[stg]);
                 }
             } else if (lane == 0) {
-                const int64_t off = (u % segs) * kTmaSeg;
-                const uint32_t bytes = (uint32_t)min((int64_t)kTmaSeg, p.row_bytes - off);
-                mbar_arrive_expect_tx(&full[stg], bytes);
-                tma_load(dst, p.src + cur * p.row_bytes + off, bytes, &full[stg]);
+                const int64_t b = u % geo.upr;
+                if (geo.pb) {                                         // HWC: pixel block of every plane
+                    const int64_t p0 = b * geo.pb;
+                    const uint32_t np = (uint32_t)min(geo.pb, p.plane - p0);
+                    mbar_arrive_expect_tx(&full[stg], np * (uint32_t)p.channels);
+                    for (int c = 0; c < p.channels; ++c)
+                        tma_load(dst + c * geo.pb, p.src + cur * p.row_bytes + c * p.plane + p0, np, &full[stg]);
+                } else {
+                    const int64_t off = b * kTmaSeg;
+                    const uint32_t bytes = (uint32_t)min((int64_t)kTmaSeg, p.row_bytes - off);
+                    mbar_arrive_expect_tx(&full[stg], bytes);
+                    tma_load(dst, p.src + cur * p.row_bytes + off, bytes, &full[stg]);
+                }
             }
             cur = nxt;
         }
     } else {
-        // consumer warps: smem -> convert -> 16-byte stores, lanes on consecutive vectors of one row
+        // consumer warps: smem -> convert -> 16-byte stores, lanes on consecutive vectors / pixel groups
         const int cw = warp - 1;
         const int64_t vpr = p.row_bytes / 16;
         uint32_t k = 0;
-        for (int64_t u = blockIdx.x; u < units; u += G, ++k) {
+        for (int64_t u = blockIdx.x; u < geo.units; u += G, ++k) {
             const int stg = (int)(k % kTmaStages);
             mbar_wait(&full[stg], (k / kTmaStages) & 1);
-            const uint4* sv = reinterpret_cast<const uint4*>(smem + (size_t)stg * kTmaSeg);
-            if (rpu > 1) {
-                const int64_t nrows = min(rpu, p.n - u * rpu);
+            const uint8_t* sb = smem + (size_t)stg * kTmaSeg;
+            const uint4* sv = reinterpret_cast<const uint4*>(sb);
+            if (geo.rpu > 1) {
+                const int64_t nrows = min(geo.rpu, p.n - u * geo.rpu);
                 for (int64_t rl = cw; rl < nrows; rl += kTmaConsumerWarps) {
-                    uint8_t* drow = p.dst + (u * rpu + rl) * p.row_bytes * out_mul;
-                    for (int64_t v = lane; v < vpr; v += 32) convert_store<OP>(p, drow, v, sv[rl * vpr + v]);
+                    uint8_t* drow = p.dst + (u * geo.rpu + rl) * p.row_bytes * out_mul;
+                    if (OP != PR_GATHER_COPY && p.hwc) {
+                        for (int64_t gi = lane; gi < p.plane / 8; gi += 32)
+                            hwc_dispatch<OP>(p, drow, gi * 8, sb + rl * p.row_bytes + gi * 8, p.plane);
+                    } else {
+                        for (int64_t v = lane; v < vpr; v += 32) convert_store<OP>(p, drow, v, sv[rl * vpr + v]);
+                    }
                 }
             } else {
-                const int64_t row = u / segs, off = (u - row * segs) * kTmaSeg;
-                const int64_t nv = min((int64_t)kTmaSeg, p.row_bytes - off) / 16;
+                const int64_t row = u / geo.upr, b = u - row * geo.upr;
                 uint8_t* drow = p.dst + row * p.row_bytes * out_mul;
-                for (int64_t v = threadIdx.x - 32; v < nv; v += 32 * kTmaConsumerWarps)
-                    convert_store<OP>(p, drow, off / 16 + v, sv[v]);
+                if (OP != PR_GATHER_COPY && geo.pb) {
+                    const int64_t p0 = b * geo.pb, np = min(geo.pb, p.plane - p0);
+                    for (int64_t gi = threadIdx.x - 32; gi < np / 8; gi += 32 * kTmaConsumerWarps)
+                        hwc_dispatch<OP>(p, drow, p0 + gi * 8, sb + gi * 8, geo.pb);
+                } else {
+                    const int64_t off = b * kTmaSeg;
+                    const int64_t nv = min((int64_t)kTmaSeg, p.row_bytes - off) / 16;
+                    for (int64_t v = threadIdx.x - 32; v < nv; v += 32 * kTmaConsumerWarps)
+                        convert_store<OP>(p, drow, off / 16 + v, sv[v]);
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stg]);
@@ -301,6 +419,7 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
     p.op = op ? op->op : PR_GATHER_COPY;
     p.channels = 1;
     p.plane = row_bytes;
+    p.hwc = 0;
     for (int i = 0; i < PR_GATHER_MAX_CHANNELS; ++i) { p.scale[i] = 1.0f; p.shift[i] = 0.0f; }
     if (p.op != PR_GATHER_COPY) {
         if (p.op != PR_GATHER_U8_TO_F32_AFFINE && p.op != PR_GATHER_U8_TO_BF16_AFFINE) return PR_ERR_INVALID;
@@ -310,6 +429,12 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
         p.channels = op->channels;
         p.plane = op->plane;
         for (int i = 0; i < op->channels; ++i) { p.scale[i] = op->scale[i]; p.shift[i] = op->shift[i]; }
+        if (op->layout == PR_GATHER_LAYOUT_HWC) {
+            if (op->channels > kMaxHwcChannels || op->plane % 16) return PR_ERR_INVALID;
+            p.hwc = 1;
+        } else if (op->layout != PR_GATHER_LAYOUT_CHW) {
+            return PR_ERR_INVALID;
+        }
     }
     p.lab_src = d_lab_src;
     p.lab_dst = d_lab_dst;
@@ -327,9 +452,8 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
                      (impl == PR_GATHER_IMPL_AUTO && !host_src && n * row_bytes >= (8ll << 20));
     if (tma) {
         const size_t smem = (size_t)kTmaStages * kTmaSeg;
-        const int64_t rpu = row_bytes <= kTmaSeg / 2 ? (kTmaSeg / row_bytes < 32 ? kTmaSeg / row_bytes : 32) : 1;
-        const int64_t units = rpu > 1 ? (n + rpu - 1) / rpu : n * ((row_bytes + kTmaSeg - 1) / kTmaSeg);
-        int64_t blocks = units < 148 * 2 ? units : 148 * 2;
+        const TmaGeom geo = tma_geom(n, row_bytes, p.hwc, p.channels, p.plane);
+        const int64_t blocks = geo.units < 148 * 2 ? geo.units : 148 * 2;
         const dim3 block(32 * (kTmaConsumerWarps + 1));
         static bool attr = false;
         if (!attr) {

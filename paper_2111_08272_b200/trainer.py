@@ -55,6 +55,8 @@ class RunConfig:
     host_data: bool = False                 # e2e: data set in pinned host memory, gathered over PCIe
     bf16_compute: bool = True               # autocast for the model's forward/backward
     gather: str = "epoch"                   # "epoch": one K2 launch per epoch; "step": one per step
+    channels_last: bool = True              # K2 writes HWC rows; the model runs channels-last (no transposes)
+    graphs: bool = True                     # capture each step's forward/backward (+ spin) in a CUDA graph
 
 
 def build_model(name: str, num_classes: int):
@@ -87,10 +89,18 @@ class Worker:
         self.X = data.pin_memory() if cfg.host_data else data.to(self.dev)
         self.Y = labels.to(self.dev)
         C, H, W = cfg.shape
+        # K2 kernel chosen here (TMA for the resident data set, LSU over PCIe for host data) so the
+        # launch does no host-side pointer query
         self.gop = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE if cfg.bf16_compute else pr.GATHER_U8_TO_F32_AFFINE,
-                                     [1.0 / s for s in CIFAR_STD[:C]], CIFAR_MEAN[:C], H * W)
+                                     [1.0 / s for s in CIFAR_STD[:C]], CIFAR_MEAN[:C], H * W,
+                                     impl=pr.GATHER_IMPL_LSU if cfg.host_data else pr.GATHER_IMPL_TMA,
+                                     layout=pr.GATHER_LAYOUT_HWC if cfg.channels_last else pr.GATHER_LAYOUT_CHW)
+        torch.backends.cudnn.benchmark = True
         torch.manual_seed(cfg.seed)                   # identical initial weights on every rank
         self.model = build_model(cfg.model, cfg.num_classes).to(self.dev)
+        if cfg.channels_last:
+            self.model = self.model.to(memory_format=torch.channels_last)
+        self._graphs = {}                             # (n_r, spin_ns) -> captured step
         params = list(self.model.parameters())
         self.L = sum(p.numel() for p in params)
         if comm is not None:
@@ -98,8 +108,8 @@ class Worker:
         else:
             self.flat = torch.zeros(self.L, dtype=torch.float32, device=self.dev)
         off = 0
-        for p in params:
-            p.grad = self.flat[off:off + p.numel()].view_as(p)
+        for p in params:   # .grad = a view of the flat buffer with the parameter's own (channels-last) strides
+            p.grad = self.flat[off:off + p.numel()].as_strided(p.shape, p.stride())
             off += p.numel()
         self.opt = torch.optim.SGD(params, lr=cfg.lr, weight_decay=cfg.wd)
         self.idx = torch.empty(cfg.N, dtype=torch.int64, device=self.dev)   # any shard size after re-allocation
@@ -129,10 +139,15 @@ class Worker:
         return x, y
 
     # ---- a4: forward/backward with gradient accumulation (P:69 steps (1)-(3)) --------------------------
+    def _input(self, x, n_r: int):
+        C, H, W = self.cfg.shape
+        if self.cfg.channels_last:                    # HWC rows -> logical NCHW with channels-last strides
+            return x[:n_r].view(n_r, H, W, C).permute(0, 3, 1, 2)
+        return x[:n_r].view(n_r, C, H, W)
+
     def compute(self, x, y, n_r: int):
         cfg = self.cfg
-        C, H, W = cfg.shape
-        x = x[:n_r].view(n_r, C, H, W)
+        x = self._input(x, n_r)
         losses = []
         for m0 in range(0, n_r, cfg.micro):
             xm, ym = x[m0:m0 + cfg.micro], y[m0:m0 + cfg.micro]
@@ -141,11 +156,45 @@ class Worker:
                 loss = F.cross_entropy(out.float(), ym)
             (loss * (xm.shape[0] / n_r)).backward()           # local mean over n_r (DESIGN §3 #11)
             losses.append(loss.detach() * xm.shape[0])
-        sigma = cfg.slowdown[self.rank] if cfg.slowdown else 1.0
-        if sigma > 1.0 and self.c0_ns > 0:
-            pr.spin(int((sigma - 1.0) * self.c0_ns * n_r), stream=self.stream)   # K4
+        ns = self._spin_ns(n_r)
+        if ns > 0:
+            pr.spin(ns)                                      # K4 on the current (possibly capturing) stream
             self.launches += 1
         return torch.stack(losses).sum() / n_r
+
+    def _spin_ns(self, n_r: int) -> int:
+        sigma = self.cfg.slowdown[self.rank] if self.cfg.slowdown else 1.0
+        return int((sigma - 1.0) * self.c0_ns * n_r) if sigma > 1.0 and self.c0_ns > 0 else 0
+
+    def compute_graphed(self, x, y, n_r: int):
+        """a4 through a CUDA graph: static input buffers, captured forward/backward (+ K4 spin).
+        Capture is rank-local (no collective inside), so a rank whose n_r changes re-captures alone."""
+        key = (n_r, self._spin_ns(n_r))
+        st = self._graphs.get(key)
+        if st is None:
+            xs = torch.empty((n_r, self.row_bytes), dtype=self.xdt, device=self.dev)
+            ys = torch.zeros(n_r, dtype=torch.int64, device=self.dev)
+            xs.copy_(x[:n_r])
+            ys.copy_(y[:n_r])
+            side = torch.cuda.Stream(self.dev)
+            side.wait_stream(self.stream)
+            launches = self.launches
+            with torch.cuda.stream(side):
+                self.compute(xs, ys, n_r)                     # warm-up (cuDNN autotune, allocator)
+            self.stream.wait_stream(side)
+            self.flat.zero_()                                 # the warm-up's gradients are discarded
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                loss = self.compute(xs, ys, n_r)
+            self.stream.wait_stream(side)
+            self.launches = launches
+            st = self._graphs[key] = (g, xs, ys, loss, key[1] > 0)
+        g, xs, ys, loss, spins = st
+        xs.copy_(x[:n_r])
+        ys.copy_(y[:n_r])
+        g.replay()
+        self.launches += 1 if spins else 0                    # K4 inside the graph
+        return loss.clone()
 
     # ---- a6-a9: weighted ring allreduce + SGD (Algorithm 1 steps 5-6) ---------------------------------
     def allreduce_and_update(self, n_r: int, record=False):
@@ -182,7 +231,7 @@ class Worker:
                     x, y = xe[s * n_r:(s + 1) * n_r], ye[s * n_r:(s + 1) * n_r]
                 else:
                     x, y = self.gather(s * n_r, n_r, record)
-                loss = self.compute(x, y, n_r)
+                loss = self.compute_graphed(x, y, n_r) if cfg.graphs else self.compute(x, y, n_r)
             else:
                 loss = torch.zeros((), device=self.dev)
             ev[s][1].record(self.stream)

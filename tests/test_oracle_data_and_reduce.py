@@ -39,6 +39,19 @@ def test_gather_affine_matches_exact_rounding():
     assert np.array_equal(bf, ref)
 
 
+def test_gather_hwc_layout_is_channels_last_permute():
+    """layout="hwc" = the CHW result permuted to channels-last (torch permute/contiguous: library routine)."""
+    X = synth.images_u8(7, seed=6)
+    idx = np.array([3, 0, 6, 6])
+    scale = np.array([0.5, 0.25, 0.125], dtype=np.float32)
+    shift = np.array([1.0, 2.0, 3.0], dtype=np.float32)
+    chw, _ = G.gather_rows(X, idx, G.U8_TO_F32_AFFINE, scale, shift, plane=1024)
+    hwc, _ = G.gather_rows(X, idx, G.U8_TO_F32_AFFINE, scale, shift, plane=1024, layout="hwc")
+    ref = torch.from_numpy(chw).view(4, 3, 32, 32).permute(0, 2, 3, 1).contiguous().view(4, -1).numpy()
+    assert np.array_equal(hwc, ref)
+    assert hwc[1, 5 * 3 + 2] == chw[1, 2 * 1024 + 5]       # element (c=2, p=5) of row 1
+
+
 def test_bf16_rne_against_torch_random_bits():
     rng = np.random.Generator(np.random.PCG64(8))
     bits = rng.integers(0, 2 ** 32, 200000, dtype=np.uint64).astype(np.uint32)
