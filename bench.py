@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--e2e-epochs", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-colocated", action="store_true")
+    ap.add_argument("--data-n", type=int, default=N_DATA,
+                    help="data-set rows (default 50,000; smaller only for profiling runs: S = N // 1024)")
+    ap.add_argument("--kernel-shares", action="store_true",
+                    help="also report each library kernel's share of the timed step (live CUDA events)")
     return ap.parse_args()
 
 
@@ -139,7 +143,7 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = pr.comm_init(rank, world, local) if world > 1 else None
-    cfg = RunConfig(N=N_DATA, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024)
+    cfg = RunConfig(N=args.data_n, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024)
     wk = Worker(cfg, rank, world, local, comm)
 
     def barrier():
@@ -187,7 +191,8 @@ def run_ours(args):
     g_rows = [n for _, _, n in wk.gather_events]
     g_bytes = statistics.mean(g_rows) * (ROW_BYTES + 2 * ROW_BYTES + 8 + 8 + 8)
     g_avg = statistics.mean(g_ms) if g_ms else float("nan")
-    gather_roof = {"kernel": "gather_tma_kernel<U8_TO_BF16_AFFINE> (K2, one launch per epoch)", "bound": "hbm",
+    gather_roof = {"kernel": "gather_kernel<U8_TO_BF16_AFFINE> channels-last (K2, LSU, one launch per epoch)",
+                   "bound": "hbm",
                    "achieved": g_bytes / (g_avg * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                    "peak_kind": peak_kind, "launches": len(g_ms), "avg_us": g_avg * 1e3,
                    "bytes_per_launch": g_bytes, "total_ms": sum(g_ms)}
@@ -206,11 +211,13 @@ def run_ours(args):
                      "frac_of_900_nominal": bus / 900.0, "total_ms": sum(a_ms), "traffic": None}
         if allreduce["total_ms"] > gather_roof["total_ms"]:
             roof = allreduce
+        if not shared:
+            allreduce["nccl_baseline"] = nccl_baseline(wk, world, rank)
 
     # ---- e2e: host-resident data set, per-step loss read back --------------------------------------
     e2e = None
     if args.e2e_epochs > 0:
-        cfg_h = RunConfig(N=N_DATA, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024,
+        cfg_h = RunConfig(N=args.data_n, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024,
                           host_data=True)
         wk_h = Worker(cfg_h, rank, world, local, comm, data=wk.X.cpu(), labels=wk.Y.cpu())
         wk_h.model.load_state_dict(wk.model.state_dict())
@@ -266,12 +273,64 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "alloc_w": wk.alloc.view()["w"],
             "loss_last_epoch": recs[-1]["loss"],
+            # share of the timed region spent in each library kernel (live events; compare with the ncu
+            # launch list of the same command in profiles/)
+            "kernel_shares": {"gather_kernel": gather_roof["total_ms"] / ms,
+                              "ring_kernel": (allreduce["total_ms"] / ms) if allreduce else 0.0},
         }
+        if args.data_n != N_DATA:
+            out["config"]["workload"] += f" [PROFILING VARIANT: N={args.data_n}]"
         print(json.dumps(out))
     if comm is not None:
         comm.destroy()
     if world > 1:
         dist.destroy_process_group()
+
+
+def nccl_baseline(wk, world, rank, reps=20):
+    """K5: the same weighted average through NCCL on the same buffer — premul-sum
+    (ncclRedOpCreatePreMulSum via torch) and scale + SUM — against K3, all timed back to back."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2111_08272_b200 as pr
+
+    n_r = wk.alloc.view()["n"][rank]
+    sumn = wk.alloc.view()["B"]
+    s = n_r / sumn
+    buf = wk.flat
+    Z = buf.numel() * 4
+
+    def timed(fn):
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / reps], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        us = float(t) * 1e3
+        return {"us": us, "busbw_GBs": Z * 2 * (world - 1) / world / (us * 1e-6) / 1e9}
+
+    out = {"propring_K3": timed(lambda: pr.weighted_allreduce(wk.comm, buf, n_r))}
+    try:
+        op = dist._make_nccl_premul_sum(s)
+        out["nccl_premul_sum"] = timed(lambda: dist.all_reduce(buf, op=op))
+    except Exception as e:   # noqa: BLE001
+        out["nccl_premul_sum"] = {"error": repr(e)[:200]}
+
+    def scale_sum():
+        buf.mul_(s)
+        dist.all_reduce(buf)
+
+    out["nccl_scale_then_sum"] = timed(scale_sum)
+    buf.zero_()
+    return out
 
 
 def traffic_from_profiles(kind):

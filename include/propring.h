@@ -172,6 +172,8 @@ typedef struct pr_comm pr_comm;
 #define PR_DTYPE_BF16 1
 
 #define PR_COMM_FLAG_FORCE_STAGED 1   /* all-gather through staging even when buffers are registered */
+#define PR_COMM_FLAG_SYS_SCOPE    2   /* system-scope release/acquire even when every rank shares one GPU
+                                         (by default .gpu scope is used exactly when that is the case) */
 
 typedef struct {
     int32_t channels;     /* ring channels = CTAs per rank (default 16)                               */

@@ -218,13 +218,15 @@ def test_philox(ctr, key: int, use_curand: bool, out, stream=None):
 # ---------------------------------------------------------------------------------------------------
 
 COMM_FLAG_FORCE_STAGED = 1
+COMM_FLAG_SYS_SCOPE = 2
 
 
 def comm_config(channels=16, slots=8, threads=512, slot_bytes=256 * 1024, watchdog_ns=10_000_000_000,
-                force_staged=False, stages=6, tile_bytes=16384):
-    """K3 launch/pipeline configuration; the defaults are the best of tools/sweep_ring.py on B200."""
-    return CommConfig(channels=channels, slots=slots, threads=threads,
-                      flags=COMM_FLAG_FORCE_STAGED if force_staged else 0, slot_bytes=slot_bytes,
+                force_staged=False, stages=6, tile_bytes=16384, sys_scope=False):
+    """K3 launch/pipeline configuration; the defaults are the best of tools/sweep_ring.py on B200.
+    sys_scope=True forces system-scope synchronisation even when all ranks share one GPU (tests)."""
+    flags = (COMM_FLAG_FORCE_STAGED if force_staged else 0) | (COMM_FLAG_SYS_SCOPE if sys_scope else 0)
+    return CommConfig(channels=channels, slots=slots, threads=threads, flags=flags, slot_bytes=slot_bytes,
                       watchdog_ns=watchdog_ns, stages=stages, tile_bytes=tile_bytes)
 
 

@@ -448,8 +448,10 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
         if (cudaPointerGetAttributes(&at, d_src) == cudaSuccess) host_src = at.type == cudaMemoryTypeHost;
         else cudaGetLastError();
     }
+    // Measured on B200: CHW output, >= 8 MiB: TMA 5.26 vs LSU 4.89 TB/s; HWC output: LSU
+    // 5.61 vs TMA 4.90 TB/s (each lane's per-plane 8-byte loads coalesce; no extra smem pass).
     const bool tma = impl == PR_GATHER_IMPL_TMA ||
-                     (impl == PR_GATHER_IMPL_AUTO && !host_src && n * row_bytes >= (8ll << 20));
+                     (impl == PR_GATHER_IMPL_AUTO && !host_src && !p.hwc && n * row_bytes >= (8ll << 20));
     if (tma) {
         const size_t smem = (size_t)kTmaStages * kTmaSeg;
         const TmaGeom geo = tma_geom(n, row_bytes, p.hwc, p.channels, p.plane);

@@ -68,6 +68,7 @@ static_assert(sizeof(ChanState) == 128, "state");
 struct DevTable {
     int32_t rank, P, channels, slots;
     int32_t stages, tile_bytes;     // TMA pipeline: depth, bytes per input per stage
+    int32_t sysscope, pad0;         // 1: some peer is another GPU (use .sys release/acquire)
     int64_t slot_bytes;
     int64_t watchdog_ns;
     uint64_t off_flags, off_hs, off_state, off_ag, off_staging, window_bytes;
@@ -115,24 +116,32 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+// Memory scope of the protocol: .sys when a peer window lives on another GPU (NVLink peer memory), .gpu
+// when every rank of the group shares this device (local groups, co-located processes) — the cheapest
+// scope that is still correct.
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p, bool sys) {
     unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v, bool sys) {
+    if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v, bool sys) {
+    if (sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ long long ld_relaxed_s64(const void* p) {
+__device__ __forceinline__ long long ld_relaxed_s64(const void* p, bool sys) {
     long long v;
-    asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if (sys) asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_relaxed_s64(void* p, long long v) {
-    asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_s64(void* p, long long v, bool sys) {
+    if (sys) asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
     asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
@@ -268,8 +277,8 @@ __device__ __forceinline__ void latch(const DevTable* t, int code) {
 
 // Spin until *p >= target; false on watchdog expiry.
 __device__ __forceinline__ bool wait_ge(const unsigned long long* p, unsigned long long target,
-                                        unsigned long long deadline) {
-    while (ld_acquire(p) < target) {
+                                        unsigned long long deadline, bool sys) {
+    while (ld_acquire(p, sys) < target) {
         if (gtimer() > deadline) return false;
     }
     return true;
@@ -309,6 +318,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
     ChanFlags* nxf = flags_of(tab->win[next], tab, ch);
     ChanFlags* pvf = flags_of(tab->win[prev], tab, ch);
     const bool t0 = threadIdx.x == 0;
+    const bool sys = tab->sysscope != 0;
     const int nc = blockDim.x - 64;                 // consumer threads (warps 2..): warp 0 producer, warp 1 signal
     const int kStages = tab->stages;
     const int kTileBytes = tab->tile_bytes;
@@ -329,21 +339,21 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
         const int par = (int)(seq & 1ull);
         for (int q = 0; q < P; ++q) {
             HsEntry* e = hs_of(tab->win[q], tab, ch, par, r);
-            st_relaxed_s64(&e->count, A.count);
-            st_relaxed_s64(&e->n, rc.n_local);
-            st_relaxed_s64(&e->dtype, ((long long)rc.reg_id << 32) | (unsigned)A.dtype);  // dtype | reg_id
-            st_relaxed_s64(&e->offset, rc.reg_off);
-            st_release(&e->seq, seq);
+            st_relaxed_s64(&e->count, A.count, sys);
+            st_relaxed_s64(&e->n, rc.n_local, sys);
+            st_relaxed_s64(&e->dtype, ((long long)rc.reg_id << 32) | (unsigned)A.dtype, sys);  // dtype | reg_id
+            st_relaxed_s64(&e->offset, rc.reg_off, sys);
+            st_release(&e->seq, seq, sys);
         }
         int err = 0, direct = 1, next_reg = -1;
         long long sumn = 0, next_off = 0;
         for (int q = 0; q < P && !err; ++q) {
             HsEntry* e = hs_of(my, tab, ch, par, q);
-            if (!wait_ge(&e->seq, seq, deadline)) { err = PR_ERR_PEER_TIMEOUT; break; }
-            const long long cnt = ld_relaxed_s64(&e->count);
-            const long long n = ld_relaxed_s64(&e->n);
-            const long long dr = ld_relaxed_s64(&e->dtype);
-            const long long off = ld_relaxed_s64(&e->offset);
+            if (!wait_ge(&e->seq, seq, deadline, sys)) { err = PR_ERR_PEER_TIMEOUT; break; }
+            const long long cnt = ld_relaxed_s64(&e->count, sys);
+            const long long n = ld_relaxed_s64(&e->n, sys);
+            const long long dr = ld_relaxed_s64(&e->dtype, sys);
+            const long long off = ld_relaxed_s64(&e->offset, sys);
             const int dt = (int)(dr & 0xffffffffll), rid = (int)(dr >> 32);
             if (cnt != A.count || dt != A.dtype) err = PR_ERR_LENGTH_MISMATCH;
             sumn += n;
@@ -429,9 +439,9 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 range(c, i, lo, len);
                 if (!bad) {
                     bool ok = true;
-                    if (reads_slot(kind)) ok = wait_ge(&myf->rs_ready, consJ + 1, deadline);
-                    if (ok && waits_ag(kind)) ok = wait_ge(&myf->ag_ready, agC + 1, deadline);
-                    if (ok && writes_slot(kind) && prodJ + 1 > K) ok = wait_ge(&myf->rs_credit, prodJ + 1 - K, deadline);
+                    if (reads_slot(kind)) ok = wait_ge(&myf->rs_ready, consJ + 1, deadline, sys);
+                    if (ok && waits_ag(kind)) ok = wait_ge(&myf->ag_ready, agC + 1, deadline, sys);
+                    if (ok && writes_slot(kind) && prodJ + 1 > K) ok = wait_ge(&myf->rs_credit, prodJ + 1 - K, deadline, sys);
                     if (!ok) {
                         bad = true;
                         *(volatile int*)&sh.err = PR_ERR_PEER_TIMEOUT;
@@ -488,14 +498,14 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                     if (sends) mbar_wait(&sh.stored[stg], (tc / (uint32_t)kStages) & 1);
                     ok = ok && sh.tile_ok[stg] != 0;
                     if (t == nt - 1 && sends && ok) {
-                        if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1);
-                        else st_release(&nxf->rs_ready, prodJ + 1);
+                        if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
+                        else st_release(&nxf->rs_ready, prodJ + 1, sys);
                     }
                     mbar_arrive(&sh.empty[stg]);
                 }
                 if (nt == 0 && sends && !*(volatile int*)&sh.err) {   // empty slice: nothing to wait for
-                    if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1);
-                    else st_release(&nxf->rs_ready, prodJ + 1);
+                    if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
+                    else st_release(&nxf->rs_ready, prodJ + 1, sys);
                 }
                 if (sends_ag(kind)) ++agP;
                 else if (writes_slot(kind)) ++prodJ;
@@ -529,7 +539,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 mbar_wait(&sh.full[stg], (tc / (uint32_t)kStages) & 1);
                 ok = sh.tile_ok[stg] != 0;
                 if (ok && t == nt - 1 && reads_slot(kind) && cid == 0)   // slot landed in smem: hand it back
-                    st_relaxed_u64(&pvf->rs_credit, consJ + 1);     // (ordered after the TMA reads by the wait)
+                    st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);     // (ordered after the TMA reads by the wait)
                 const int64_t e0 = t * te;
                 const int64_t ne = min(te, len - e0);
                 const int64_t nv = (ne * (int64_t)sizeof(T)) / 16;
@@ -562,7 +572,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 }
             }
             const bool err = *(volatile int*)&sh.err != 0;
-            if (nt == 0 && reads_slot(kind) && cid == 0 && !err) st_relaxed_u64(&pvf->rs_credit, consJ + 1);
+            if (nt == 0 && reads_slot(kind) && cid == 0 && !err) st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);
             if (reads_slot(kind)) ++consJ;
             if (writes_slot(kind)) ++prodJ;
         });
@@ -579,19 +589,20 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
 
 __global__ void allgather_f64_kernel(const DevTable* tab, unsigned long long seq, double v, double* out) {
     if (threadIdx.x != 0) return;
+    const bool sys = tab->sysscope != 0;
     const int r = tab->rank, P = tab->P;
     const int par = (int)(seq & 1ull);
     unsigned long long deadline = ~0ull;
     if (tab->watchdog_ns > 0) deadline = gtimer() + (unsigned long long)tab->watchdog_ns;
     for (int q = 0; q < P; ++q) {
         AgEntry* e = reinterpret_cast<AgEntry*>(tab->win[q] + tab->off_ag) + par * P + r;
-        st_relaxed_s64(&e->v, __double_as_longlong(v));
-        st_release(&e->seq, seq);
+        st_relaxed_s64(&e->v, __double_as_longlong(v), sys);
+        st_release(&e->seq, seq, sys);
     }
     for (int q = 0; q < P; ++q) {
         AgEntry* e = reinterpret_cast<AgEntry*>(tab->win[r] + tab->off_ag) + par * P + q;
-        if (!wait_ge(&e->seq, seq, deadline)) { latch(tab, PR_ERR_PEER_TIMEOUT); return; }
-        out[q] = __longlong_as_double(ld_relaxed_s64(&e->v));
+        if (!wait_ge(&e->seq, seq, deadline, sys)) { latch(tab, PR_ERR_PEER_TIMEOUT); return; }
+        out[q] = __longlong_as_double(ld_relaxed_s64(&e->v, sys));
     }
 }
 
@@ -616,6 +627,7 @@ struct Hello {
     int32_t P, rank, device, channels, slots, threads, stages, tile_bytes;
     int64_t slot_bytes, window_bytes;
     uint64_t bytes;   // registration size
+    unsigned char uuid[16];   // device identity: peers on another GPU need .sys-scope synchronisation
 };
 }  // namespace
 
@@ -657,7 +669,7 @@ pr_comm_config default_config() {
 }
 
 int check_config(const pr_comm_config& c) {
-    if ((c.flags & ~PR_COMM_FLAG_FORCE_STAGED) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
+    if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
         (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024)
@@ -786,6 +798,10 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
     me.P = P; me.rank = rank; me.device = device; me.channels = c->cfg.channels; me.slots = c->cfg.slots;
     me.threads = c->cfg.threads; me.slot_bytes = c->cfg.slot_bytes; me.window_bytes = (int64_t)c->tab.window_bytes;
     me.stages = c->cfg.stages; me.tile_bytes = c->cfg.tile_bytes;
+    {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) std::memcpy(me.uuid, &prop.uuid, 16);
+    }
     me.bytes = rc ? 1 : 0;   // error flag travels with the hello so every rank fails together
     std::vector<Hello> all(P);
     int xrc = exchange(c, &me, sizeof(Hello), all.data());
@@ -810,6 +826,9 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
         c->opened.push_back((uint8_t*)p);
         c->tab.win[q] = (uint8_t*)p;
     }
+    c->tab.sysscope = (c->cfg.flags & PR_COMM_FLAG_SYS_SCOPE) ? 1 : 0;
+    for (int q = 0; q < P; ++q)
+        if (std::memcmp(all[q].uuid, me.uuid, 16) != 0) c->tab.sysscope = 1;   // a peer on another GPU
     if (!rc) rc = push_table(c);
     // barrier: nobody signals into a window before every rank has mapped every window
     int flag = rc ? 1 : 0;
@@ -839,6 +858,7 @@ extern "C" int pr_comm_init_local(pr_comm** out, int32_t P, int32_t device, cons
                 cs[r]->tab.win[q] = cs[q]->win;
                 cs[r]->tab.reg[0][q] = nullptr;   // local region 0: the whole address space, base 0
             }
+            cs[r]->tab.sysscope = (cf.flags & PR_COMM_FLAG_SYS_SCOPE) ? 1 : 0;   // one device: .gpu suffices
             if ((rc = push_table(cs[r]))) break;
         }
     }

@@ -89,11 +89,12 @@ class Worker:
         self.X = data.pin_memory() if cfg.host_data else data.to(self.dev)
         self.Y = labels.to(self.dev)
         C, H, W = cfg.shape
-        # K2 kernel chosen here (TMA for the resident data set, LSU over PCIe for host data) so the
-        # launch does no host-side pointer query
+        # K2 kernel chosen here, as the library's AUTO rule would (HWC or host data -> LSU, CHW -> TMA),
+        # so the launch does no host-side pointer query
+        lsu = cfg.host_data or cfg.channels_last
         self.gop = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE if cfg.bf16_compute else pr.GATHER_U8_TO_F32_AFFINE,
                                      [1.0 / s for s in CIFAR_STD[:C]], CIFAR_MEAN[:C], H * W,
-                                     impl=pr.GATHER_IMPL_LSU if cfg.host_data else pr.GATHER_IMPL_TMA,
+                                     impl=pr.GATHER_IMPL_LSU if lsu else pr.GATHER_IMPL_TMA,
                                      layout=pr.GATHER_LAYOUT_HWC if cfg.channels_last else pr.GATHER_LAYOUT_CHW)
         torch.backends.cudnn.benchmark = True
         torch.manual_seed(cfg.seed)                   # identical initial weights on every rank

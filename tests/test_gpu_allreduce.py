@@ -184,6 +184,17 @@ def test_staged_allgather_path():
             _check(P, L, "bf16", [3] * P, comms, seed=L)
 
 
+@pytest.mark.parametrize("P", [2, 5, 8])
+def test_system_scope_protocol(P):
+    """The multi-GPU flavour of the protocol (.sys release/acquire) on the one test GPU."""
+    comms = group(P, sys_scope=True)
+    for L in (7, 4099, 2 ** 20 + 3, 11_689_512):
+        _check(P, L, "f32", [64, 64, 64, 64, 128, 128, 256, 256][:P], comms, seed=L)
+    _check(P, 2 ** 20 + 3, "bf16", [3] * P, comms)
+    comms2 = group(P, sys_scope=True, force_staged=True)
+    _check(P, 300_001, "f32", [1 + r for r in range(P)], comms2)
+
+
 @pytest.mark.parametrize("cfg", [dict(channels=1, slots=2, slot_bytes=256, stages=2, tile_bytes=256), dict(channels=3, slots=3, slot_bytes=4096),
                                  dict(channels=32, slots=8, slot_bytes=65536, threads=256, stages=4, tile_bytes=8192),
                                  dict(channels=3, slots=4, slot_bytes=1024, force_staged=True),

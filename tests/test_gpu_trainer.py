@@ -1,0 +1,61 @@
+"""GPU checks of the harness (rows a3-a5, a9) built on the library.
+
+* the epoch-level gather (one K2 launch per epoch) yields exactly the per-step batches of P:150, bitwise;
+* the channels-last + CUDA-graph step computes the same training step as the eager NCHW step (losses
+  and parameters agree to bf16-autocast noise);
+* t_s is positive and the controller runs at the epoch boundary.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+pr = pytest.importorskip("paper_2111_08272_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _worker(**kw):
+    from paper_2111_08272_b200.trainer import RunConfig, Worker
+
+    cfg = RunConfig(N=4096, ratios=[1], C=64, g=16, micro=1024, adaptive=True, **kw)
+    return Worker(cfg, 0, 1, 0, None)
+
+
+def test_epoch_gather_equals_step_gathers():
+    for cl in (False, True):
+        w = _worker(channels_last=cl)
+        v = w.alloc.view()
+        n, S = v["n"][0], v["S"]
+        pr.shard_indices(w.alloc, 0, 3, w.cfg.seed, w.idx)
+        xe, ye = w.gather(0, S * n)
+        for s in range(S):
+            x, y = w.gather(s * n, n)
+            assert torch.equal(x.view(torch.int16), xe[s * n:(s + 1) * n].view(torch.int16))
+            assert torch.equal(y, ye[s * n:(s + 1) * n])
+
+
+def test_graphed_channels_last_step_matches_eager():
+    a = _worker(channels_last=True, graphs=True)
+    b = _worker(channels_last=False, graphs=False)
+    for _ in range(3):
+        ra, rb = a.run_epoch(), b.run_epoch()
+        assert abs(ra["loss"] - rb["loss"]) <= 2e-2 * abs(rb["loss"])
+        assert ra["t_s"] > 0 and rb["t_s"] > 0
+    pa = torch.cat([p.detach().float().flatten() for p in a.model.parameters()])
+    pb = torch.cat([p.detach().float().flatten() for p in b.model.parameters()])
+    assert float((pa - pb).norm() / pb.norm()) < 1e-2
+
+
+def test_boundary_runs_controller():
+    w = _worker()
+    assert w.boundary() is False              # first boundary: no t_s yet
+    w.run_epoch()
+    w.boundary()                              # P = 1: Eq. 10 keeps w = [C]
+    v = w.alloc.view()
+    assert v["w"] == [64] and v["epoch"] == 1

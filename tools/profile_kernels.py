@@ -31,7 +31,7 @@ def timed(fn, reps):
     return a.elapsed_time(b) / reps * 1e3   # us
 
 
-def gather(rows, row_bytes, nsrc, reps, plane, impls=(1, 2)):
+def gather(rows, row_bytes, nsrc, reps, plane, impls=(1, 2), layout=0):
     X = torch.randint(0, 256, (nsrc, row_bytes), dtype=torch.uint8, device="cuda")
     Y = torch.randint(0, 10, (nsrc,), dtype=torch.int64, device="cuda")
     idx = torch.randint(0, nsrc, (rows,), device="cuda")
@@ -39,10 +39,10 @@ def gather(rows, row_bytes, nsrc, reps, plane, impls=(1, 2)):
     lab = torch.empty(rows, dtype=torch.int64, device="cuda")
     for impl in impls:
         op = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE, [0.02, 0.02, 0.02], [120.0, 120.0, 110.0], plane,
-                               impl=impl)
+                               impl=impl, layout=layout)
         us = timed(lambda: pr.gather_rows(X, nsrc, row_bytes, idx, rows, out, op, Y, lab), reps)
         byts = rows * (3 * row_bytes + 24)
-        print(f"gather[{'LSU' if impl == 1 else 'TMA'}] rows={rows} row_bytes={row_bytes}: {us:.2f} us, "
+        print(f"gather[{'LSU' if impl == 1 else 'TMA'}{',HWC' if layout else ''}] rows={rows} row_bytes={row_bytes}: {us:.2f} us, "
               f"{byts / us / 1e3:.1f} GB/s algorithmic")
 
 
@@ -71,6 +71,8 @@ if __name__ == "__main__":
         gather(1024, 3072, 50000, reps, 1024)
     if what in ("gather_epoch", "all"):
         gather(49152, 3072, 50000, reps, 1024)          # one launch per epoch (48 steps x 1024 rows)
+    if what in ("gather_epoch_hwc", "all"):
+        gather(49152, 3072, 50000, reps, 1024, impls=(2, 1) if what == "all" else (2,), layout=1)  # bench form
     if what in ("gather_imagenet", "all"):
         gather(336, 150528, 2000, reps, 50176)
     if what in ("shard", "all"):
