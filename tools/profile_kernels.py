@@ -72,7 +72,9 @@ if __name__ == "__main__":
     if what in ("gather_epoch", "all"):
         gather(49152, 3072, 50000, reps, 1024)          # one launch per epoch (48 steps x 1024 rows)
     if what in ("gather_epoch_hwc", "all"):
-        gather(49152, 3072, 50000, reps, 1024, impls=(2, 1) if what == "all" else (2,), layout=1)  # bench form
+        gather(49152, 3072, 50000, reps, 1024, impls=(2, 1) if what == "all" else (2,), layout=1)
+    if what == "gather_epoch_hwc_lsu":                 # exactly the bench's launch (channels-last, LSU)
+        gather(49152, 3072, 50000, reps, 1024, impls=(1,), layout=1)
     if what in ("gather_imagenet", "all"):
         gather(336, 150528, 2000, reps, 50176)
     if what in ("shard", "all"):
