@@ -167,34 +167,49 @@ class Worker:
         sigma = self.cfg.slowdown[self.rank] if self.cfg.slowdown else 1.0
         return int((sigma - 1.0) * self.c0_ns * n_r) if sigma > 1.0 and self.c0_ns > 0 else 0
 
+    def prepare(self, n_r: int, calib_reps: int = 3):
+        """Capture the forward/backward of n_r rows in a CUDA graph and time its replay, t1(n_r) — the
+        rank's compute time at σ = 1.  Done OUTSIDE any timed region (warm-up and capture would otherwise
+        pollute t_s).  Capture is rank-local (no collective inside), so a rank whose n_r changes
+        re-captures alone."""
+        if n_r <= 0 or n_r in self._graphs:
+            return
+        xs = torch.randn((n_r, self.row_bytes), device=self.dev).to(self.xdt)
+        ys = torch.randint(0, self.cfg.classes, (n_r,), device=self.dev)
+        side = torch.cuda.Stream(self.dev)
+        side.wait_stream(self.stream)
+        launches, save = self.launches, self.cfg.slowdown
+        self.cfg.slowdown = None                              # the spin is launched after the replay
+        with torch.cuda.stream(side):
+            self.compute(xs, ys, n_r)                         # warm-up (cuDNN autotune, allocator)
+        self.stream.wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            loss = self.compute(xs, ys, n_r)
+        self.stream.wait_stream(side)
+        self.cfg.slowdown, self.launches = save, launches
+        g.replay()                                            # warm replay, then t1(n_r)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(self.stream)
+        for _ in range(calib_reps):
+            g.replay()
+        b.record(self.stream)
+        b.synchronize()
+        self.flat.zero_()                                     # discard the warm-up/calibration gradients
+        self._graphs[n_r] = (g, xs, ys, loss, a.elapsed_time(b) * 1e6 / calib_reps)
+
     def compute_graphed(self, x, y, n_r: int):
-        """a4 through a CUDA graph: static input buffers, captured forward/backward (+ K4 spin).
-        Capture is rank-local (no collective inside), so a rank whose n_r changes re-captures alone."""
-        key = (n_r, self._spin_ns(n_r))
-        st = self._graphs.get(key)
-        if st is None:
-            xs = torch.empty((n_r, self.row_bytes), dtype=self.xdt, device=self.dev)
-            ys = torch.zeros(n_r, dtype=torch.int64, device=self.dev)
-            xs.copy_(x[:n_r])
-            ys.copy_(y[:n_r])
-            side = torch.cuda.Stream(self.dev)
-            side.wait_stream(self.stream)
-            launches = self.launches
-            with torch.cuda.stream(side):
-                self.compute(xs, ys, n_r)                     # warm-up (cuDNN autotune, allocator)
-            self.stream.wait_stream(side)
-            self.flat.zero_()                                 # the warm-up's gradients are discarded
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=side):
-                loss = self.compute(xs, ys, n_r)
-            self.stream.wait_stream(side)
-            self.launches = launches
-            st = self._graphs[key] = (g, xs, ys, loss, key[1] > 0)
-        g, xs, ys, loss, spins = st
+        """a4 through the captured graph; emulated slowdown σ_r (K4): a rank σ× slower takes σ× its own
+        measured compute time, so the spin is (σ_r − 1)·t1(n_r) for the n_r it actually processes."""
+        self.prepare(n_r)
+        g, xs, ys, loss, t1_ns = self._graphs[n_r]
         xs.copy_(x[:n_r])
         ys.copy_(y[:n_r])
         g.replay()
-        self.launches += 1 if spins else 0                    # K4 inside the graph
+        sigma = self.cfg.slowdown[self.rank] if self.cfg.slowdown else 1.0
+        if sigma > 1.0:
+            pr.spin(int((sigma - 1.0) * t1_ns), stream=self.stream)
+            self.launches += 1
         return loss.clone()
 
     # ---- a6-a9: weighted ring allreduce + SGD (Algorithm 1 steps 5-6) ---------------------------------
@@ -216,6 +231,8 @@ class Worker:
         cfg = self.cfg
         v = self.alloc.view()
         n_r, S = v["n"][self.rank], v["S"]
+        if cfg.graphs:
+            self.prepare(n_r)                                 # capture + t1(n_r) outside the timed region
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(self.stream)
         pr.shard_indices(self.alloc, self.rank, self.epoch, cfg.seed, self.idx, stream=self.stream)   # a2
