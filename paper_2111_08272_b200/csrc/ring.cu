@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
         for (int k = 0; k < kStages; ++k) {
             mbar_init(&sh.full[k], 1);
             mbar_init(&sh.stored[k], (uint32_t)(nc / 32));
-            mbar_init(&sh.empty[k], (uint32_t)(nc / 32 + 1));
+            mbar_init(&sh.empty[k], 1);                     // the signal warp, after `stored`
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const unsigned long long seq = st->seq + 1;
@@ -467,11 +467,11 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                         if (needs_in(kind)) tx += vb;
                     }
                     sh.tile_ok[stg] = bad ? 0 : 1;
-                    mbar_arrive_expect_tx(&sh.full[stg], tx);
-                    if (!bad && vb) {
+                    if (!bad && vb) {      // copies first, then the arrive that carries their byte count
                         if (needs_g(kind)) tma_load(gs, gsrc + e0, vb, &sh.full[stg]);
                         if (needs_in(kind)) tma_load(is, isrc + e0, vb, &sh.full[stg]);
                     }
+                    mbar_arrive_expect_tx(&sh.full[stg], tx);
                 }
                 if (reads_slot(kind)) ++consJ;
                 if (writes_slot(kind)) ++prodJ;
@@ -495,13 +495,17 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 bool ok = true;
                 for (int64_t t = 0; t < nt; ++t, ++tc) {
                     const int stg = (int)(tc % (uint32_t)kStages);
-                    if (sends) mbar_wait(&sh.stored[stg], (tc / (uint32_t)kStages) & 1);
+                    // wait for EVERY tile's phase: try_wait.parity cannot tell phase k+1 from k−1, so a
+                    // skipped phase would let a later wait on this stage return early (found by synccheck)
+                    mbar_wait(&sh.stored[stg], (tc / (uint32_t)kStages) & 1);
                     ok = ok && sh.tile_ok[stg] != 0;
+                    // stage free: consumers read it before arriving on `stored`; the chain consumer ->
+                    // stored -> signal -> empty -> producer is transitive (release/acquire at each step)
+                    mbar_arrive(&sh.empty[stg]);
                     if (t == nt - 1 && sends && ok) {
                         if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
                         else st_release(&nxf->rs_ready, prodJ + 1, sys);
                     }
-                    mbar_arrive(&sh.empty[stg]);
                 }
                 if (nt == 0 && sends && !*(volatile int*)&sh.err) {   // empty slice: nothing to wait for
                     if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
@@ -567,8 +571,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(&sh.stored[stg]);                   // release.cta: this warp's stores precede
-                    mbar_arrive(&sh.empty[stg]);
+                    mbar_arrive(&sh.stored[stg]);   // release.cta: this warp's smem reads and stores precede
                 }
             }
             const bool err = *(volatile int*)&sh.err != 0;
