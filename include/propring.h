@@ -184,7 +184,20 @@ typedef struct {
     int64_t watchdog_ns;  /* spin-wait deadline per call (default 10 s); <= 0 disables               */
     int32_t stages;       /* TMA smem pipeline depth per CTA, 2..16 (default 6)                       */
     int32_t tile_bytes;   /* bytes per input per pipeline stage, multiple of 16, <= 32768 (default 16384) */
+    int32_t algo;         /* PR_ALGO_* (default PR_ALGO_RING)                                         */
+    int32_t ts_slots;     /* two-shot staging slots per (channel, source), >= 2 (default 2)          */
+    int64_t ts_slot_bytes;/* two-shot slice bytes, multiple of 256 (default 65536)                   */
+    int64_t ts_max_bytes; /* PR_ALGO_AUTO: two-shot for buffers up to this many bytes (default 4 MiB)  */
 } pr_comm_config;
+
+/* Allreduce algorithm.  Both compute the same bits (the two-shot reducer adds the contributions in the
+ * ring's order with the ring's per-hop rounding).  Two-shot: each rank pushes its raw
+ * slice of chunk d to rank d (one hop), rank d reduces and stores the result into every peer's
+ * registered buffer (second hop) — 2 synchronisation phases instead of 2(P−1); it needs every rank's
+ * buffer registered (else PR_ERR_INVALID is latched on all ranks). */
+#define PR_ALGO_RING     0
+#define PR_ALGO_TWO_SHOT 1
+#define PR_ALGO_AUTO     2   /* two-shot when count·elem_size <= ts_max_bytes, ring above */
 
 /* Byte allgather supplied by the caller (e.g. over a torch process group): every rank passes `len`
  * bytes in `send` and receives the P·len bytes of all ranks, rank-ordered, in `recv`.  Returns 0 on

@@ -55,7 +55,13 @@ struct ChanState {          // local only: cumulative counters carried across ca
     unsigned long long seq;         // handshake sequence number
     unsigned long long slot_base;   // staging-slot slices produced (= consumed: uniform slicing)
     unsigned long long ag_base;     // direct all-gather slices sent (= received)
-    uint64_t pad[13];
+    unsigned long long ts_base;     // two-shot slices processed (every rank processes the same number)
+    uint64_t pad[12];
+};
+struct TsFlags {            // two-shot flags, one counter per peer (index = the peer that writes it)
+    unsigned long long ready[PR_MAX_RANKS];    // by q: slices of its raw contribution stored in my staging
+    unsigned long long credit[PR_MAX_RANKS];   // by q: slices of MY contribution it has consumed
+    unsigned long long ag[PR_MAX_RANKS];       // by q: slices of its reduced chunk stored into my buffer
 };
 struct AgEntry {
     unsigned long long seq;
@@ -72,6 +78,9 @@ struct DevTable {
     int64_t slot_bytes;
     int64_t watchdog_ns;
     uint64_t off_flags, off_hs, off_state, off_ag, off_staging, window_bytes;
+    uint64_t off_ts_flags, off_ts_staging;
+    int32_t ts_slots, pad1;
+    int64_t ts_slot_bytes;
     volatile int* status;           // host-mapped
     volatile long long* stamps;     // host-mapped [3]
     uint8_t* win[PR_MAX_RANKS];
@@ -107,6 +116,10 @@ void layout(DevTable& t) {
     o += 2ull * t.P * sizeof(AgEntry);
     t.off_staging = o = align_up(o, 4096);
     o += (uint64_t)t.channels * t.slots * (uint64_t)t.slot_bytes;
+    t.off_ts_flags = o = align_up(o, 4096);
+    o += (uint64_t)t.channels * sizeof(TsFlags);
+    t.off_ts_staging = o = align_up(o, 4096);
+    o += (uint64_t)t.channels * t.P * t.ts_slots * (uint64_t)t.ts_slot_bytes;
     t.window_bytes = align_up(o, 4096);
 }
 
@@ -303,6 +316,49 @@ __device__ __forceinline__ void for_each_step(int P, int r, int64_t nsl, int64_t
     }
 }
 
+// Handshake = the barrier; its duration is t_w.  Thread 0 only.  Publishes (seq, count,
+// dtype, n_r, registration) into every rank's page and waits for all P entries of this call (entries are
+// double-buffered by seq parity).  Returns Σn and whether every rank's buffer is registered; fills ns[q]
+// (n of rank q) and bufs[q] (rank q's buffer mapped in this process, if registered) when given.
+struct HsOut {
+    int err;
+    int direct;
+    long long sumn;
+};
+__device__ HsOut handshake(const LaunchArgs& A, const RankCall& rc, const DevTable* tab, ChanState* st, int ch, bool sys,
+                           unsigned long long deadline, long long* ns, uint8_t** bufs) {
+    const int r = tab->rank, P = tab->P;
+    uint8_t* my = tab->win[r];
+    const unsigned long long seq = st->seq + 1;
+    const int par = (int)(seq & 1ull);
+    for (int q = 0; q < P; ++q) {
+        HsEntry* e = hs_of(tab->win[q], tab, ch, par, r);
+        st_relaxed_s64(&e->count, A.count, sys);
+        st_relaxed_s64(&e->n, rc.n_local, sys);
+        st_relaxed_s64(&e->dtype, ((long long)rc.reg_id << 32) | (unsigned)A.dtype, sys);  // dtype | reg_id
+        st_relaxed_s64(&e->offset, rc.reg_off, sys);
+        st_release(&e->seq, seq, sys);
+    }
+    HsOut o{0, 1, 0};
+    for (int q = 0; q < P && !o.err; ++q) {
+        HsEntry* e = hs_of(my, tab, ch, par, q);
+        if (!wait_ge(&e->seq, seq, deadline, sys)) { o.err = PR_ERR_PEER_TIMEOUT; break; }
+        const long long cnt = ld_relaxed_s64(&e->count, sys);
+        const long long n = ld_relaxed_s64(&e->n, sys);
+        const long long dr = ld_relaxed_s64(&e->dtype, sys);
+        const long long off = ld_relaxed_s64(&e->offset, sys);
+        const int dt = (int)(dr & 0xffffffffll), rid = (int)(dr >> 32);
+        if (cnt != A.count || dt != A.dtype) o.err = PR_ERR_LENGTH_MISMATCH;
+        o.sumn += n;
+        if (rid < 0) o.direct = 0;
+        if (ns) ns[q] = n;
+        if (bufs) bufs[q] = rid >= 0 ? (uint8_t*)((uintptr_t)tab->reg[rid][q] + (uintptr_t)off) : nullptr;
+    }
+    if (!o.err && o.sumn <= 0) o.err = PR_ERR_ZERO_SAMPLES;
+    st->seq = seq;
+    return o;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ LaunchArgs A) {
     extern __shared__ __align__(128) uint8_t smem[];   // [stages][2][tile_bytes]: g tile, recv tile
@@ -335,39 +391,12 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
             mbar_init(&sh.empty[k], 1);                     // the signal warp, after `stored`
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const unsigned long long seq = st->seq + 1;
-        const int par = (int)(seq & 1ull);
-        for (int q = 0; q < P; ++q) {
-            HsEntry* e = hs_of(tab->win[q], tab, ch, par, r);
-            st_relaxed_s64(&e->count, A.count, sys);
-            st_relaxed_s64(&e->n, rc.n_local, sys);
-            st_relaxed_s64(&e->dtype, ((long long)rc.reg_id << 32) | (unsigned)A.dtype, sys);  // dtype | reg_id
-            st_relaxed_s64(&e->offset, rc.reg_off, sys);
-            st_release(&e->seq, seq, sys);
-        }
-        int err = 0, direct = 1, next_reg = -1;
-        long long sumn = 0, next_off = 0;
-        for (int q = 0; q < P && !err; ++q) {
-            HsEntry* e = hs_of(my, tab, ch, par, q);
-            if (!wait_ge(&e->seq, seq, deadline, sys)) { err = PR_ERR_PEER_TIMEOUT; break; }
-            const long long cnt = ld_relaxed_s64(&e->count, sys);
-            const long long n = ld_relaxed_s64(&e->n, sys);
-            const long long dr = ld_relaxed_s64(&e->dtype, sys);
-            const long long off = ld_relaxed_s64(&e->offset, sys);
-            const int dt = (int)(dr & 0xffffffffll), rid = (int)(dr >> 32);
-            if (cnt != A.count || dt != A.dtype) err = PR_ERR_LENGTH_MISMATCH;
-            sumn += n;
-            if (rid < 0) direct = 0;
-            if (q == next) { next_reg = rid; next_off = off; }
-        }
-        if (!err && sumn <= 0) err = PR_ERR_ZERO_SAMPLES;
-        st->seq = seq;
-        sh.err = err;
-        sh.direct = direct;
-        sh.sumn = sumn;
-        sh.next_buf = (direct && next_reg >= 0)
-                          ? (void*)((uintptr_t)tab->reg[next_reg][next] + (uintptr_t)next_off)
-                          : nullptr;
+        __shared__ uint8_t* s_bufs[PR_MAX_RANKS];
+        const HsOut hs = handshake(A, rc, tab, st, ch, sys, deadline, nullptr, s_bufs);
+        sh.err = hs.err;
+        sh.direct = hs.direct;
+        sh.sumn = hs.sumn;
+        sh.next_buf = hs.direct ? (void*)s_bufs[next] : nullptr;
         if (ch == 0) tab->stamps[1] = (long long)gtimer();
     }
     __syncthreads();
@@ -590,6 +619,194 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
     }
 }
 
+// =====================================================================================================
+// Two-shot variant: 2 synchronisation phases instead of 2(P−1) — NVSwitch gives every
+// peer full bandwidth, so the ring's hop chain is only needed for its order, not its topology.
+//   phase A  rank r pushes its RAW slice i of every other chunk d into rank d's staging [src r]
+//   phase B  rank d reduces chunk d's slice i in the ring's order (d, d+1, …, d+P−1) with the ring's
+//            per-hop rounding — so the result is bit-identical to ring_kernel — and stores it into its
+//            own buffer and every peer's registered buffer (direct all-gather)
+// Per-peer counters in TsFlags: ready (data landed), credit (slot consumed), ag (reduced slice landed).
+// K2 >= 2 staging slots per (channel, source): to push slice i+1 a rank needs the credit for slice
+// i+1−K2, returned by the destination's phase B of that slice, which precedes its phase A of slice
+// i+2−K2 ≤ i — so the schedule cannot deadlock.
+// =====================================================================================================
+__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {     // L2-coherent load of peer-written data
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ TsFlags* ts_flags_of(uint8_t* w, const DevTable* t, int ch) {
+    return reinterpret_cast<TsFlags*>(w + t->off_ts_flags) + ch;
+}
+__device__ __forceinline__ uint8_t* ts_slot_of(uint8_t* w, const DevTable* t, int ch, int src, unsigned long long J) {
+    return w + t->off_ts_staging +
+           (((size_t)ch * t->P + src) * t->ts_slots + (size_t)(J % (unsigned long long)t->ts_slots)) * t->ts_slot_bytes;
+}
+template <typename T> __device__ __forceinline__ float rnd_dtype(float x);
+template <> __device__ __forceinline__ float rnd_dtype<float>(float x) { return x; }
+template <> __device__ __forceinline__ float rnd_dtype<__nv_bfloat16>(float x) {
+    return __bfloat162float(__float2bfloat16_rn(x));
+}
+template <typename T> __device__ __forceinline__ float lane_f(const uint4& v, int j);
+template <> __device__ __forceinline__ float lane_f<float>(const uint4& v, int j) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    return __uint_as_float(w[j]);
+}
+template <> __device__ __forceinline__ float lane_f<__nv_bfloat16>(const uint4& v, int j) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    return (j & 1) ? __uint_as_float(w[j >> 1] & 0xffff0000u) : __uint_as_float(w[j >> 1] << 16);
+}
+template <typename T> __device__ __forceinline__ uint4 pack_f(const float* f);
+template <> __device__ __forceinline__ uint4 pack_f<float>(const float* f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+}
+template <> __device__ __forceinline__ uint4 pack_f<__nv_bfloat16>(const float* f) {
+    return make_uint4(Vec<__nv_bfloat16>::pack(f[0], f[1]), Vec<__nv_bfloat16>::pack(f[2], f[3]),
+                      Vec<__nv_bfloat16>::pack(f[4], f[5]), Vec<__nv_bfloat16>::pack(f[6], f[7]));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__ LaunchArgs A) {
+    __shared__ int s_err;
+    __shared__ long long s_sumn;
+    __shared__ long long s_n[PR_MAX_RANKS];
+    __shared__ uint8_t* s_bufs[PR_MAX_RANKS];
+    __shared__ float s_w[PR_MAX_RANKS];
+    const RankCall& rc = A.calls[blockIdx.y];
+    const DevTable* tab = rc.tab;
+    const int ch = blockIdx.x;
+    const int r = tab->rank, P = tab->P;
+    uint8_t* my = tab->win[r];
+    ChanState* st = state_of(my, tab, ch);
+    TsFlags* mf = ts_flags_of(my, tab, ch);
+    const bool t0 = threadIdx.x == 0;
+    const bool sys = tab->sysscope != 0;
+    unsigned long long deadline = ~0ull;
+    if (t0) {
+        const unsigned long long start = gtimer();
+        if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
+        if (ch == 0) tab->stamps[0] = (long long)start;
+        const HsOut hs = handshake(A, rc, tab, st, ch, sys, deadline, s_n, s_bufs);
+        s_err = hs.err ? hs.err : (hs.direct ? 0 : PR_ERR_INVALID);   // two-shot needs registered buffers
+        s_sumn = hs.sumn;
+        for (int q = 0; q < P; ++q) s_w[q] = hs.sumn > 0 ? (float)((double)s_n[q] / (double)hs.sumn) : 0.0f;
+        if (ch == 0) tab->stamps[1] = (long long)gtimer();
+    }
+    __syncthreads();
+    if (s_err) {
+        if (t0) latch(tab, s_err);
+        return;
+    }
+    constexpr int V = Vec<T>::V;
+    const int64_t count = A.count;
+    const int64_t per = (count + P - 1) / P;
+    const int64_t cs = (per + V - 1) / V * V;
+    const int64_t subp = (cs + tab->channels - 1) / tab->channels;
+    const int64_t sub = (subp + V - 1) / V * V;
+    const int64_t sl = tab->ts_slot_bytes / (int64_t)sizeof(T);
+    const int64_t nsl = sub > 0 ? (sub + sl - 1) / sl : 0;
+    const unsigned long long K2 = (unsigned long long)tab->ts_slots;
+    const unsigned long long base = st->ts_base;
+    T* buf = reinterpret_cast<T*>(rc.buf);
+    auto range = [&](int c, int64_t i, int64_t& lo, int64_t& len) {
+        const int64_t clo = (int64_t)c * cs;
+        const int64_t chi = min(clo + cs, count);
+        const int64_t a = clo + (int64_t)ch * sub + i * sl;
+        const int64_t b = min(min(a + sl, clo + min((int64_t)(ch + 1) * sub, cs)), chi);
+        lo = a;
+        len = b > a ? b - a : 0;
+    };
+    __shared__ int s_abort;
+    if (t0) s_abort = 0;
+    auto sync_ok = [&]() -> bool {
+        __syncthreads();
+        return s_abort == 0;
+    };
+    auto fail = [&]() {
+        s_abort = 1;
+        latch(tab, PR_ERR_PEER_TIMEOUT);
+    };
+    for (int64_t i = 0; i < nsl; ++i) {
+        const unsigned long long J = base + (unsigned long long)i;
+        // ---- phase A: raw slice i of every chunk d != r -> rank d's staging [src r], all peers at once --------
+        if (t0 && J + 1 > K2)
+            for (int k = 1; k < P && !s_abort; ++k)
+                if (!wait_ge(&mf->credit[(r + k) % P], J + 1 - K2, deadline, sys)) fail();
+        if (!sync_ok()) return;
+        for (int k = 1; k < P; ++k) {                               // no barrier between destinations
+            const int d = (r + k) % P;
+            int64_t lo, len;
+            range(d, i, lo, len);
+            T* dst = reinterpret_cast<T*>(ts_slot_of(tab->win[d], tab, ch, r, J));
+            const int64_t nv = len / V;
+            for (int64_t v = threadIdx.x; v < nv; v += blockDim.x)
+                st_v4(dst + v * V, *reinterpret_cast<const uint4*>(buf + lo + v * V));
+            for (int64_t e = nv * V + threadIdx.x; e < len; e += blockDim.x) dst[e] = buf[lo + e];
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < P - 1) {                              // one releasing thread per peer
+            const int d = (r + 1 + (int)threadIdx.x) % P;
+            st_release(&ts_flags_of(tab->win[d], tab, ch)->ready[r], J + 1, sys);
+        }
+        // ---- phase B: reduce chunk r's slice i in ring order, store into every rank's buffer -------------
+        int64_t lo, len;
+        range(r, i, lo, len);
+        if (t0)
+            for (int h = 1; h < P && !s_abort; ++h) {
+                const int q = (r + h) % P;
+                if (!wait_ge(&mf->ready[q], J + 1, deadline, sys)) fail();
+            }
+        if (!sync_ok()) return;
+        const int64_t nv = len / V;
+        for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+            float acc[V];
+#pragma unroll
+            for (int j = 0; j < V; ++j) acc[j] = 0.0f;
+            for (int h = 0; h < P; ++h) {
+                const int q = (r + h) % P;
+                const uint4 x = (q == r) ? *reinterpret_cast<const uint4*>(buf + lo + v * V)
+                                         : ld_cg_v4(ts_slot_of(my, tab, ch, q, J) + (size_t)v * 16);
+                if (s_n[q] <= 0) continue;                   // n_q = 0 contributes nothing (never multiplied)
+                const float sq = s_w[q];
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    acc[j] = rnd_dtype<T>(h == 0 ? __fmul_rn(sq, lane_f<T>(x, j)) : __fmaf_rn(sq, lane_f<T>(x, j), acc[j]));
+            }
+            const uint4 y = pack_f<T>(acc);
+            for (int q = 0; q < P; ++q) st_v4(reinterpret_cast<T*>(s_bufs[q]) + lo + v * V, y);
+        }
+        for (int64_t e = nv * V + threadIdx.x; e < len; e += blockDim.x) {   // ragged tail: end of buffer
+            float acc = 0.0f;
+            for (int h = 0; h < P; ++h) {
+                const int q = (r + h) % P;
+                const T xv = (q == r) ? buf[lo + e] : reinterpret_cast<const T*>(ts_slot_of(my, tab, ch, q, J))[e];
+                if (s_n[q] <= 0) continue;
+                acc = rnd_dtype<T>(h == 0 ? __fmul_rn(s_w[q], Vec<T>::to_f(xv)) : __fmaf_rn(s_w[q], Vec<T>::to_f(xv), acc));
+            }
+            for (int q = 0; q < P; ++q) reinterpret_cast<T*>(s_bufs[q])[lo + e] = Vec<T>::from_f(acc);
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < P - 1) {                              // one releasing thread per peer
+            const int q = (r + 1 + (int)threadIdx.x) % P;
+            TsFlags* qf = ts_flags_of(tab->win[q], tab, ch);
+            st_relaxed_u64(&qf->credit[r], J + 1, sys);       // its slot in my staging is free again
+            st_release(&qf->ag[r], J + 1, sys);               // my reduced slice i is in its buffer
+        }
+    }
+    // every other rank's reduced chunk has landed in my buffer
+    if (t0)
+        for (int h = 1; h < P && !s_abort; ++h) {
+            const int q = (r + h) % P;
+            if (!wait_ge(&mf->ag[q], base + (unsigned long long)nsl, deadline, sys)) fail();
+        }
+    __syncthreads();
+    if (t0) {
+        if (!s_abort) st->ts_base = base + (unsigned long long)nsl;
+        if (ch == 0) tab->stamps[2] = (long long)gtimer();
+    }
+}
+
 __global__ void allgather_f64_kernel(const DevTable* tab, unsigned long long seq, double v, double* out) {
     if (threadIdx.x != 0) return;
     const bool sys = tab->sysscope != 0;
@@ -627,7 +844,8 @@ struct Reg {
 
 struct Hello {
     cudaIpcMemHandle_t handle;
-    int32_t P, rank, device, channels, slots, threads, stages, tile_bytes;
+    int32_t P, rank, device, channels, slots, threads, stages, tile_bytes, algo, ts_slots;
+    int64_t ts_slot_bytes, ts_max_bytes;
     int64_t slot_bytes, window_bytes;
     uint64_t bytes;   // registration size
     unsigned char uuid[16];   // device identity: peers on another GPU need .sys-scope synchronisation
@@ -668,6 +886,10 @@ pr_comm_config default_config() {
     c.watchdog_ns = 10ll * 1000 * 1000 * 1000;
     c.stages = 6;
     c.tile_bytes = 16384;
+    c.algo = PR_ALGO_RING;
+    c.ts_slots = 2;
+    c.ts_slot_bytes = 64 * 1024;
+    c.ts_max_bytes = 4ll << 20;     // measured crossover (co-located P = 4, 8): two-shot wins up to ~4 MiB
     return c;
 }
 
@@ -675,7 +897,9 @@ int check_config(const pr_comm_config& c) {
     if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
-        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024)
+        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_AUTO ||
+        c.ts_slots < 2 || c.ts_slots > 16 || c.ts_slot_bytes < 256 || c.ts_slot_bytes % 256 ||
+        c.ts_slot_bytes > (16ll << 20) || c.ts_max_bytes < 0)
         return PR_ERR_INVALID;
     return PR_OK;
 }
@@ -691,6 +915,8 @@ int alloc_common(pr_comm* c) {
     t.watchdog_ns = c->cfg.watchdog_ns;
     t.stages = c->cfg.stages;
     t.tile_bytes = c->cfg.tile_bytes;
+    t.ts_slots = c->cfg.ts_slots;
+    t.ts_slot_bytes = c->cfg.ts_slot_bytes;
     layout(t);
     PR_CUDA_TRY(cudaMalloc((void**)&c->win, t.window_bytes));
     PR_CUDA_TRY(cudaMemset(c->win, 0, t.window_bytes));
@@ -762,6 +988,19 @@ size_t dtype_size(int32_t dt) { return dt == PR_DTYPE_F32 ? 4 : (dt == PR_DTYPE_
 
 int launch_ring(const LaunchArgs& a, int nranks, const pr_comm_config& cfg, cudaStream_t s, bool coop) {
     const int32_t threads = cfg.threads, channels = cfg.channels;
+    // algorithm: a pure function of (config, count, dtype), identical on every rank
+    const int64_t bytes = a.count * (a.dtype == PR_DTYPE_F32 ? 4 : 2);
+    if (cfg.algo == PR_ALGO_TWO_SHOT || (cfg.algo == PR_ALGO_AUTO && bytes <= cfg.ts_max_bytes)) {
+        void* fn2 = (a.dtype == PR_DTYPE_F32) ? (void*)twoshot_kernel<float> : (void*)twoshot_kernel<__nv_bfloat16>;
+        void* args2[] = {(void*)&a};
+        const dim3 grid2((unsigned)channels, (unsigned)nranks), block2((unsigned)threads);
+        if (coop) {
+            PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn2, grid2, block2, args2, 0, s));
+        } else {
+            PR_CUDA_TRY(cudaLaunchKernel(fn2, grid2, block2, args2, 0, s));
+        }
+        return PR_OK;
+    }
     void* fn = (a.dtype == PR_DTYPE_F32) ? (void*)ring_kernel<float> : (void*)ring_kernel<__nv_bfloat16>;
     const size_t smem = (size_t)cfg.stages * 2 * cfg.tile_bytes;
     static size_t attr_set[2] = {0, 0};
@@ -801,6 +1040,8 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
     me.P = P; me.rank = rank; me.device = device; me.channels = c->cfg.channels; me.slots = c->cfg.slots;
     me.threads = c->cfg.threads; me.slot_bytes = c->cfg.slot_bytes; me.window_bytes = (int64_t)c->tab.window_bytes;
     me.stages = c->cfg.stages; me.tile_bytes = c->cfg.tile_bytes;
+    me.algo = c->cfg.algo; me.ts_slots = c->cfg.ts_slots; me.ts_slot_bytes = c->cfg.ts_slot_bytes;
+    me.ts_max_bytes = c->cfg.ts_max_bytes;
     {
         cudaDeviceProp prop;
         if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) std::memcpy(me.uuid, &prop.uuid, 16);
@@ -813,7 +1054,8 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
         const Hello& h = all[q];
         if (h.bytes) rc = rc ? rc : PR_ERR_CUDA;
         if (h.P != P || h.rank != q || h.channels != me.channels || h.slots != me.slots || h.slot_bytes != me.slot_bytes ||
-            h.threads != me.threads || h.stages != me.stages || h.tile_bytes != me.tile_bytes)
+            h.threads != me.threads || h.stages != me.stages || h.tile_bytes != me.tile_bytes || h.algo != me.algo ||
+            h.ts_slots != me.ts_slots || h.ts_slot_bytes != me.ts_slot_bytes || h.ts_max_bytes != me.ts_max_bytes)
             rc = rc ? rc : PR_ERR_INVALID;
     }
     if (rc) { free_comm(c); return rc; }

@@ -268,3 +268,56 @@ def test_timestamps_and_status():
     for c in comms:
         t = c.timestamps()
         assert 0 < t[0] <= t[1] <= t[2]
+
+
+# ---- two-shot variant: same bits as the ring -------------------------------------------
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("P", [2, 3, 5, 8])
+def test_two_shot_bit_identical_to_ring_replay(P, dtype):
+    comms = group(P, algo=pr.ALGO_TWO_SHOT)
+    rng = np.random.Generator(np.random.PCG64(100 + P))
+    for L in (1, 7, P + 1, 4099, 2 ** 20 + 3):
+        n = [int(x) * 16 for x in rng.integers(1, 9, P)]
+        if L % 2:
+            n[int(rng.integers(0, P))] = 0
+        _check(P, L, dtype, n, comms, kind="mixed" if L % 3 == 0 else "gaussian", seed=L)
+
+
+def test_two_shot_small_slots_many_slices_and_sys_scope():
+    for cfg in (dict(ts_slots=2, ts_slot_bytes=256, channels=3), dict(ts_slots=3, ts_slot_bytes=4096, sys_scope=True)):
+        for P in (2, 4):
+            comms = group(P, algo=pr.ALGO_TWO_SHOT, **cfg)
+            for L in (999, 300_001):
+                _check(P, L, "f32", [5] * (P - 1) + [1], comms, seed=L)
+                _check(P, L, "bf16", [2] * P, comms, seed=L)
+
+
+def test_auto_mixes_algorithms_back_to_back():
+    """ALGO_AUTO: two-shot up to ts_max_bytes, ring above; interleaved calls share the handshake sequence."""
+    P = 4
+    comms = group(P, algo=pr.ALGO_AUTO, ts_max_bytes=1 << 20)
+    for it, L in enumerate([100, 2 ** 20, 3, 300_000, 5_000_000, 17]):   # 400 B .. 20 MB
+        _check(P, L, "f32" if it % 2 else "bf16", [it + 1, 2, 0 if it == 3 else 3, 4], comms, seed=it)
+
+
+def test_two_shot_graph_replay():
+    P, L = 3, 40_000
+    comms = group(P, algo=pr.ALGO_TWO_SHOT)
+    host, dev = _inputs(P, L, "f32", seed=21)
+    src = [d.clone() for d in dev]
+    n = [3, 1, 2]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        pr.weighted_allreduce_local(comms, dev, n, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            pr.weighted_allreduce_local(comms, dev, n, stream=s)
+    emu = W.ring_emulate(host, n, "f32")
+    for _ in range(3):
+        for d, s0 in zip(dev, src):
+            d.copy_(s0)
+        g.replay()
+        torch.cuda.synchronize()
+        assert all(np.array_equal(d.cpu().numpy(), emu) for d in dev)

@@ -60,8 +60,8 @@ def sizes(max_mib):
     return s
 
 
-def run_colocated(P, max_mib, reps):
-    comms = pr.comm_init_local(P, 0, pr.comm_config())
+def run_colocated(P, max_mib, reps, algo=0):
+    comms = pr.comm_init_local(P, 0, pr.comm_config(algo=algo))
     n = weights(P)
     for dtype, es in ((torch.float32, 4), (torch.bfloat16, 2)):
         for Z in sizes(max_mib):
@@ -82,7 +82,7 @@ def run_colocated(P, max_mib, reps):
             torch.cuda.synchronize()
             us = a.elapsed_time(b) / reps * 1e3
             hbm = (6 + 5 * (P - 2)) * Z / (us * 1e-6) / 1e9
-            print(json.dumps({"mode": "colocated", "P": P, "dtype": str(dtype).split(".")[-1], "bytes": Z, "us": us,
+            print(json.dumps({"mode": "colocated", "algo": algo, "P": P, "dtype": str(dtype).split(".")[-1], "bytes": Z, "us": us,
                               "hbm_algorithmic_GBs": hbm, "max_err": err, "zero_violations": zb}), flush=True)
             del bufs
     for c in comms:
@@ -152,8 +152,9 @@ if __name__ == "__main__":
     ap.add_argument("--colocated", type=int, default=0)
     ap.add_argument("--max-mib", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--algo", type=int, default=0, help="0 ring, 1 two-shot, 2 auto")
     a = ap.parse_args()
     if a.colocated:
-        run_colocated(a.colocated, a.max_mib, a.reps)
+        run_colocated(a.colocated, a.max_mib, a.reps, a.algo)
     else:
         run_multi(a.max_mib, a.reps)
