@@ -325,13 +325,17 @@ struct HsOut {
     int direct;
     long long sumn;
 };
+// Executed by ALL 32 lanes of warp 0: lane q publishes into rank q's page and polls entry q of this
+// page (ranks q, q+32, …), so the P peers are contacted in parallel; Σn, "all registered" and the error
+// code are combined with warp shuffles (DESIGN.md §3 #37).  The result is valid in every lane.
 __device__ HsOut handshake(const LaunchArgs& A, const RankCall& rc, const DevTable* tab, ChanState* st, int ch, bool sys,
                            unsigned long long deadline, long long* ns, uint8_t** bufs) {
     const int r = tab->rank, P = tab->P;
+    const int lane = threadIdx.x & 31;
     uint8_t* my = tab->win[r];
     const unsigned long long seq = st->seq + 1;
     const int par = (int)(seq & 1ull);
-    for (int q = 0; q < P; ++q) {
+    for (int q = lane; q < P; q += 32) {
         HsEntry* e = hs_of(tab->win[q], tab, ch, par, r);
         st_relaxed_s64(&e->count, A.count, sys);
         st_relaxed_s64(&e->n, rc.n_local, sys);
@@ -339,24 +343,33 @@ __device__ HsOut handshake(const LaunchArgs& A, const RankCall& rc, const DevTab
         st_relaxed_s64(&e->offset, rc.reg_off, sys);
         st_release(&e->seq, seq, sys);
     }
-    HsOut o{0, 1, 0};
-    for (int q = 0; q < P && !o.err; ++q) {
+    int err = 0, direct = 1;
+    long long sumn = 0;
+    for (int q = lane; q < P; q += 32) {
         HsEntry* e = hs_of(my, tab, ch, par, q);
-        if (!wait_ge(&e->seq, seq, deadline, sys)) { o.err = PR_ERR_PEER_TIMEOUT; break; }
+        if (!wait_ge(&e->seq, seq, deadline, sys)) { err = PR_ERR_PEER_TIMEOUT; break; }
         const long long cnt = ld_relaxed_s64(&e->count, sys);
         const long long n = ld_relaxed_s64(&e->n, sys);
         const long long dr = ld_relaxed_s64(&e->dtype, sys);
         const long long off = ld_relaxed_s64(&e->offset, sys);
         const int dt = (int)(dr & 0xffffffffll), rid = (int)(dr >> 32);
-        if (cnt != A.count || dt != A.dtype) o.err = PR_ERR_LENGTH_MISMATCH;
-        o.sumn += n;
-        if (rid < 0) o.direct = 0;
+        if (cnt != A.count || dt != A.dtype) err = PR_ERR_LENGTH_MISMATCH;
+        sumn += n;
+        if (rid < 0) direct = 0;
         if (ns) ns[q] = n;
         if (bufs) bufs[q] = rid >= 0 ? (uint8_t*)((uintptr_t)tab->reg[rid][q] + (uintptr_t)off) : nullptr;
     }
-    if (!o.err && o.sumn <= 0) o.err = PR_ERR_ZERO_SAMPLES;
-    st->seq = seq;
-    return o;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {                    // warp-shuffle reductions
+        sumn += __shfl_xor_sync(0xffffffffu, sumn, o);
+        err = min(err, __shfl_xor_sync(0xffffffffu, err, o));   // error codes are negative
+    }
+    direct = __all_sync(0xffffffffu, direct);
+    HsOut out{err, direct, sumn};
+    if (!out.err && out.sumn <= 0) out.err = PR_ERR_ZERO_SAMPLES;
+    __syncwarp();
+    if (lane == 0) st->seq = seq;
+    return out;
 }
 
 template <typename T>
@@ -381,23 +394,27 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
     unsigned long long deadline = ~0ull;
 
     // ---- handshake = the barrier; its duration is t_w ---------------------------------
-    if (t0) {
+    if (threadIdx.x < 32) {                           // warp 0 (the producer warp) runs the handshake
         const unsigned long long start = gtimer();
         if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
-        if (ch == 0) tab->stamps[0] = (long long)start;
-        for (int k = 0; k < kStages; ++k) {
-            mbar_init(&sh.full[k], 1);
-            mbar_init(&sh.stored[k], (uint32_t)(nc / 32));
-            mbar_init(&sh.empty[k], 1);                     // the signal warp, after `stored`
+        if (t0) {
+            if (ch == 0) tab->stamps[0] = (long long)start;
+            for (int k = 0; k < kStages; ++k) {
+                mbar_init(&sh.full[k], 1);
+                mbar_init(&sh.stored[k], (uint32_t)(nc / 32));
+                mbar_init(&sh.empty[k], 1);                 // the signal warp, after `stored`
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         __shared__ uint8_t* s_bufs[PR_MAX_RANKS];
         const HsOut hs = handshake(A, rc, tab, st, ch, sys, deadline, nullptr, s_bufs);
-        sh.err = hs.err;
-        sh.direct = hs.direct;
-        sh.sumn = hs.sumn;
-        sh.next_buf = hs.direct ? (void*)s_bufs[next] : nullptr;
-        if (ch == 0) tab->stamps[1] = (long long)gtimer();
+        if (t0) {
+            sh.err = hs.err;
+            sh.direct = hs.direct;
+            sh.sumn = hs.sumn;
+            sh.next_buf = hs.direct ? (void*)s_bufs[next] : nullptr;
+            if (ch == 0) tab->stamps[1] = (long long)gtimer();
+        }
     }
     __syncthreads();
     if (sh.err) {
@@ -683,15 +700,19 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__
     const bool t0 = threadIdx.x == 0;
     const bool sys = tab->sysscope != 0;
     unsigned long long deadline = ~0ull;
-    if (t0) {
+    if (threadIdx.x < 32) {                           // warp 0 runs the handshake
         const unsigned long long start = gtimer();
         if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
-        if (ch == 0) tab->stamps[0] = (long long)start;
+        if (t0 && ch == 0) tab->stamps[0] = (long long)start;
         const HsOut hs = handshake(A, rc, tab, st, ch, sys, deadline, s_n, s_bufs);
-        s_err = hs.err ? hs.err : (hs.direct ? 0 : PR_ERR_INVALID);   // two-shot needs registered buffers
-        s_sumn = hs.sumn;
-        for (int q = 0; q < P; ++q) s_w[q] = hs.sumn > 0 ? (float)((double)s_n[q] / (double)hs.sumn) : 0.0f;
-        if (ch == 0) tab->stamps[1] = (long long)gtimer();
+        __syncwarp();
+        for (int q = (int)threadIdx.x; q < P; q += 32)
+            s_w[q] = hs.sumn > 0 ? (float)((double)s_n[q] / (double)hs.sumn) : 0.0f;
+        if (t0) {
+            s_err = hs.err ? hs.err : (hs.direct ? 0 : PR_ERR_INVALID);   // two-shot needs registered buffers
+            s_sumn = hs.sumn;
+            if (ch == 0) tab->stamps[1] = (long long)gtimer();
+        }
     }
     __syncthreads();
     if (s_err) {
