@@ -42,6 +42,12 @@ SCENARIOS = {
     "c2-5x-lin": ("resnet18", 50_000, (3, 32, 32), 2, [1, 1], 24, 256, [5.0, 1.0], True),
     "c4-lin": ("resnet18", 50_000, (3, 32, 32), 8, [1] * 8, 64, 256, [4, 4, 4, 4, 2, 2, 1, 1], True),
     "c4-replace-lin": ("resnet18", 50_000, (3, 32, 32), 8, [1] * 8, 64, 256, [1, 4, 4, 4, 2, 2, 1, 1], True),
+    # N4: convergence invariance under static ratios (Fig. 6, caption P:291):
+    # minibatch 100, total batch 1000 (C = 10), lr 1e-2, wd 1e-4, ratios 5:5, 6:4, 3:7, 7:3
+    "n4-55": ("resnet18", 50_000, (3, 32, 32), 2, [5, 5], 10, 100, [1.0, 1.0], False),
+    "n4-64": ("resnet18", 50_000, (3, 32, 32), 2, [6, 4], 10, 100, [1.0, 1.0], False),
+    "n4-37": ("resnet18", 50_000, (3, 32, 32), 2, [3, 7], 10, 100, [1.0, 1.0], False),
+    "n4-73": ("resnet18", 50_000, (3, 32, 32), 2, [7, 3], 10, 100, [1.0, 1.0], False),
 }
 
 
