@@ -48,6 +48,14 @@ SCENARIOS = {
     "n4-64": ("resnet18", 50_000, (3, 32, 32), 2, [6, 4], 10, 100, [1.0, 1.0], False),
     "n4-37": ("resnet18", 50_000, (3, 32, 32), 2, [3, 7], 10, 100, [1.0, 1.0], False),
     "n4-73": ("resnet18", 50_000, (3, 32, 32), 2, [7, 3], 10, 100, [1.0, 1.0], False),
+    # N3: time-varying stragglers ("Load and network bandwidth during training will change",
+    # P:98).  Two pairs of ranks swap a 3x slowdown every 150 aggregation steps (1.5 epochs of S = 100).
+    "n3-swap": ("resnet18", 409_600, (3, 32, 32), 4, [1] * 4, 64, 64, [3, 3, 1, 1], True),
+}
+
+# σ schedules of the drift scenarios: [(global step, σ per rank), ...]
+SCHEDULES = {
+    "n3-swap": [(0, [3, 3, 1, 1]), (150, [1, 1, 3, 3]), (300, [3, 3, 1, 1]), (450, [1, 1, 3, 3])],
 }
 
 
@@ -57,10 +65,12 @@ def run_virtual(args):
     Each aggregation step: for every rank r, its own rows (K1 shard, K2 gather) go through the shared
     model's forward/backward with rank r's emulated slowdown (K4), timed alone by CUDA events (t_{r,s},
     the rank's gradient-computing time); its local mean gradient is copied into buffer r; then K3
-    reduces the P buffers (local group) and SGD updates the model once.  At the epoch boundary the
-    controller gets t_s^r = Σ_s t_{r,s} (Algorithm 1 steps 1-3).  Because ranks run serially, the
-    *emulated parallel* epoch time is T = Σ_s max_r t_{r,s} + S·t_c (what P GPUs would take, each rank's
-    compute measured alone on a full B200), compared with the bound S·(B/Σv + t_c).
+    reduces the P buffers (local group) and SGD updates the model once.  At each controller boundary
+    (every epoch — Algorithm 1 — or every k steps with --adapt-every k, N3) the controller gets
+    t_s^r = Σ_s t_{r,s} over the steps since the last boundary.  Because ranks run serially, the
+    *emulated parallel* time is T = Σ_s max_r t_{r,s} + S·t_c (what P GPUs would take, each rank's
+    compute measured alone on a full B200), compared with the bound Σ_s B/Σ_r v_{r,s} + S·t_c, where
+    v_{r,s} = n_r/t_{r,s} is rank r's measured speed at step s (= S·(B/Σv + t_c) when speeds are constant).
     """
     import torch
 
@@ -70,60 +80,83 @@ def run_virtual(args):
     model, N, shape, P, ratios, C, g, sigma, adaptive = SCENARIOS[args.scenario]
     if args.N:
         N = args.N
+    k = args.adapt_every
+    policy = {"never_freeze": True} if (args.never_freeze or args.scenario in SCHEDULES) else None
+    if policy is not None and args.ema < 1.0:
+        policy["ema_alpha"] = args.ema
     cfg = RunConfig(N=N, shape=shape, model=model, ratios=ratios, C=C, g=g, slowdown=sigma,
-                    adaptive=adaptive and not args.static, micro=256 if model == "vgg16" else 1024)
+                    adaptive=adaptive and not args.static, micro=256 if model == "vgg16" else 1024,
+                    adapt_every=k, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario))
     w = Worker(cfg, 0, 1, 0, None)
     comms = pr.comm_init_local(P, 0, pr.comm_config())
     bufs = [torch.zeros(w.L, dtype=torch.float32, device="cuda") for _ in range(P)]
     idx = [torch.empty(N, dtype=torch.int64, device="cuda") for _ in range(P)]
+    totals = {"T": 0.0, "bound": 0.0}
     for e in range(args.epochs):
-        v = w.alloc.view()
-        S, n = v["S"], v["n"]
-        xs, ys = [], []
-        for r in range(P):                                # a2 + a3 for every rank
-            pr.shard_indices(w.alloc, r, e, cfg.seed, idx[r])
-            x = torch.empty((max(1, S * n[r]), w.row_bytes), dtype=w.xdt, device="cuda")
-            y = torch.empty(max(1, S * n[r]), dtype=torch.int64, device="cuda")
-            pr.gather_rows(w.X.data_ptr(), N, w.row_bytes, idx[r], S * n[r], x, w.gop, w.Y, y)
-            xs.append(x)
-            ys.append(y)
-        for r in range(P):                                # graphs + t1(n_r) outside the timed region
-            w.rank = r
-            w.prepare(n[r])
-        ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
-              for _ in range(P)]
-        ar = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
-        losses = []
-        for s in range(S):
-            for r in range(P):
+        S = w.alloc.view()["S"]
+        seg = k if k > 0 else S
+        rows, losses, ws = [], [], []
+        for s0 in range(0, S, seg):
+            v = w.alloc.view()
+            n, ns = v["n"], min(seg, S - s0)
+            ws.append(v["w"])
+            xs, ys = [], []
+            for r in range(P):                            # a2 + a3 for every rank
+                if k > 0:
+                    pr.shard_steps(w.alloc, r, e, cfg.seed, s0, ns, idx[r])
+                else:
+                    pr.shard_indices(w.alloc, r, e, cfg.seed, idx[r])
+                x = torch.empty((max(1, ns * n[r]), w.row_bytes), dtype=w.xdt, device="cuda")
+                y = torch.empty(max(1, ns * n[r]), dtype=torch.int64, device="cuda")
+                pr.gather_rows(w.X.data_ptr(), N, w.row_bytes, idx[r], ns * n[r], x, w.gop, w.Y, y)
+                xs.append(x)
+                ys.append(y)
+            for r in range(P):                            # graphs + t1(n_r) outside the timed region
                 w.rank = r
-                ev[r][s][0].record()
-                if n[r] > 0:
-                    losses.append(w.compute_graphed(xs[r][s * n[r]:], ys[r][s * n[r]:], n[r]))
-                ev[r][s][1].record()
-                bufs[r].copy_(w.flat)
+                w.prepare(n[r])
+            ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ns)]
+                  for _ in range(P)]
+            ar = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ns)]
+            for j in range(ns):
+                for r in range(P):
+                    w.rank = r
+                    ev[r][j][0].record()
+                    if n[r] > 0:
+                        losses.append(w.compute_graphed(xs[r][j * n[r]:], ys[r][j * n[r]:], n[r]))
+                    ev[r][j][1].record()
+                    bufs[r].copy_(w.flat)
+                    w.flat.zero_()
+                ar[j][0].record()
+                pr.weighted_allreduce_local(comms, bufs, n)                              # K3
+                w.flat.copy_(bufs[0])
+                w.opt.step()
                 w.flat.zero_()
-            ar[s][0].record()
-            pr.weighted_allreduce_local(comms, bufs, n)                                  # K3
-            w.flat.copy_(bufs[0])
-            w.opt.step()
-            w.flat.zero_()
-            ar[s][1].record()
-        torch.cuda.synchronize()
-        t = [[ev[r][s][0].elapsed_time(ev[r][s][1]) / 1e3 for s in range(S)] for r in range(P)]
-        ts = [sum(x) for x in t]
-        t_c = sum(a.elapsed_time(b) for a, b in ar) / 1e3 / S
-        T = sum(max(t[r][s] for r in range(P)) for s in range(S)) + S * t_c
-        vel = [S * n[r] / ts[r] for r in range(P)]
-        bound = S * (sum(n) / sum(vel) + t_c)
-        print(json.dumps({"scenario": args.scenario, "mode": "virtual", "epoch": e, "w": v["w"],
-                          "frozen": v["frozen"], "t_s": ts, "t_w": [S * 0 + sum(max(t[q][s] for q in range(P)) - t[r][s]
-                                                                          for s in range(S)) for r in range(P)],
-                          "T_emulated": T, "bound": bound, "T_over_bound": T / bound, "t_c": t_c,
-                          "loss": float(torch.stack(losses).mean()) if losses else None}), flush=True)
+                ar[j][1].record()
+                w.gstep += 1
+            torch.cuda.synchronize()
+            t = [[ev[r][j][0].elapsed_time(ev[r][j][1]) / 1e3 for j in range(ns)] for r in range(P)]
+            t_c = [a.elapsed_time(b) / 1e3 for a, b in ar]
+            rows.append((n, t, t_c))
+            if cfg.adaptive:
+                w.alloc.update([sum(x) for x in t])       # a10: Eq. 10 + rounding + stop rule
+        # emulated parallel time and the speed-balanced bound over the epoch's steps
+        T = sum(sum(max(t[r][j] for r in range(P)) + tc[j] for j in range(len(tc))) for _, t, tc in rows)
+        bound = sum(sum(sum(n) / sum(n[r] / t[r][j] for r in range(P) if n[r] > 0) + tc[j] for j in range(len(tc)))
+                    for n, t, tc in rows)
+        ts = [sum(sum(t[r]) for _, t, _ in rows) for r in range(P)]
+        totals["T"] += T
+        totals["bound"] += bound
+        rec = {"scenario": args.scenario, "mode": "virtual", "adapt_every": k, "epoch": e, "w": ws[0],
+               "w_end": w.alloc.view()["w"], "frozen": w.alloc.view()["frozen"], "t_s": ts,
+               "T_emulated": T, "bound": bound, "T_over_bound": T / bound,
+               "t_c": sum(sum(tc) for _, _, tc in rows) / S, "loss": float(torch.stack(losses).mean()) if losses else None}
+        if k > 0:
+            rec["w_segments"] = ws
+        print(json.dumps(rec), flush=True)
         w.epoch += 1
-        if cfg.adaptive:
-            w.alloc.update(ts)                            # a10: Eq. 10 + rounding + stop rule
+    print(json.dumps({"scenario": args.scenario, "mode": "virtual", "adapt_every": k, "static": args.static,
+                      "epochs": args.epochs, "T_total": totals["T"], "bound_total": totals["bound"],
+                      "T_over_bound": totals["T"] / totals["bound"]}), flush=True)
     for c in comms:
         c.destroy()
 
@@ -135,6 +168,10 @@ def main():
     ap.add_argument("--N", type=int, default=0, help="override the data set size (shorter epochs)")
     ap.add_argument("--static", action="store_true", help="disable the self-adaptive controller")
     ap.add_argument("--virtual", action="store_true", help="all ranks on one GPU, serially (see run_virtual)")
+    ap.add_argument("--adapt-every", type=int, default=0,
+                    help="N3: controller every k aggregation steps over the step-interleaved shard (0 = per epoch)")
+    ap.add_argument("--never-freeze", action="store_true", help="keep adapting after the ratio is stable")
+    ap.add_argument("--ema", type=float, default=1.0, help="EMA weight on t_s (1 = raw, S:166)")
     args = ap.parse_args()
     if args.virtual:
         return run_virtual(args)
@@ -159,8 +196,12 @@ def main():
     dist.init_process_group("gloo" if shared else "nccl", **({} if shared else {"device_id": torch.device("cuda", local)}))
     tdev = "cpu" if shared else "cuda"
     comm = pr.comm_init(rank, world, local)
+    policy = {"never_freeze": True} if (args.never_freeze or args.scenario in SCHEDULES) else None
+    if policy is not None and args.ema < 1.0:
+        policy["ema_alpha"] = args.ema
     cfg = RunConfig(N=N, shape=shape, model=model, ratios=ratios, C=C, g=g, slowdown=sigma,
-                    adaptive=adaptive and not args.static, micro=256 if model == "vgg16" else 1024)
+                    adaptive=adaptive and not args.static, micro=256 if model == "vgg16" else 1024,
+                    adapt_every=args.adapt_every, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario))
     wk = Worker(cfg, rank, world, local, comm)
     wk.calibrate()
     c0 = torch.tensor([wk.c0_ns], dtype=torch.float64, device=tdev)

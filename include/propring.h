@@ -121,6 +121,16 @@ void pr_alloc_destroy(pr_alloc *a);
  *   Errors: PR_ERR_INVALID (rank out of range), PR_ERR_CAPACITY, PR_ERR_CUDA. */
 int pr_shard_indices(const pr_alloc *a, int32_t rank, int64_t epoch, uint64_t seed, int64_t *d_out,
                      int64_t cap, void *stream);
+/* Step-interleaved shard for intra-epoch re-allocation ("Load ... will change
+ * slightly" P:98; DESIGN §3 #43).  Aggregation step s of the epoch owns permuted positions
+ * [s·B, (s+1)·B), B = g·C; rank r takes the n_r = g·w_r positions starting at o_r = g·Σ_{j<r} w_j:
+ *   d_out[(s − step0)·n_r + t] = π_{seed,epoch}(s·B + o_r + t),  step0 <= s < step0 + nsteps, t < n_r.
+ * Because B is fixed (Σw = C, Eq. 4), the step's sample set does not depend on w, so the allocation may
+ * change between any two steps and the ranks' rows stay disjoint.  Requires step0 + nsteps <= S.
+ * d_out: caller-owned device int64[cap], cap >= nsteps·n_r.  Async on stream.
+ * Errors: PR_ERR_INVALID (rank or step range), PR_ERR_CAPACITY, PR_ERR_CUDA. */
+int pr_shard_steps(const pr_alloc *a, int32_t rank, int64_t epoch, uint64_t seed, int64_t step0,
+                   int64_t nsteps, int64_t *d_out, int64_t cap, void *stream);
 /* The permutation itself on positions [begin, begin+count): d_out[t] = π_{seed,epoch}(begin + t).
  * Requires 1 <= N <= 2^62 and begin + count <= N. */
 int pr_permute(int64_t N, uint64_t seed, int64_t epoch, int64_t begin, int64_t count, int64_t *d_out,

@@ -99,3 +99,11 @@ def permute(j, N: int, seed: int, epoch: int):
 def shard_indices(N: int, off: int, length: int, seed: int, epoch: int):
     """O4: idx[t] = π(off + t) for t < length."""
     return permute(np.arange(off, off + length, dtype=np.uint64), N, seed, epoch)
+
+
+def shard_steps(N: int, B: int, o: int, n: int, seed: int, epoch: int, step0: int, nsteps: int):
+    """Step-interleaved shard (DESIGN.md §3 #43): aggregation step s owns the permuted
+    positions [s·B, (s+1)·B) and the rank takes the n of them starting at o = g·Σ_{j<r} w_j:
+    idx[(s − step0)·n + t] = π(s·B + o + t) for step0 <= s < step0 + nsteps, t < n."""
+    pos = [s * B + o + t for s in range(step0, step0 + nsteps) for t in range(n)]
+    return permute(np.array(pos, dtype=np.uint64), N, seed, epoch)

@@ -8,6 +8,7 @@ device work runs in the library's kernels.  PyTorch supplies device memory, stre
     alloc_init(N, ratios, C, g, floor)      -> Alloc           static allocation
     Alloc.update(step_times)                -> changed          self-adaptive Eq. 10
     shard_indices(alloc, rank, epoch, seed, out)               per-epoch shard
+    shard_steps(alloc, rank, epoch, seed, step0, nsteps, out)  step-interleaved shard (N3)
     gather_rows(src, idx, out, op, ...)                        step-batch gather
     comm_init(rank, P, device, group) / comm_init_local(P)     NVLink peer-memory communicator
     weighted_allreduce(comm, buf, n_local)                     Σ_r (n_r/Σn)·buf_r     (Eq. 1)
@@ -159,6 +160,14 @@ def shard_indices(alloc: Alloc, rank: int, epoch: int, seed: int, out, stream=No
     """out[t] = π_{seed,epoch}(off_rank + t), t < len_rank (K1).  out: int64 CUDA tensor."""
     _check(LIB.pr_shard_indices(alloc.handle, rank, epoch, seed & (2 ** 64 - 1), _ptr(out), out.numel(),
                                 _stream(stream)), "pr_shard_indices")
+    return out
+
+
+def shard_steps(alloc: Alloc, rank: int, epoch: int, seed: int, step0: int, nsteps: int, out, stream=None):
+    """Step-interleaved shard (N3): out[(s-step0)·n_r + t] = π(s·B + o_rank + t) for steps
+    [step0, step0+nsteps) — the allocation may change between any two steps.  out: int64 CUDA tensor."""
+    _check(LIB.pr_shard_steps(alloc.handle, rank, epoch, seed & (2 ** 64 - 1), step0, nsteps, _ptr(out),
+                              out.numel(), _stream(stream)), "pr_shard_steps")
     return out
 
 

@@ -57,6 +57,7 @@ SIGNATURES = {
     "pr_alloc_load": (ctypes.c_int, [ctypes.POINTER(c_vp), c_vp, c_sz]),
     "pr_alloc_destroy": (None, [c_vp]),
     "pr_shard_indices": (ctypes.c_int, [c_vp, c_i32, c_i64, c_u64, c_vp, c_i64, c_vp]),
+    "pr_shard_steps": (ctypes.c_int, [c_vp, c_i32, c_i64, c_u64, c_i64, c_i64, c_vp, c_i64, c_vp]),
     "pr_permute": (ctypes.c_int, [c_i64, c_u64, c_i64, c_i64, c_i64, c_vp, c_vp]),
     "pr_gather_rows": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, ctypes.POINTER(GatherOp), c_vp, c_vp, c_vp]),
     "pr_spin": (ctypes.c_int, [c_i64, c_vp]),
@@ -79,7 +80,7 @@ SIGNATURES = {
 
 def load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2111_08272_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: run `python paper_2111_08272_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():

@@ -1,6 +1,6 @@
 """Build libpropring.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-    python -m paper_2111_08272_b200.build [--force] [--ptxas-v]
+    python paper_2111_08272_b200/build.py [--force] [--ptxas-v]
 
 Host C++ (the control plane) is compiled with -ffp-contract=off so the fp64 controller arithmetic is
 the fixed operation order DESIGN.md §3 #35 specifies.  CUDA sources: -gencode arch=compute_100a,

@@ -301,3 +301,13 @@ int pr_internal_shard_range(const pr_alloc* a, int32_t rank, int64_t* N, int64_t
     *N = a->N; *off = o[rank]; *len = l[rank];
     return PR_OK;
 }
+
+int pr_internal_step_layout(const pr_alloc* a, int32_t rank, int64_t* N, int64_t* B, int64_t* S, int64_t* o,
+                            int64_t* n) {
+    if (!a || rank < 0 || rank >= a->P) return PR_ERR_INVALID;
+    int64_t units = 0;
+    for (int32_t i = 0; i < rank; ++i) units += a->w[i];
+    *N = a->N; *B = a->g * a->C; *S = a->N / (a->g * a->C);
+    *o = a->g * units; *n = a->g * a->w[rank];
+    return PR_OK;
+}

@@ -137,23 +137,30 @@ __device__ __forceinline__ void convert_store(const GatherParams& p, uint8_t* dr
     }
 }
 
-// Channels-last: 8 consecutive pixels of all C channels (8 bytes per plane in smem, plane stride ps) ->
-// 8·C interleaved outputs at pixel pix0 of the HWC output row: C (bf16) or 2C (f32) 16-byte stores.
-template <int OP, int C>
+// Channels-last: PX (8 or 16) consecutive pixels of all C channels (PX bytes per plane, plane stride ps,
+// in smem or global) -> PX·C interleaved outputs at pixel pix0 of the HWC output row, written as
+// PX·C·es/16 16-byte stores (es = 2 for bf16, 4 for f32).
+template <int OP, int C, int PX>
 __device__ __forceinline__ void hwc_store(const GatherParams& p, uint8_t* drow, int64_t pix0, const uint8_t* s,
                                           int64_t ps) {
-    float f[C][8];
+    float f[C][PX];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
-        const uint2 w = *reinterpret_cast<const uint2*>(s + c * ps);
-        const uint32_t ww[2] = {w.x, w.y};
-        affine_words<2>(ww, p.scale[c], p.shift[c], f[c]);
+        uint32_t ww[PX / 4];
+        if (PX == 16) {
+            const uint4 w = *reinterpret_cast<const uint4*>(s + c * ps);
+            ww[0] = w.x; ww[1] = w.y; ww[2 % (PX / 4)] = w.z; ww[3 % (PX / 4)] = w.w;
+        } else {
+            const uint2 w = *reinterpret_cast<const uint2*>(s + c * ps);
+            ww[0] = w.x; ww[1 % (PX / 4)] = w.y;
+        }
+        affine_words<PX / 4>(ww, p.scale[c], p.shift[c], f[c]);
     }
     // interleaved value k = pixel (k / C), channel (k % C)
     if (OP == PR_GATHER_U8_TO_BF16_AFFINE) {
         uint8_t* d = drow + pix0 * C * 2;
 #pragma unroll
-        for (int q = 0; q < C; ++q) {
+        for (int q = 0; q < C * PX / 8; ++q) {
             uint32_t o[4];
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
@@ -165,7 +172,7 @@ __device__ __forceinline__ void hwc_store(const GatherParams& p, uint8_t* drow, 
     } else {
         uint8_t* d = drow + pix0 * C * 4;
 #pragma unroll
-        for (int q = 0; q < 2 * C; ++q) {
+        for (int q = 0; q < C * PX / 4; ++q) {
             uint32_t o[4];
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
@@ -177,14 +184,14 @@ __device__ __forceinline__ void hwc_store(const GatherParams& p, uint8_t* drow, 
     }
 }
 
-template <int OP>
+template <int OP, int PX = 8>
 __device__ __forceinline__ void hwc_dispatch(const GatherParams& p, uint8_t* drow, int64_t pix0, const uint8_t* s,
                                              int64_t ps) {
     switch (p.channels) {
-        case 1: hwc_store<OP, 1>(p, drow, pix0, s, ps); break;
-        case 2: hwc_store<OP, 2>(p, drow, pix0, s, ps); break;
-        case 3: hwc_store<OP, 3>(p, drow, pix0, s, ps); break;
-        default: hwc_store<OP, 4>(p, drow, pix0, s, ps); break;
+        case 1: hwc_store<OP, 1, PX>(p, drow, pix0, s, ps); break;
+        case 2: hwc_store<OP, 2, PX>(p, drow, pix0, s, ps); break;
+        case 3: hwc_store<OP, 3, PX>(p, drow, pix0, s, ps); break;
+        default: hwc_store<OP, 4, PX>(p, drow, pix0, s, ps); break;
     }
 }
 
@@ -204,13 +211,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) gather_kernel(const __grid_
             p.lab_dst[t] = p.lab_src[p.idx[t]];
     }
     if (OP != PR_GATHER_COPY && p.hwc) {
-        // channels-last: a lane takes 8 pixels of every plane (C 8-byte loads, coalesced per plane)
+        // channels-last: a lane takes 8 pixels of every plane (C 8-byte loads, coalesced per plane).
+        // 16-pixel items (PX=16: 16-byte loads) measured slower (99 vs 81 us on the epoch gather):
+        // 96-byte lane strides spread each warp store over twice the sectors.
         const int64_t groups = p.plane / 8, gsegs = (groups + 31) / 32;
         for (int64_t it = warp; it < p.n * gsegs; it += nwarps) {
             const int64_t row = it / gsegs, gi = (it - row * gsegs) * 32 + lane;
             if (gi < groups)
-                hwc_dispatch<OP>(p, p.dst + row * p.row_bytes * out_mul, gi * 8,
-                                 p.src + __ldg(p.idx + row) * p.row_bytes + gi * 8, p.plane);
+                hwc_dispatch<OP, 8>(p, p.dst + row * p.row_bytes * out_mul, gi * 8,
+                                    p.src + __ldg(p.idx + row) * p.row_bytes + gi * 8, p.plane);
         }
         return;
     }

@@ -62,6 +62,19 @@ __global__ void __launch_bounds__(256) permute_kernel(uint64_t N, FeistelKey fk,
     }
 }
 
+// Step-interleaved shard (N3): out[i] = π(s·B + o + t) with s = step0 + i / n, t = i mod n.
+__global__ void __launch_bounds__(256) shard_steps_kernel(uint64_t N, FeistelKey fk, uint64_t B, uint64_t o,
+                                                          uint64_t n, uint64_t step0, uint64_t count,
+                                                          int64_t* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        const uint64_t s = step0 + i / n, t = i - (i / n) * n;
+        uint64_t y = feistel(s * B + o + t, fk);
+        while (y >= N) y = feistel(y, fk);
+        out[i] = (int64_t)y;
+    }
+}
+
 __global__ void philox_test_kernel(const uint32_t* __restrict__ ctr, int64_t n, uint32_t k0, uint32_t k1,
                                    int use_curand, uint32_t* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -114,6 +127,25 @@ extern "C" int pr_shard_indices(const pr_alloc* a, int32_t rank, int64_t epoch, 
     if (rc) return rc;
     if (cap < len) return PR_ERR_CAPACITY;
     return pr_permute(N, seed, epoch, off, len, d_out, stream);
+}
+
+extern "C" int pr_shard_steps(const pr_alloc* a, int32_t rank, int64_t epoch, uint64_t seed, int64_t step0,
+                              int64_t nsteps, int64_t* d_out, int64_t cap, void* stream) {
+    int64_t N, B, S, o, n;
+    int rc = pr_internal_step_layout(a, rank, &N, &B, &S, &o, &n);
+    if (rc) return rc;
+    if (step0 < 0 || nsteps < 0 || step0 + nsteps > S) return PR_ERR_INVALID;
+    const int64_t count = nsteps * n;
+    if (cap < count) return PR_ERR_CAPACITY;
+    if (count == 0) return PR_OK;
+    if (!d_out) return PR_ERR_INVALID;
+    const FeistelKey fk = make_key(N, seed, epoch);
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    shard_steps_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        (uint64_t)N, fk, (uint64_t)B, (uint64_t)o, (uint64_t)n, (uint64_t)step0, (uint64_t)count, d_out);
+    PR_CUDA_TRY(cudaGetLastError());
+    return PR_OK;
 }
 
 extern "C" int pr_test_philox(const uint32_t* d_ctr, int64_t n, uint64_t key, int32_t use_curand, uint32_t* d_out,

@@ -57,6 +57,13 @@ class RunConfig:
     gather: str = "epoch"                   # "epoch": one K2 launch per epoch; "step": one per step
     channels_last: bool = True              # K2 writes HWC rows; the model runs channels-last (no transposes)
     graphs: bool = True                     # capture each step's forward/backward (+ spin) in a CUDA graph
+    # N3: intra-epoch controller.  adapt_every = k > 0 runs the epoch as segments of k
+    # aggregation steps over the step-interleaved shard (pr_shard_steps) and calls the controller at every
+    # segment boundary with that segment's t_s; 0 = once per epoch (Algorithm 1 as written).
+    adapt_every: int = 0
+    policy: dict | None = None              # Alloc.set_policy kwargs (e.g. never_freeze, ema_alpha)
+    # time-varying stragglers: [(global_step, [σ_r ...]), ...]; σ at step s = the last entry with step <= s
+    slowdown_schedule: list | None = None
 
 
 def build_model(name: str, num_classes: int):
@@ -80,6 +87,9 @@ class Worker:
         self.comm = comm
         self.stream = torch.cuda.current_stream(self.dev)
         self.alloc = pr.alloc_init(cfg.N, cfg.ratios, C=cfg.C, g=cfg.g, floor=cfg.floor)
+        if cfg.policy:
+            self.alloc.set_policy(**cfg.policy)
+        self.gstep = 0                                # global aggregation-step counter (slowdown schedule)
         self.row_bytes = int(torch.tensor(cfg.shape).prod())
         if data is None:                              # synthetic data set, replicated per rank
             import synth
@@ -101,7 +111,8 @@ class Worker:
         self.model = build_model(cfg.model, cfg.num_classes).to(self.dev)
         if cfg.channels_last:
             self.model = self.model.to(memory_format=torch.channels_last)
-        self._graphs = {}                             # (n_r, spin_ns) -> captured step
+        self._graphs = {}                             # n_r -> captured step
+        self._pool = None
         params = list(self.model.parameters())
         self.L = sum(p.numel() for p in params)
         if comm is not None:
@@ -163,8 +174,21 @@ class Worker:
             self.launches += 1
         return torch.stack(losses).sum() / n_r
 
+    def sigma(self, rank: int | None = None) -> float:
+        """Emulated slowdown σ of `rank` at the current global step (K4 target)."""
+        rank = self.rank if rank is None else rank
+        sched = self.cfg.slowdown_schedule
+        if sched:
+            cur = None
+            for step, sig in sched:
+                if step <= self.gstep:
+                    cur = sig
+            if cur is not None:
+                return float(cur[rank])
+        return float(self.cfg.slowdown[rank]) if self.cfg.slowdown else 1.0
+
     def _spin_ns(self, n_r: int) -> int:
-        sigma = self.cfg.slowdown[self.rank] if self.cfg.slowdown else 1.0
+        sigma = self.sigma() if self.cfg.slowdown or self.cfg.slowdown_schedule else 1.0
         return int((sigma - 1.0) * self.c0_ns * n_r) if sigma > 1.0 and self.c0_ns > 0 else 0
 
     def prepare(self, n_r: int, calib_reps: int = 3):
@@ -178,16 +202,20 @@ class Worker:
         ys = torch.randint(0, self.cfg.classes, (n_r,), device=self.dev)
         side = torch.cuda.Stream(self.dev)
         side.wait_stream(self.stream)
-        launches, save = self.launches, self.cfg.slowdown
-        self.cfg.slowdown = None                              # the spin is launched after the replay
+        launches, save, save_sched = self.launches, self.cfg.slowdown, self.cfg.slowdown_schedule
+        self.cfg.slowdown = self.cfg.slowdown_schedule = None  # the spin is launched after the replay
         with torch.cuda.stream(side):
             self.compute(xs, ys, n_r)                         # warm-up (cuDNN autotune, allocator)
         self.stream.wait_stream(side)
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=side):
+        if self._pool is None:
+            self._pool = torch.cuda.graph_pool_handle()
+        # one memory pool for every n_r's graph: the graphs replay one at a time on one stream and keep no
+        # temporaries live between replays, so a re-allocation that visits many n_r costs no extra memory
+        with torch.cuda.graph(g, pool=self._pool, stream=side):
             loss = self.compute(xs, ys, n_r)
         self.stream.wait_stream(side)
-        self.cfg.slowdown, self.launches = save, launches
+        self.cfg.slowdown, self.cfg.slowdown_schedule, self.launches = save, save_sched, launches
         g.replay()                                            # warm replay, then t1(n_r)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(self.stream)
@@ -206,7 +234,7 @@ class Worker:
         xs.copy_(x[:n_r])
         ys.copy_(y[:n_r])
         g.replay()
-        sigma = self.cfg.slowdown[self.rank] if self.cfg.slowdown else 1.0
+        sigma = self.sigma()
         if sigma > 1.0:
             pr.spin(int((sigma - 1.0) * t1_ns), stream=self.stream)
             self.launches += 1
@@ -241,6 +269,8 @@ class Worker:
 
     def run_epoch(self, record=False, loss_to_host=False):
         cfg = self.cfg
+        if cfg.adapt_every > 0:
+            return self.run_epoch_segments(record, loss_to_host)
         v = self.alloc.view()
         n_r, S = v["n"][self.rank], v["S"]
         if cfg.graphs:
@@ -264,6 +294,7 @@ class Worker:
                 loss = torch.zeros((), device=self.dev)
             ev[s][1].record(self.stream)
             self.allreduce_and_update(n_r, record)
+            self.gstep += 1
             losses.append(loss)
             if loss_to_host:
                 host_losses.append(float(loss))          # D2H of the step's result (e2e contract)
@@ -279,10 +310,65 @@ class Worker:
         self.last_ts = t_s
         return rec
 
+    def run_epoch_segments(self, record=False, loss_to_host=False):
+        """N3: the epoch as segments of k = adapt_every aggregation steps over the step-interleaved shard.
+        Per segment: K1 (pr_shard_steps) + K2 for k·n_r rows, k steps of a4 + a6-a9, then the segment's
+        t_s (a5) is exchanged (K6) and the controller (a10) may change w before the next segment.  Step s
+        always trains on the same B permuted positions whatever w is (DESIGN §3 #43)."""
+        cfg = self.cfg
+        S = self.alloc.view()["S"]
+        k = cfg.adapt_every
+        losses, host_losses, segs = [], [], []
+        t_epoch, s0 = 0.0, 0
+        while s0 < S:
+            v = self.alloc.view()
+            n_r, ns = v["n"][self.rank], min(k, S - s0)
+            if cfg.graphs:
+                self.prepare(n_r)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+            pr.shard_steps(self.alloc, self.rank, self.epoch, cfg.seed, s0, ns, self.idx, stream=self.stream)
+            self.launches += 1
+            xe, ye = self.gather(0, ns * n_r, record)
+            e1.record(self.stream)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ns)]
+            for j in range(ns):
+                ev[j][0].record(self.stream)
+                if n_r > 0:
+                    x, y = xe[j * n_r:(j + 1) * n_r], ye[j * n_r:(j + 1) * n_r]
+                    loss = self.compute_graphed(x, y, n_r) if cfg.graphs else self.compute(x, y, n_r)
+                else:
+                    loss = torch.zeros((), device=self.dev)
+                ev[j][1].record(self.stream)
+                self.allreduce_and_update(n_r, record)
+                self.gstep += 1
+                losses.append(loss)
+                if loss_to_host:
+                    host_losses.append(float(loss))
+            ev[-1][1].synchronize()
+            t_seg = (e0.elapsed_time(e1) + sum(a.elapsed_time(b) for a, b in ev)) / 1e3
+            t_epoch += t_seg
+            changed = False
+            if self.comm is not None:
+                ts = self.comm.allgather_f64(t_seg, stream=self.stream)
+                self.launches += 1
+            else:
+                ts = [t_seg]
+            if cfg.adaptive:
+                changed = self.alloc.update(ts)
+            segs.append({"s0": s0, "steps": ns, "w": v["w"], "t_s": ts, "changed": changed})
+            s0 += ns
+        self.epoch += 1
+        self.last_ts = t_epoch
+        rec = {"t_s": t_epoch, "loss": float(torch.stack(losses).mean()), "S": S,
+               "n_r": self.alloc.view()["n"][self.rank], "w": segs[0]["w"], "segments": segs}
+        self.history.append(rec)
+        return rec
+
     def boundary(self):
         """Algorithm 1 steps 1-3: exchange t_s (K6), Eq. 10 + rounding, redistribute."""
-        if self.epoch == 0:
-            return False                              # "t_s ... is set to 0" (P:133): nothing to adapt yet
+        if self.epoch == 0 or self.cfg.adapt_every > 0:
+            return False                              # "t_s ... is set to 0" / N3 adapts per segment
         if self.comm is not None:
             ts = self.comm.allgather_f64(self.last_ts, stream=self.stream)
             self.launches += 1
@@ -298,7 +384,8 @@ class Worker:
         n_r = v["n"][self.rank]
         pr.shard_indices(self.alloc, self.rank, 0, self.cfg.seed, self.idx, stream=self.stream)
         x, y = self.gather(0, n_r)
-        save, self.cfg.slowdown = self.cfg.slowdown, None
+        save, save_sched = self.cfg.slowdown, self.cfg.slowdown_schedule
+        self.cfg.slowdown = self.cfg.slowdown_schedule = None
         for _ in range(2):
             self.compute(x, y, n_r)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -308,6 +395,6 @@ class Worker:
         b.record(self.stream)
         b.synchronize()
         self.flat.zero_()
-        self.cfg.slowdown = save
+        self.cfg.slowdown, self.cfg.slowdown_schedule = save, save_sched
         self.c0_ns = a.elapsed_time(b) * 1e6 / (steps * n_r)
         return self.c0_ns

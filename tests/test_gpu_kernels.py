@@ -107,6 +107,34 @@ def test_shard_indices_bit_exact(N, ratios, C, g):
     assert e.value.code == pr.PR_ERR_CAPACITY
 
 
+@pytest.mark.parametrize("N,ratios,C,g", [(1000, [1, 3], 4, 25), (50000, [1, 1, 1, 1, 2, 2, 4, 4], 64, 16),
+                                          (1281167, [3, 1, 4, 1, 5], 14, 2)])
+def test_shard_steps_bit_exact(N, ratios, C, g):
+    a = pr.alloc_init(N, ratios, C=C, g=g)
+    v = a.view()
+    B, S = g * sum(v["w"]), v["S"]
+    for step0, nsteps in ((0, 1), (1, 3), (S - 2, 2), (0, S)):
+        if nsteps * B > 4_000_000:
+            continue
+        seen = []
+        for r in range(len(ratios)):
+            n_r, o_r = v["n"][r], g * sum(v["w"][:r])
+            out = torch.empty(nsteps * n_r + 3, dtype=torch.int64, device="cuda")
+            pr.shard_steps(a, r, 5, 77, step0, nsteps, out)
+            got = out[:nsteps * n_r].cpu().numpy()
+            assert np.array_equal(got, PM.shard_steps(N, B, o_r, n_r, 77, 5, step0, nsteps))
+            seen.append(got)
+        assert np.unique(np.concatenate(seen)).size == nsteps * B
+    out = torch.empty(v["n"][0], dtype=torch.int64, device="cuda")
+    for bad in ((S, 1), (-1, 1), (S - 1, 2)):
+        with pytest.raises(pr.PropringError) as e:
+            pr.shard_steps(a, 0, 0, 1, bad[0], bad[1], out)
+        assert e.value.code == pr.PR_ERR_INVALID
+    with pytest.raises(pr.PropringError) as e:
+        pr.shard_steps(a, 0, 0, 1, 0, 2, out)
+    assert e.value.code == pr.PR_ERR_CAPACITY
+
+
 # ---------------------------------------------------------------- K2 ----------------------------
 
 MEAN = [123.675, 116.28, 103.53]

@@ -59,3 +59,25 @@ def test_boundary_runs_controller():
     w.boundary()                              # P = 1: Eq. 10 keeps w = [C]
     v = w.alloc.view()
     assert v["w"] == [64] and v["epoch"] == 1
+
+
+def test_segmented_epoch_matches_contiguous_at_one_rank():
+    # N3 at P = 1: the step-interleaved shard of step s is positions [s·B, (s+1)·B) = the contiguous
+    # shard's step s, so the segmented epoch trains on the same batches (same losses up to bf16 noise)
+    a = _worker(adapt_every=3, policy={"never_freeze": True})
+    b = _worker()
+    ra, rb = a.run_epoch(), b.run_epoch()
+    S = rb["S"]
+    assert [sg["steps"] for sg in ra["segments"]] == [3] * (S // 3) + ([S % 3] if S % 3 else [])
+    assert abs(ra["loss"] - rb["loss"]) <= 2e-2 * abs(rb["loss"])
+    assert a.alloc.view()["hist_len"] == 1 + len(ra["segments"])   # one controller call per segment
+    assert a.gstep == S and a.boundary() is False
+
+
+def test_slowdown_schedule_lookup():
+    w = _worker(slowdown=[2.0], slowdown_schedule=[(5, [3.0]), (9, [1.5])])
+    seen = []
+    for s in (0, 4, 5, 8, 9, 100):
+        w.gstep = s
+        seen.append(w.sigma())
+    assert seen == [2.0, 2.0, 3.0, 3.0, 1.5, 1.5]

@@ -80,3 +80,35 @@ def test_shards_disjoint_and_cover():
         allv = np.concatenate(shards)
         assert allv.size == N and np.array_equal(np.sort(allv), np.arange(N))
         assert all(s.size == a.len[r] for r, s in enumerate(shards))
+
+
+def test_shard_steps_reduces_to_contiguous_shard_at_one_rank():
+    # P = 1 (w = [C]): step s takes positions [s·B, (s+1)·B), so S steps are the first S·B of the shard
+    N, C, g = 5000, 4, 25
+    a = A.alloc_init(N, [1], C=C, g=g)
+    B, S = g * C, N // (g * C)
+    got = PM.shard_steps(N, B, 0, B, 3, 1, 0, S)
+    assert np.array_equal(got, PM.shard_indices(N, 0, a.len[0], 3, 1)[:S * B])
+
+
+def test_shard_steps_disjoint_under_reallocation():
+    # the allocation changes every 3 steps; each step's rows over ranks are exactly π([s·B, (s+1)·B))
+    N, C, g = 6000, 8, 10
+    B, S = g * C, N // (g * C)
+    plans = [[1, 1, 2, 4], [4, 2, 1, 1], [2, 2, 2, 2], [1, 1, 1, 5]]
+    seen = []
+    for s in range(S):
+        w = plans[(s // 3) % len(plans)]
+        o = np.concatenate([[0], np.cumsum(w)[:-1]]) * g
+        step = [PM.shard_steps(N, B, int(o[r]), g * w[r], 5, 2, s, 1) for r in range(4)]
+        assert sorted(np.concatenate(step).tolist()) == sorted(PM.shard_indices(N, s * B, B, 5, 2).tolist())
+        seen.extend(np.concatenate(step).tolist())
+    assert len(set(seen)) == S * B
+
+
+def test_shard_steps_segments_compose():
+    N, B, o, n = 10007, 96, 32, 40
+    whole = PM.shard_steps(N, B, o, n, 11, 4, 7, 20)
+    parts = np.concatenate([PM.shard_steps(N, B, o, n, 11, 4, 7, 5), PM.shard_steps(N, B, o, n, 11, 4, 12, 15)])
+    assert np.array_equal(whole, parts)
+    assert np.array_equal(whole[:n], PM.shard_indices(N, 7 * B + o, n, 11, 4))
