@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-epochs", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--overlap", action="store_true",
+                    help="N1: bucketed weighted allreduce overlapped with backward (N > 1)")
+    ap.add_argument("--bucket-mb", type=float, default=8.0)
     ap.add_argument("--no-colocated", action="store_true")
     ap.add_argument("--data-n", type=int, default=N_DATA,
                     help="data-set rows (default 50,000; smaller only for profiling runs: S = N // 1024)")
@@ -143,7 +146,8 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = pr.comm_init(rank, world, local) if world > 1 else None
-    cfg = RunConfig(N=args.data_n, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024)
+    cfg = RunConfig(N=args.data_n, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024,
+                    overlap=args.overlap, bucket_mb=args.bucket_mb)
     wk = Worker(cfg, rank, world, local, comm)
 
     def barrier():
@@ -218,7 +222,7 @@ def run_ours(args):
     e2e = None
     if args.e2e_epochs > 0:
         cfg_h = RunConfig(N=args.data_n, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024,
-                          host_data=True)
+                          host_data=True, overlap=args.overlap, bucket_mb=args.bucket_mb)
         wk_h = Worker(cfg_h, rank, world, local, comm, data=wk.X.cpu(), labels=wk.Y.cpu())
         wk_h.model.load_state_dict(wk.model.state_dict())
         epoch(w=wk_h)                                      # warm-up
@@ -260,6 +264,7 @@ def run_ours(args):
                                    "self-adaptive allocation, fp32 gradients (11,689,512), bf16 autocast compute",
                        "model": "resnet18 (1000-class head, random init)", "global_batch": 1024,
                        "seq_len": None, "parallelism": f"dp{world}", "step": "one epoch (S=48 aggregations)",
+                       "overlap": bool(args.overlap and world > 1),
                        "l2": "inputs larger than L2 (153.6 MB data set streamed every epoch)"},
             "epoch_time_s": ms_epoch / 1e3,
             "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},

@@ -172,6 +172,14 @@ int pr_gather_rows(const void *d_src, int64_t n_src, int64_t row_bytes, const in
  * nanoseconds on `stream` (the per-rank calibrated slowdown of the north star). ns <= 0: no launch. */
 int pr_spin(int64_t ns, void *stream);
 
+/* t_s capture (row a5) where CUDA events cannot bracket the compute — inside a captured
+ * graph whose tail also joins an overlapped allreduce (N1): a 1-thread kernel appends the %globaltimer
+ * value (ns) to a caller-owned device ring, stream-ordered:
+ *   i = d_ring[0]++ (atomic);  d_ring[1 + i mod cap] = now.
+ * The caller zeroes d_ring[0] and reads the ring after the stream completes.  cap >= 1.
+ * Errors: PR_ERR_INVALID, PR_ERR_CUDA. */
+int pr_stamp(int64_t *d_ring, int64_t cap, void *stream);
+
 /* =================================================================================================
  * 3. Weighted ring allreduce (K3) — §8(a) rows a6, a7, a8
  * ================================================================================================= */

@@ -215,6 +215,12 @@ def spin(ns: int, stream=None):
     _check(LIB.pr_spin(int(ns), _stream(stream)), "pr_spin")
 
 
+def stamp(ring, stream=None):
+    """Append the device %globaltimer (ns) to ring[1 + (ring[0]++ mod cap)] (a5 t_s stamps inside graphs).
+    ring: int64 CUDA tensor of 1 + cap entries; zero ring[0] to restart."""
+    _check(LIB.pr_stamp(_ptr(ring), ring.numel() - 1, _stream(stream)), "pr_stamp")
+
+
 def test_philox(ctr, key: int, use_curand: bool, out, stream=None):
     n = ctr.numel() // 4
     _check(LIB.pr_test_philox(_ptr(ctr), n, key, 1 if use_curand else 0, _ptr(out), _stream(stream)),

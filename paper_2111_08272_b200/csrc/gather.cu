@@ -520,3 +520,20 @@ extern "C" int pr_spin(int64_t ns, void* stream) {
     PR_CUDA_TRY(cudaGetLastError());
     return PR_OK;
 }
+
+// ---- a5: device-side step stamps ---------------------------------------------------------------------
+namespace {
+__global__ void stamp_kernel(int64_t* ring, int64_t cap) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(ring), 1ull);
+    ring[1 + (int64_t)(i % (unsigned long long)cap)] = (int64_t)t;
+}
+}  // namespace
+
+extern "C" int pr_stamp(int64_t* d_ring, int64_t cap, void* stream) {
+    if (!d_ring || cap < 1) return PR_ERR_INVALID;
+    stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_ring, cap);
+    PR_CUDA_TRY(cudaGetLastError());
+    return PR_OK;
+}

@@ -64,6 +64,12 @@ class RunConfig:
     policy: dict | None = None              # Alloc.set_policy kwargs (e.g. never_freeze, ema_alpha)
     # time-varying stragglers: [(global_step, [σ_r ...]), ...]; σ at step s = the last entry with step <= s
     slowdown_schedule: list | None = None
+    # N1: overlap the weighted allreduce with backward.  The flat gradient buffer is cut into
+    # ~bucket_mb buckets in reverse parameter order; each bucket's K3 is launched on a comm stream from a
+    # post-accumulate-grad hook as soon as its last gradient is final (in bucket order on every rank).
+    # Needs graphs=True (the overlapped step is one captured graph per n_r).
+    overlap: bool = False
+    bucket_mb: float = 8.0
 
 
 def build_model(name: str, num_classes: int):
@@ -124,6 +130,11 @@ class Worker:
             p.grad = self.flat[off:off + p.numel()].as_strided(p.shape, p.stride())
             off += p.numel()
         self.opt = torch.optim.SGD(params, lr=cfg.lr, weight_decay=cfg.wd)
+        self._overlap = bool(cfg.overlap and comm is not None and world > 1)
+        if cfg.overlap and not cfg.graphs:
+            raise ValueError("overlap=True needs graphs=True")
+        if self._overlap:
+            self._setup_buckets(params)
         self.idx = torch.empty(cfg.N, dtype=torch.int64, device=self.dev)   # any shard size after re-allocation
         self.xdt = torch.bfloat16 if cfg.bf16_compute else torch.float32
         self.c0_ns = 0.0                               # calibrated per-sample compute time (ns) at σ = 1
@@ -132,6 +143,49 @@ class Worker:
         self.epoch = 0
         self.last_ts = 0.0
         self.history = []
+
+    # ---- N1: bucketed allreduce overlapped with backward ----------------------------------------------
+    def _setup_buckets(self, params):
+        """Buckets = contiguous ranges [lo, hi) of the flat buffer, filled in reverse parameter order (the
+        order backward finalises gradients), closed at >= bucket_mb and at 16-byte boundaries (K3 alignment)."""
+        import functools
+
+        spans, off = [], 0
+        for p in params:
+            spans.append((off, off + p.numel()))
+            off += p.numel()
+        limit = max(4, int(self.cfg.bucket_mb * 2 ** 20 / 4))
+        self._buckets, bucket_of, cur, hi = [], {}, [], None
+        for i in reversed(range(len(params))):
+            lo = spans[i][0]
+            hi = spans[i][1] if hi is None else hi
+            cur.append(i)
+            if (hi - lo >= limit and lo % 4 == 0) or i == 0:
+                for j in cur:
+                    bucket_of[j] = len(self._buckets)
+                self._buckets.append((lo, hi, len(cur)))
+                cur, hi = [], None
+        self._ready = [0] * len(self._buckets)
+        self._next, self._armed, self._n_armed = 0, False, 0
+        self._bucket_ev = [torch.cuda.Event() for _ in self._buckets]
+        self.comm_stream = torch.cuda.Stream(self.dev)
+        self.stamps = torch.zeros(1 + 2 * (self.cfg.N + 1), dtype=torch.int64, device=self.dev)
+        for i, p in enumerate(params):
+            p.register_post_accumulate_grad_hook(functools.partial(self._grad_ready, bucket_of[i]))
+
+    def _grad_ready(self, b, _param):
+        """Post-accumulate-grad hook (runs while backward is captured): launch every bucket that is complete,
+        in bucket order, on the comm stream after the work that produced it."""
+        if not self._armed:
+            return
+        self._ready[b] += 1
+        while self._next < len(self._buckets) and self._ready[self._next] == self._buckets[self._next][2]:
+            lo, hi, _ = self._buckets[self._next]
+            ev = self._bucket_ev[self._next]
+            ev.record(torch.cuda.current_stream(self.dev))
+            self.comm_stream.wait_event(ev)
+            pr.weighted_allreduce(self.comm, self.flat[lo:hi], self._n_armed, stream=self.comm_stream)
+            self._next += 1
 
     # ---- a3: data movement --------------------------------------------------------------------------
     def gather(self, first: int, rows: int, record=False):
@@ -157,7 +211,7 @@ class Worker:
             return x[:n_r].view(n_r, H, W, C).permute(0, 3, 1, 2)
         return x[:n_r].view(n_r, C, H, W)
 
-    def compute(self, x, y, n_r: int):
+    def compute(self, x, y, n_r: int, overlap: bool = False):
         cfg = self.cfg
         x = self._input(x, n_r)
         losses = []
@@ -166,8 +220,17 @@ class Worker:
             with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.bf16_compute):
                 out = self.model(xm)
                 loss = F.cross_entropy(out.float(), ym)
+            if overlap and m0 + cfg.micro >= n_r:             # N1: the last microbatch finalises every grad
+                self._ready, self._next, self._armed, self._n_armed = [0] * len(self._buckets), 0, True, n_r
             (loss * (xm.shape[0] / n_r)).backward()           # local mean over n_r (DESIGN §3 #11)
             losses.append(loss.detach() * xm.shape[0])
+        if overlap:
+            self._armed = False
+            if self._next != len(self._buckets):
+                raise RuntimeError(f"N1: {self._next} of {len(self._buckets)} buckets launched")
+            cur = torch.cuda.current_stream(self.dev)
+            pr.stamp(self.stamps, stream=cur)                  # end of this rank's compute (t_s, a5)
+            cur.wait_stream(self.comm_stream)                  # join: the update needs the reduced buffer
         ns = self._spin_ns(n_r)
         if ns > 0:
             pr.spin(ns)                                      # K4 on the current (possibly capturing) stream
@@ -224,17 +287,37 @@ class Worker:
         b.record(self.stream)
         b.synchronize()
         self.flat.zero_()                                     # discard the warm-up/calibration gradients
-        self._graphs[n_r] = (g, xs, ys, loss, a.elapsed_time(b) * 1e6 / calib_reps)
+        g2 = loss2 = None
+        if self._overlap:
+            # N1: a second graph of the same step whose backward launches the bucket allreduces (capture
+            # executes nothing, so no collective runs here; the plain graph above gave t1 without them)
+            g2 = torch.cuda.CUDAGraph()
+            side.wait_stream(self.stream)
+            self.cfg.slowdown = self.cfg.slowdown_schedule = None
+            with torch.cuda.graph(g2, pool=self._pool, stream=side):
+                loss2 = self.compute(xs, ys, n_r, overlap=True)
+            self.stream.wait_stream(side)
+            self.cfg.slowdown, self.cfg.slowdown_schedule = save, save_sched
+        self._graphs[n_r] = (g, xs, ys, loss, a.elapsed_time(b) * 1e6 / calib_reps, g2, loss2)
 
     def compute_graphed(self, x, y, n_r: int):
         """a4 through the captured graph; emulated slowdown σ_r (K4): a rank σ× slower takes σ× its own
         measured compute time, so the spin is (σ_r − 1)·t1(n_r) for the n_r it actually processes."""
         self.prepare(n_r)
-        g, xs, ys, loss, t1_ns = self._graphs[n_r]
+        g, xs, ys, loss, t1_ns, g2, loss2 = self._graphs[n_r]
         xs.copy_(x[:n_r])
         ys.copy_(y[:n_r])
-        g.replay()
         sigma = self.sigma()
+        if g2 is not None:
+            # N1: stamp, slowdown first (a slower GPU finishes every bucket later), then the step whose
+            # backward overlaps the bucket allreduces; the graph stamps the end of compute before its join
+            pr.stamp(self.stamps, stream=self.stream)
+            if sigma > 1.0:
+                pr.spin(int((sigma - 1.0) * t1_ns), stream=self.stream)
+            g2.replay()
+            self.launches += 2 + len(self._buckets) + (sigma > 1.0)
+            return loss2.clone()
+        g.replay()
         if sigma > 1.0:
             pr.spin(int((sigma - 1.0) * t1_ns), stream=self.stream)
             self.launches += 1
@@ -242,7 +325,11 @@ class Worker:
 
     # ---- a6-a9: weighted ring allreduce + SGD (Algorithm 1 steps 5-6) ---------------------------------
     def allreduce_and_update(self, n_r: int, record=False):
-        if self.P > 1:
+        if self._overlap and n_r == 0:                        # N1: an idle rank still joins every bucket
+            for lo, hi, _ in self._buckets:
+                pr.weighted_allreduce(self.comm, self.flat[lo:hi], 0, stream=self.stream)
+                self.launches += 1
+        elif self.P > 1 and not self._overlap:
             if record:
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(self.stream)
@@ -253,6 +340,16 @@ class Worker:
                 self.ar_events.append((a0, a1))
         self.opt.step()
         self.flat.zero_()
+
+    def _compute_time(self, ev) -> float:
+        """Σ over the recorded steps of this rank's compute time in seconds (a5).  With N1 the step's CUDA
+        events would include the overlapped allreduce (and the wait for peers), so the device stamps taken
+        before the spin and at the end of backward are used instead (DESIGN §3 #4: t_s excludes waiting)."""
+        if self._overlap:
+            k = int(self.stamps[0])
+            st = self.stamps[1:1 + k].cpu()
+            return float((st[1::2] - st[0::2]).sum()) / 1e9
+        return sum(a.elapsed_time(b) for a, b in ev) / 1e3
 
     # ---- one epoch (Algorithm 1 outer loop) -----------------------------------------------------------
     def _data(self, epoch: int, n_r: int, S: int, record: bool):
@@ -281,6 +378,8 @@ class Worker:
         else:
             xe, ye, e0, e1 = self._data(self.epoch, n_r, S, record)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
+        if self._overlap:
+            self.stamps[0].zero_()
         losses, host_losses = [], []
         for s in range(S):
             ev[s][0].record(self.stream)
@@ -303,7 +402,7 @@ class Worker:
             # are enqueued now and run while the host synchronises for t_s and runs the controller
             self._prefetched = ((self.epoch + 1, n_r), self._data(self.epoch + 1, n_r, S, record))
         ev[-1][1].synchronize()
-        t_s = (e0.elapsed_time(e1) + sum(a.elapsed_time(b) for a, b in ev)) / 1e3   # seconds (a5)
+        t_s = e0.elapsed_time(e1) / 1e3 + self._compute_time(ev)                      # seconds (a5)
         self.epoch += 1
         rec = {"t_s": t_s, "loss": float(torch.stack(losses).mean()), "S": S, "n_r": n_r, "w": v["w"]}
         self.history.append(rec)
@@ -332,6 +431,8 @@ class Worker:
             xe, ye = self.gather(0, ns * n_r, record)
             e1.record(self.stream)
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ns)]
+            if self._overlap:
+                self.stamps[0].zero_()
             for j in range(ns):
                 ev[j][0].record(self.stream)
                 if n_r > 0:
@@ -346,7 +447,7 @@ class Worker:
                 if loss_to_host:
                     host_losses.append(float(loss))
             ev[-1][1].synchronize()
-            t_seg = (e0.elapsed_time(e1) + sum(a.elapsed_time(b) for a, b in ev)) / 1e3
+            t_seg = e0.elapsed_time(e1) / 1e3 + self._compute_time(ev)
             t_epoch += t_seg
             changed = False
             if self.comm is not None:

@@ -20,7 +20,7 @@ def test_c2_lin_converges_and_meets_bound():
         pytest.skip("no CUDA device")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "experiments.py"), "--virtual", "--scenario", "c2-lin",
                           "--epochs", "3", "--N", "24576"], capture_output=True, text=True, timeout=600, cwd=ROOT)
-    recs = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    recs = [r for r in (json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")) if "epoch" in r]
     assert len(recs) == 3, out.stderr[-2000:]
     assert recs[0]["w"] == [12, 12]
     assert recs[1]["w"] == [8, 16] and recs[2]["w"] == [8, 16] and recs[2]["frozen"]

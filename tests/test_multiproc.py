@@ -129,3 +129,66 @@ def test_ipc_two_processes_one_gpu():
     for p in ps:
         p.join(60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def _overlap_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import gc
+
+        import paper_2111_08272_b200 as pr
+        from paper_2111_08272_b200.trainer import RunConfig, Worker
+
+        torch.cuda.set_device(0)
+        res, p0 = {}, None
+        for ov in (False, True):
+            comm = pr.comm_init(rank, world, 0, config=pr.comm_config(watchdog_ns=60_000_000_000))
+            cfg = RunConfig(N=2048, ratios=[1, 3], C=4, g=64, micro=1024, overlap=ov, bucket_mb=4.0)
+            w = Worker(cfg, rank, world, 0, comm)
+            if p0 is None:
+                p0 = torch.cat([p.detach().flatten() for p in w.model.parameters()]).cpu()
+            rec = w.run_epoch()
+            torch.cuda.synchronize()
+            params = torch.cat([p.detach().flatten() for p in w.model.parameters()]).cpu()
+            nb = len(w._buckets) if ov else 0
+            st = comm.status()
+            del w
+            gc.collect()
+            comm.destroy()
+            res[ov] = (params, rec["t_s"], nb, st)
+        d_base, d_ov = res[False][0] - p0, res[True][0] - p0
+        rel = float((d_ov - d_base).norm() / d_base.norm())
+        # every bucket reduced: the ranks hold bit-identical parameters after the overlapped epoch
+        mine = res[True][0].double()
+        other = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(other, mine)
+        same = all(torch.equal(o, other[0]) for o in other)
+        ok = (rel < 1e-2 and same and res[True][2] > 1 and res[True][1] > 0 and res[False][1] > 0
+              and res[True][3] == 0 and res[False][3] == 0)
+        q.put((rank, "ok" if ok else f"rel={rel} same={same} buckets={res[True][2]} t_s={res[True][1]}"))
+    except Exception as e:
+        import traceback
+
+        q.put((rank, repr(e) + traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_overlapped_bucket_allreduce_two_processes():
+    """N1: bucketed allreduce launched from backward hooks inside the captured step gives the same training
+    step as the allreduce after backward, and leaves the ranks with identical parameters."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_overlap_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in ps)
+    for p in ps:
+        p.join(60)
+    assert res == {0: "ok", 1: "ok"}, res
