@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpropring.so")
+# PROPRING_LIB: another build of this same library (tools/variants.sh compiles A/B variants for profiling)
+LIB_PATH = os.environ.get("PROPRING_LIB") or os.path.join(HERE, "libpropring.so")
 
 PR_MAX_RANKS = 64
 PR_GATHER_MAX_CHANNELS = 16

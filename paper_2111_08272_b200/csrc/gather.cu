@@ -137,61 +137,75 @@ __device__ __forceinline__ void convert_store(const GatherParams& p, uint8_t* dr
     }
 }
 
-// Channels-last: PX (8 or 16) consecutive pixels of all C channels (PX bytes per plane, plane stride ps,
-// in smem or global) -> PX·C interleaved outputs at pixel pix0 of the HWC output row, written as
-// PX·C·es/16 16-byte stores (es = 2 for bf16, 4 for f32).
+// Channels-last: PX (8 or 16) consecutive pixels of all C channels (ww = PX/4 words per channel) -> the
+// PX·C interleaved outputs (value k = pixel k / C, channel k mod C) as NV = PX·C·es/16 16-byte vectors o[]
+// (es = 2 for bf16, 4 for f32).
 template <int OP, int C, int PX>
-__device__ __forceinline__ void hwc_store(const GatherParams& p, uint8_t* drow, int64_t pix0, const uint8_t* s,
-                                          int64_t ps) {
+__device__ __forceinline__ void hwc_convert_words(const GatherParams& p, const uint32_t* ww, uint4* o) {
     float f[C][PX];
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-        uint32_t ww[PX / 4];
-        if (PX == 16) {
-            const uint4 w = *reinterpret_cast<const uint4*>(s + c * ps);
-            ww[0] = w.x; ww[1] = w.y; ww[2 % (PX / 4)] = w.z; ww[3 % (PX / 4)] = w.w;
-        } else {
-            const uint2 w = *reinterpret_cast<const uint2*>(s + c * ps);
-            ww[0] = w.x; ww[1 % (PX / 4)] = w.y;
-        }
-        affine_words<PX / 4>(ww, p.scale[c], p.shift[c], f[c]);
-    }
-    // interleaved value k = pixel (k / C), channel (k % C)
+    for (int c = 0; c < C; ++c) affine_words<PX / 4>(ww + c * (PX / 4), p.scale[c], p.shift[c], f[c]);
     if (OP == PR_GATHER_U8_TO_BF16_AFFINE) {
-        uint8_t* d = drow + pix0 * C * 2;
 #pragma unroll
         for (int q = 0; q < C * PX / 8; ++q) {
-            uint32_t o[4];
+            uint32_t h[4];
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int k = 8 * q + 2 * h;
-                o[h] = pack_bf16x2(f[k % C][k / C], f[(k + 1) % C][(k + 1) / C]);
+            for (int j = 0; j < 4; ++j) {
+                const int k = 8 * q + 2 * j;
+                h[j] = pack_bf16x2(f[k % C][k / C], f[(k + 1) % C][(k + 1) / C]);
             }
-            st_v4(d + 16 * q, make_uint4(o[0], o[1], o[2], o[3]));
+            o[q] = make_uint4(h[0], h[1], h[2], h[3]);
         }
     } else {
-        uint8_t* d = drow + pix0 * C * 4;
 #pragma unroll
         for (int q = 0; q < C * PX / 4; ++q) {
-            uint32_t o[4];
+            uint32_t h[4];
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int k = 4 * q + h;
-                o[h] = __float_as_uint(f[k % C][k / C]);
+            for (int j = 0; j < 4; ++j) {
+                const int k = 4 * q + j;
+                h[j] = __float_as_uint(f[k % C][k / C]);
             }
-            st_v4(d + 16 * q, make_uint4(o[0], o[1], o[2], o[3]));
+            o[q] = make_uint4(h[0], h[1], h[2], h[3]);
         }
     }
 }
 
-template <int OP, int PX = 8>
+template <int OP, int C, int PX>
+__device__ __forceinline__ void hwc_convert(const GatherParams& p, const uint8_t* s, int64_t ps, uint4* o) {
+    uint32_t ww[C * PX / 4];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        if (PX == 16) {
+            const uint4 w = *reinterpret_cast<const uint4*>(s + c * ps);
+            ww[4 * c] = w.x; ww[4 * c + 1] = w.y; ww[(4 * c + 2) % (C * PX / 4)] = w.z; ww[(4 * c + 3) % (C * PX / 4)] = w.w;
+        } else {
+            const uint2 w = *reinterpret_cast<const uint2*>(s + c * ps);
+            ww[2 * c] = w.x; ww[2 * c + 1] = w.y;
+        }
+    }
+    hwc_convert_words<OP, C, PX>(p, ww, o);
+}
+
+// TMA consumer path: 8 pixels from the smem stage straight to the HWC output row (8·C·es bytes per lane).
+template <int OP, int C>
+__device__ __forceinline__ void hwc_store(const GatherParams& p, uint8_t* drow, int64_t pix0, const uint8_t* s,
+                                          int64_t ps) {
+    constexpr int NV = C * 8 * (OP == PR_GATHER_U8_TO_BF16_AFFINE ? 2 : 4) / 16;
+    uint4 o[NV];
+    hwc_convert<OP, C, 8>(p, s, ps, o);
+    uint8_t* d = drow + pix0 * C * (OP == PR_GATHER_U8_TO_BF16_AFFINE ? 2 : 4);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) st_v4(d + 16 * q, o[q]);
+}
+
+template <int OP>
 __device__ __forceinline__ void hwc_dispatch(const GatherParams& p, uint8_t* drow, int64_t pix0, const uint8_t* s,
                                              int64_t ps) {
     switch (p.channels) {
-        case 1: hwc_store<OP, 1, PX>(p, drow, pix0, s, ps); break;
-        case 2: hwc_store<OP, 2, PX>(p, drow, pix0, s, ps); break;
-        case 3: hwc_store<OP, 3, PX>(p, drow, pix0, s, ps); break;
-        default: hwc_store<OP, 4, PX>(p, drow, pix0, s, ps); break;
+        case 1: hwc_store<OP, 1>(p, drow, pix0, s, ps); break;
+        case 2: hwc_store<OP, 2>(p, drow, pix0, s, ps); break;
+        case 3: hwc_store<OP, 3>(p, drow, pix0, s, ps); break;
+        default: hwc_store<OP, 4>(p, drow, pix0, s, ps); break;
     }
 }
 
@@ -211,15 +225,18 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) gather_kernel(const __grid_
             p.lab_dst[t] = p.lab_src[p.idx[t]];
     }
     if (OP != PR_GATHER_COPY && p.hwc) {
-        // channels-last: a lane takes 8 pixels of every plane (C 8-byte loads, coalesced per plane).
-        // 16-pixel items (PX=16: 16-byte loads) measured slower (99 vs 81 us on the epoch gather):
-        // 96-byte lane strides spread each warp store over twice the sectors.
+        // channels-last: a warp item is 32 lanes × 8 pixels of one row; per lane C 8-byte loads (one per
+        // plane, coalesced across the warp) and 8·C·es bytes of interleaved output stored directly.
+        // Measured alternatives (epoch gather, 49,152 rows, same box): this 83.5 us; 16-pixel items 99 us;
+        // per-warp smem staging for fully coalesced stores 85-86 us; ld.global.nc 3% slower; a software-
+        // pipelined loop (next item's loads before this item's stores) 87.8 us; grids of 2-80 waves slower
+        // than one resident wave.  A write-only probe reaches 6.6 TB/s (tools/probes/write_probe.cu).
         const int64_t groups = p.plane / 8, gsegs = (groups + 31) / 32;
         for (int64_t it = warp; it < p.n * gsegs; it += nwarps) {
             const int64_t row = it / gsegs, gi = (it - row * gsegs) * 32 + lane;
             if (gi < groups)
-                hwc_dispatch<OP, 8>(p, p.dst + row * p.row_bytes * out_mul, gi * 8,
-                                    p.src + __ldg(p.idx + row) * p.row_bytes + gi * 8, p.plane);
+                hwc_dispatch<OP>(p, p.dst + row * p.row_bytes * out_mul, gi * 8,
+                                 p.src + __ldg(p.idx + row) * p.row_bytes + gi * 8, p.plane);
         }
         return;
     }
@@ -488,8 +505,26 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
     }
     const int64_t vpr = row_bytes / 16;
     const int64_t items = n * ((vpr + kSegVec - 1) / kSegVec);
+    // grid = one resident wave (SMs × CTAs per SM from the occupancy calculator): a grid-stride loop over
+    // a grid larger than what fits leaves the second wave of CTAs as a tail
+    static int resident[3] = {0, 0, 0};
+    const int opi = p.op < 0 || p.op > 2 ? 2 : p.op;
+    if (!resident[opi]) {
+        int sms = 0, per_sm = 0, dev = 0;
+        PR_CUDA_TRY(cudaGetDevice(&dev));
+        PR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const void* fn = opi == 0 ? (const void*)gather_kernel<PR_GATHER_COPY>
+                         : opi == 1 ? (const void*)gather_kernel<PR_GATHER_U8_TO_F32_AFFINE>
+                                    : (const void*)gather_kernel<PR_GATHER_U8_TO_BF16_AFFINE>;
+        PR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarpsPerCta, 0));
+        resident[opi] = sms * (per_sm > 0 ? per_sm : 1);
+    }
     int64_t blocks = (items + kWarpsPerCta - 1) / kWarpsPerCta;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+#ifndef PR_GATHER_GRID
+    if (blocks > resident[opi]) blocks = resident[opi];
+#else
+    if (blocks > PR_GATHER_GRID) blocks = PR_GATHER_GRID;
+#endif
     if (blocks < 1) blocks = 1;
     switch (p.op) {
         case PR_GATHER_COPY: gather_kernel<PR_GATHER_COPY><<<(unsigned)blocks, 32 * kWarpsPerCta, 0, s>>>(p); break;

@@ -276,3 +276,17 @@ def test_spin_duration():
         # %globaltimer advances in coarse ticks (tens of us on B200): bound the absolute overshoot;
         # emulated slowdowns are ms-scale ((σ−1)·c0·n_r), where this is < 5% (the 1 ms case)
         assert ns / 1e6 * 0.99 <= ms <= ns / 1e6 * 1.02 + 0.05
+
+
+def test_stamp_ring_orders_and_wraps():
+    ring = torch.zeros(1 + 4, dtype=torch.int64, device="cuda")
+    for _ in range(6):
+        pr.stamp(ring)
+        pr.spin(20_000)
+    torch.cuda.synchronize()
+    r = ring.cpu().tolist()
+    assert r[0] == 6
+    s2, s3, s4, s5 = r[3], r[4], r[1], r[2]          # stamps 4 and 5 wrapped onto slots 0 and 1
+    assert s3 - s2 >= 20_000 and s4 - s3 >= 20_000 and s5 - s4 >= 20_000
+    with pytest.raises(pr.PropringError):
+        pr.stamp(torch.zeros(1, dtype=torch.int64, device="cuda"))
