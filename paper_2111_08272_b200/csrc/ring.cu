@@ -42,14 +42,8 @@ struct ChanFlags {          // written by peers, polled locally
     unsigned long long rs_credit;  uint64_t p1[15];   // by next: my slot-slices it has consumed (slot reuse)
     unsigned long long ag_ready;   uint64_t p2[15];   // by prev: direct all-gather slices written into my buf
 };
-struct HsEntry {            // handshake entry, written by rank q into every peer's page (slot [parity][q])
-    unsigned long long seq;
-    int64_t count;
-    int64_t n;
-    int32_t dtype;
-    int32_t reg_id;
-    int64_t offset;
-    uint64_t pad[3];
+struct HsEntry {            // handshake entry, written by rank q into every peer's page (slot [parity][q]):
+    uint64_t line[8];       // four LL lines: (seq32 | count, n, dtype/reg_id, offset halves), see handshake()
 };
 struct ChanState {          // local only: cumulative counters carried across calls
     unsigned long long seq;         // handshake sequence number
@@ -81,6 +75,8 @@ struct DevTable {
     uint64_t off_ts_flags, off_ts_staging;
     int32_t ts_slots, pad1;
     int64_t ts_slot_bytes;
+    uint64_t off_ll;                // LL ring: [channels][2P−2 phases][ll_region_bytes]
+    int64_t ll_region_bytes;        // 16-byte lines, 8 payload bytes each, for one channel's share of a chunk
     volatile int* status;           // host-mapped
     volatile long long* stamps;     // host-mapped [3]
     uint8_t* win[PR_MAX_RANKS];
@@ -120,6 +116,8 @@ void layout(DevTable& t) {
     o += (uint64_t)t.channels * sizeof(TsFlags);
     t.off_ts_staging = o = align_up(o, 4096);
     o += (uint64_t)t.channels * t.P * t.ts_slots * (uint64_t)t.ts_slot_bytes;
+    t.off_ll = o = align_up(o, 4096);
+    o += (uint64_t)t.channels * (uint64_t)(t.P > 1 ? 2 * t.P - 2 : 0) * (uint64_t)t.ll_region_bytes;
     t.window_bytes = align_up(o, 4096);
 }
 
@@ -316,15 +314,63 @@ __device__ __forceinline__ void for_each_step(int P, int r, int64_t nsl, int64_t
     }
 }
 
-// Handshake = the barrier; its duration is t_w.  Thread 0 only.  Publishes (seq, count,
-// dtype, n_r, registration) into every rank's page and waits for all P entries of this call (entries are
+// Handshake = the barrier; its duration is t_w.  Publishes (seq, count, dtype, n_r,
+// registration) into every rank's page and waits for all P entries of this call (entries are
 // double-buffered by seq parity).  Returns Σn and whether every rank's buffer is registered; fills ns[q]
 // (n of rank q) and bufs[q] (rank q's buffer mapped in this process, if registered) when given.
+//
+// Entries use the LL line format (see ring_ll_kernel): the 64-byte entry is four 16-byte lines of two
+// 64-bit elements, each (seq32 << 32 | 32 payload bits).  A 64-bit aligned element is single-copy
+// atomic, so a reader that sees the call's sequence number in all eight elements has the whole entry —
+// no release fence before a flag store (a MEMBAR.SYS at system scope, the dominant cost of a flag
+// round trip).  Ordering against the previous call's data is given by stream order: a rank publishes
+// its entry for call k only after its kernel for call k−1 has completed.
 struct HsOut {
     int err;
     int direct;
     long long sumn;
 };
+__device__ __forceinline__ void st_line64(void* p, unsigned long long a, unsigned long long b, bool sys) {
+    if (sys) asm volatile("st.relaxed.sys.global.v2.b64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+    else asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_line64(const void* p, unsigned long long& a, unsigned long long& b, bool sys) {
+    if (sys) asm volatile("ld.relaxed.sys.global.v2.b64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.v2.b64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ unsigned long long tag(uint32_t flag, uint32_t w) { return ((unsigned long long)flag << 32) | w; }
+__device__ __forceinline__ void hs_publish(HsEntry* e, uint32_t flag, long long count, long long n, uint32_t dtype,
+                                           int32_t reg_id, long long offset, bool sys) {
+    unsigned long long* L = reinterpret_cast<unsigned long long*>(e);
+    st_line64(L + 0, tag(flag, (uint32_t)count), tag(flag, (uint32_t)((unsigned long long)count >> 32)), sys);
+    st_line64(L + 2, tag(flag, (uint32_t)n), tag(flag, (uint32_t)((unsigned long long)n >> 32)), sys);
+    st_line64(L + 4, tag(flag, dtype), tag(flag, (uint32_t)reg_id), sys);
+    st_line64(L + 6, tag(flag, (uint32_t)offset), tag(flag, (uint32_t)((unsigned long long)offset >> 32)), sys);
+}
+// Poll one entry until all eight elements carry `flag`; false on watchdog expiry.
+__device__ __forceinline__ bool hs_read(const HsEntry* e, uint32_t flag, unsigned long long deadline, bool sys,
+                                        long long& count, long long& n, uint32_t& dtype, int32_t& reg_id,
+                                        long long& offset) {
+    const unsigned long long* L = reinterpret_cast<const unsigned long long*>(e);
+    unsigned long long w[8];
+    for (;;) {
+        ld_line64(L + 0, w[0], w[1], sys);
+        ld_line64(L + 2, w[2], w[3], sys);
+        ld_line64(L + 4, w[4], w[5], sys);
+        ld_line64(L + 6, w[6], w[7], sys);
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ok = ok && (uint32_t)(w[k] >> 32) == flag;
+        if (ok) break;
+        if (gtimer() > deadline) return false;
+    }
+    count = (long long)(((w[1] & 0xffffffffull) << 32) | (w[0] & 0xffffffffull));
+    n = (long long)(((w[3] & 0xffffffffull) << 32) | (w[2] & 0xffffffffull));
+    dtype = (uint32_t)w[4];
+    reg_id = (int32_t)(uint32_t)w[5];
+    offset = (long long)(((w[7] & 0xffffffffull) << 32) | (w[6] & 0xffffffffull));
+    return true;
+}
 // Executed by ALL 32 lanes of warp 0: lane q publishes into rank q's page and polls entry q of this
 // page (ranks q, q+32, …), so the P peers are contacted in parallel; Σn, "all registered" and the error
 // code are combined with warp shuffles (DESIGN.md §3 #37).  The result is valid in every lane.
@@ -335,25 +381,21 @@ __device__ HsOut handshake(const LaunchArgs& A, const RankCall& rc, const DevTab
     uint8_t* my = tab->win[r];
     const unsigned long long seq = st->seq + 1;
     const int par = (int)(seq & 1ull);
-    for (int q = lane; q < P; q += 32) {
-        HsEntry* e = hs_of(tab->win[q], tab, ch, par, r);
-        st_relaxed_s64(&e->count, A.count, sys);
-        st_relaxed_s64(&e->n, rc.n_local, sys);
-        st_relaxed_s64(&e->dtype, ((long long)rc.reg_id << 32) | (unsigned)A.dtype, sys);  // dtype | reg_id
-        st_relaxed_s64(&e->offset, rc.reg_off, sys);
-        st_release(&e->seq, seq, sys);
-    }
+    const uint32_t flag = (uint32_t)(seq & 0xffffffffull);
+    for (int q = lane; q < P; q += 32)
+        hs_publish(hs_of(tab->win[q], tab, ch, par, r), flag, A.count, rc.n_local, (uint32_t)A.dtype, rc.reg_id,
+                   rc.reg_off, sys);
     int err = 0, direct = 1;
     long long sumn = 0;
     for (int q = lane; q < P; q += 32) {
-        HsEntry* e = hs_of(my, tab, ch, par, q);
-        if (!wait_ge(&e->seq, seq, deadline, sys)) { err = PR_ERR_PEER_TIMEOUT; break; }
-        const long long cnt = ld_relaxed_s64(&e->count, sys);
-        const long long n = ld_relaxed_s64(&e->n, sys);
-        const long long dr = ld_relaxed_s64(&e->dtype, sys);
-        const long long off = ld_relaxed_s64(&e->offset, sys);
-        const int dt = (int)(dr & 0xffffffffll), rid = (int)(dr >> 32);
-        if (cnt != A.count || dt != A.dtype) err = PR_ERR_LENGTH_MISMATCH;
+        long long cnt, n, off;
+        uint32_t dt;
+        int32_t rid;
+        if (!hs_read(hs_of(my, tab, ch, par, q), flag, deadline, sys, cnt, n, dt, rid, off)) {
+            err = PR_ERR_PEER_TIMEOUT;
+            break;
+        }
+        if (cnt != A.count || (int)dt != A.dtype) err = PR_ERR_LENGTH_MISMATCH;
         sumn += n;
         if (rid < 0) direct = 0;
         if (ns) ns[q] = n;
@@ -683,6 +725,17 @@ template <> __device__ __forceinline__ uint4 pack_f<__nv_bfloat16>(const float* 
                       Vec<__nv_bfloat16>::pack(f[4], f[5]), Vec<__nv_bfloat16>::pack(f[6], f[7]));
 }
 
+// Executed by all 32 lanes of one warp: lane l waits on the counter of peer (r+1+l) mod P (and l+32, …),
+// so the P−1 acquire polls are in flight together instead of one after another (one flag latency per
+// wait point, not P−1).  True in every lane iff every peer reached `target` before the deadline.
+__device__ __forceinline__ bool warp_wait_peers(const unsigned long long* arr, unsigned long long target, int r, int P,
+                                                unsigned long long deadline, bool sys) {
+    bool ok = true;
+    for (int l = (int)(threadIdx.x & 31); l < P - 1; l += 32)
+        ok = ok && wait_ge(&arr[(r + 1 + l) % P], target, deadline, sys);
+    return __all_sync(0xffffffffu, ok);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__ LaunchArgs A) {
     __shared__ int s_err;
@@ -751,9 +804,8 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__
     for (int64_t i = 0; i < nsl; ++i) {
         const unsigned long long J = base + (unsigned long long)i;
         // ---- phase A: raw slice i of every chunk d != r -> rank d's staging [src r], all peers at once --------
-        if (t0 && J + 1 > K2)
-            for (int k = 1; k < P && !s_abort; ++k)
-                if (!wait_ge(&mf->credit[(r + k) % P], J + 1 - K2, deadline, sys)) fail();
+        if (threadIdx.x < 32 && J + 1 > K2)
+            if (!warp_wait_peers(mf->credit, J + 1 - K2, r, P, deadline, sys) && t0) fail();
         if (!sync_ok()) return;
         for (int k = 1; k < P; ++k) {                               // no barrier between destinations
             const int d = (r + k) % P;
@@ -773,11 +825,8 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__
         // ---- phase B: reduce chunk r's slice i in ring order, store into every rank's buffer -------------
         int64_t lo, len;
         range(r, i, lo, len);
-        if (t0)
-            for (int h = 1; h < P && !s_abort; ++h) {
-                const int q = (r + h) % P;
-                if (!wait_ge(&mf->ready[q], J + 1, deadline, sys)) fail();
-            }
+        if (threadIdx.x < 32)
+            if (!warp_wait_peers(mf->ready, J + 1, r, P, deadline, sys) && t0) fail();
         if (!sync_ok()) return;
         const int64_t nv = len / V;
         for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
@@ -816,16 +865,162 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__
         }
     }
     // every other rank's reduced chunk has landed in my buffer
-    if (t0)
-        for (int h = 1; h < P && !s_abort; ++h) {
-            const int q = (r + h) % P;
-            if (!wait_ge(&mf->ag[q], base + (unsigned long long)nsl, deadline, sys)) fail();
-        }
+    if (threadIdx.x < 32)
+        if (!warp_wait_peers(mf->ag, base + (unsigned long long)nsl, r, P, deadline, sys) && t0) fail();
     __syncthreads();
     if (t0) {
         if (!s_abort) st->ts_base = base + (unsigned long long)nsl;
         if (ch == 0) tab->stamps[2] = (long long)gtimer();
     }
+}
+
+// =====================================================================================================
+// LL ring (low-latency protocol for small buffers): the SAME ring schedule, order and per-hop rounding as
+// ring_kernel — so the result is bit-identical — but every 16-byte line a rank pushes carries its own
+// validity: two 64-bit elements, each (flag << 32 | 32 payload bits), flag = the call's handshake sequence.
+// A 64-bit aligned element is single-copy atomic, so a receiver that sees the flag in an element also
+// sees that element's payload: no release fence, no separate ready flag, no credit — the receiver polls
+// the data itself.  Each phase h has its own region in the next rank's window (2P−2 regions), so a line is
+// written once per call; the handshake (a barrier: every rank has finished the previous call) makes
+// reusing the regions in the next call safe.  Half of every line is flag, so this trades bandwidth for
+// latency: one store + one poll per hop instead of store → fence → flag → poll → TMA load.
+// Each thread owns the same line positions in every phase, so a thread runs its own mini-ring and the
+// CTA never synchronises between phases.
+// =====================================================================================================
+__device__ __forceinline__ void st_ll(void* p, uint32_t d0, uint32_t d1, uint32_t flag, bool sys) {
+    st_line64(p, tag(flag, d0), tag(flag, d1), sys);
+}
+// one 32-bit payload word: 1 fp32 or 2 bf16 (the ring's Vec<T>::op on a quarter vector)
+template <typename T> __device__ __forceinline__ uint32_t ll_op(int mode, float s, uint32_t g, uint32_t in);
+template <> __device__ __forceinline__ uint32_t ll_op<float>(int mode, float s, uint32_t g, uint32_t in) {
+    const float gv = __uint_as_float(g), iv = __uint_as_float(in);
+    float r;
+    if (mode == M_SCALE) r = __fmul_rn(s, gv);
+    else if (mode == M_FMA) r = __fmaf_rn(s, gv, iv);
+    else if (mode == M_COPY) r = iv;
+    else r = 0.0f;
+    return __float_as_uint(r);
+}
+template <> __device__ __forceinline__ uint32_t ll_op<__nv_bfloat16>(int mode, float s, uint32_t g, uint32_t in) {
+    using B = Vec<__nv_bfloat16>;
+    if (mode == M_COPY) return in;
+    return B::pack(B::one(mode, s, B::lo(g), B::lo(in)), B::one(mode, s, B::hi(g), B::hi(in)));
+}
+// load / store the elements of one line (8 bytes = E elements); `nv` < E only on the buffer's last line
+template <typename T> __device__ __forceinline__ void ld_line(const T* p, int nv, uint32_t& w0, uint32_t& w1) {
+    constexpr int E = 8 / (int)sizeof(T);
+    if (nv == E) {
+        asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(w0), "=r"(w1) : "l"(p));
+        return;
+    }
+    uint16_t h[4] = {0, 0, 0, 0};
+    const uint16_t* q = reinterpret_cast<const uint16_t*>(p);
+    for (int k = 0; k < nv * (int)sizeof(T) / 2; ++k) h[k] = q[k];
+    w0 = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
+    w1 = (uint32_t)h[2] | ((uint32_t)h[3] << 16);
+}
+template <typename T> __device__ __forceinline__ void st_line(T* p, int nv, uint32_t w0, uint32_t w1) {
+    constexpr int E = 8 / (int)sizeof(T);
+    if (nv == E) {
+        asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(w0), "r"(w1) : "memory");
+        return;
+    }
+    const uint16_t h[4] = {(uint16_t)(w0 & 0xffffu), (uint16_t)(w0 >> 16), (uint16_t)(w1 & 0xffffu), (uint16_t)(w1 >> 16)};
+    uint16_t* q = reinterpret_cast<uint16_t*>(p);
+    for (int k = 0; k < nv * (int)sizeof(T) / 2; ++k) q[k] = h[k];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, 1) ring_ll_kernel(const __grid_constant__ LaunchArgs A) {
+    __shared__ int s_err;
+    __shared__ long long s_sumn;
+    __shared__ unsigned s_flag;
+    const RankCall& rc = A.calls[blockIdx.y];
+    const DevTable* tab = rc.tab;
+    const int ch = blockIdx.x;
+    const int r = tab->rank, P = tab->P;
+    const int next = (r + 1) % P;
+    uint8_t* my = tab->win[r];
+    ChanState* st = state_of(my, tab, ch);
+    const bool t0 = threadIdx.x == 0;
+    const bool sys = tab->sysscope != 0;
+    unsigned long long deadline = ~0ull;
+    if (threadIdx.x < 32) {                           // warp 0: the handshake = the barrier
+        const unsigned long long start = gtimer();
+        if (t0 && ch == 0) tab->stamps[0] = (long long)start;
+        if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
+        const HsOut hs = handshake(A, rc, tab, st, ch, sys, deadline, nullptr, nullptr);
+        if (t0) {
+            s_err = hs.err;
+            s_sumn = hs.sumn;
+            s_flag = (unsigned)(st->seq & 0xffffffffull);   // this call's sequence: the line flag
+            if (ch == 0) tab->stamps[1] = (long long)gtimer();
+        }
+    }
+    __syncthreads();
+    if (s_err) {
+        if (t0) latch(tab, s_err);
+        return;
+    }
+    if (tab->watchdog_ns > 0) deadline = gtimer() + (unsigned long long)tab->watchdog_ns;
+    constexpr int V = Vec<T>::V;
+    constexpr int E = 8 / (int)sizeof(T);                          // elements per line
+    const int64_t count = A.count;
+    const int64_t per = (count + P - 1) / P;
+    const int64_t cs = (per + V - 1) / V * V;                      // chunk elements (as ring_kernel)
+    const int64_t subp = (cs + tab->channels - 1) / tab->channels;
+    const int64_t sub = (subp + V - 1) / V * V;                   // this channel's share of a chunk
+    const float s = (float)((double)rc.n_local / (double)s_sumn);  // n_r/Σn: fp64 division, fp32 weight
+    const bool act = rc.n_local > 0;
+    const uint32_t flag = s_flag;
+    T* buf = reinterpret_cast<T*>(rc.buf);
+    uint8_t* my_ll = my + tab->off_ll + (size_t)ch * (size_t)(2 * P - 2) * (size_t)tab->ll_region_bytes;
+    uint8_t* nx_ll = tab->win[next] + tab->off_ll + (size_t)ch * (size_t)(2 * P - 2) * (size_t)tab->ll_region_bytes;
+    bool bad = false;
+    for (int h = 0; h < 2 * P - 1 && !bad; ++h) {
+        int kind, c;
+        if (h == 0) { kind = K_FIRST; c = r; }
+        else if (h <= P - 2) { kind = K_MID; c = (r - h + P) % P; }
+        else if (h == P - 1) { kind = K_LAST; c = (r + 1) % P; }
+        else if (h <= 2 * P - 3) { kind = K_AGMID; c = (r + 1 - (h - (P - 1)) + P) % P; }
+        else { kind = K_AGLAST; c = (r + 2) % P; }
+        const int64_t clo = (int64_t)c * cs;
+        const int64_t chi = min(clo + cs, count);
+        const int64_t lo = clo + (int64_t)ch * sub;
+        const int64_t hi = min(clo + min((int64_t)(ch + 1) * sub, cs), chi);
+        const int64_t len = hi > lo ? hi - lo : 0;
+        const int64_t nl = (len + E - 1) / E;
+        int mode;
+        if (kind == K_FIRST) mode = act ? M_SCALE : M_ZERO;
+        else if (kind == K_MID || kind == K_LAST) mode = act ? M_FMA : M_COPY;
+        else mode = M_COPY;
+        const bool needs_g = act && kind <= K_LAST;
+        const uint8_t* in_reg = h > 0 ? my_ll + (size_t)(h - 1) * tab->ll_region_bytes : nullptr;
+        uint8_t* out_reg = h < 2 * P - 2 ? nx_ll + (size_t)h * tab->ll_region_bytes : nullptr;
+        for (int64_t j = threadIdx.x; j < nl; j += blockDim.x) {
+            const int nv = (int)min((int64_t)E, len - j * E);
+            T* p = buf + lo + j * E;
+            uint32_t g0 = 0, g1 = 0, i0 = 0, i1 = 0;
+            if (needs_g) ld_line<T>(p, nv, g0, g1);
+            if (in_reg) {                                          // poll the line until both halves carry this call's flag
+                unsigned long long a, b;
+                for (;;) {
+                    ld_line64(in_reg + (size_t)j * 16, a, b, sys);
+                    if ((uint32_t)(a >> 32) == flag && (uint32_t)(b >> 32) == flag) break;
+                    if (gtimer() > deadline) { bad = true; break; }
+                }
+                if (bad) break;
+                i0 = (uint32_t)a;
+                i1 = (uint32_t)b;
+            }
+            const uint32_t y0 = ll_op<T>(mode, s, g0, i0), y1 = ll_op<T>(mode, s, g1, i1);
+            if (out_reg) st_ll(out_reg + (size_t)j * 16, y0, y1, flag, sys);
+            if (kind >= K_LAST) st_line<T>(p, nv, y0, y1);          // reduced / gathered chunk -> own buffer
+        }
+    }
+    if (bad) latch(tab, PR_ERR_PEER_TIMEOUT);
+    __syncthreads();
+    if (t0 && ch == 0) tab->stamps[2] = (long long)gtimer();
 }
 
 __global__ void allgather_f64_kernel(const DevTable* tab, unsigned long long seq, double v, double* out) {
@@ -866,7 +1061,7 @@ struct Reg {
 struct Hello {
     cudaIpcMemHandle_t handle;
     int32_t P, rank, device, channels, slots, threads, stages, tile_bytes, algo, ts_slots;
-    int64_t ts_slot_bytes, ts_max_bytes;
+    int64_t ts_slot_bytes, ts_max_bytes, ll_max_bytes;
     int64_t slot_bytes, window_bytes;
     uint64_t bytes;   // registration size
     unsigned char uuid[16];   // device identity: peers on another GPU need .sys-scope synchronisation
@@ -911,6 +1106,7 @@ pr_comm_config default_config() {
     c.ts_slots = 2;
     c.ts_slot_bytes = 64 * 1024;
     c.ts_max_bytes = 4ll << 20;     // measured crossover (co-located P = 4, 8): two-shot wins up to ~4 MiB
+    c.ll_max_bytes = 256 * 1024;
     return c;
 }
 
@@ -918,11 +1114,22 @@ int check_config(const pr_comm_config& c) {
     if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
-        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_AUTO ||
+        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_LL ||
+        c.ll_max_bytes < 0 || c.ll_max_bytes > (64ll << 20) ||
         c.ts_slots < 2 || c.ts_slots > 16 || c.ts_slot_bytes < 256 || c.ts_slot_bytes % 256 ||
         c.ts_slot_bytes > (16ll << 20) || c.ts_max_bytes < 0)
         return PR_ERR_INVALID;
     return PR_OK;
+}
+
+// Bytes of one LL region: 2 × (one channel's share of a chunk of the largest LL buffer), for either dtype
+// (chunk and share are rounded up to 16 bytes exactly as the kernels round them in elements).
+uint64_t ll_region_bytes(const pr_comm_config& c, int P) {
+    if (P < 2 || c.ll_max_bytes <= 0) return 0;
+    const uint64_t per = ((uint64_t)c.ll_max_bytes + P - 1) / P;
+    const uint64_t cs = align_up(per, 16);
+    const uint64_t sub = align_up((cs + c.channels - 1) / c.channels, 16);
+    return 2 * sub;
 }
 
 int alloc_common(pr_comm* c) {
@@ -938,6 +1145,7 @@ int alloc_common(pr_comm* c) {
     t.tile_bytes = c->cfg.tile_bytes;
     t.ts_slots = c->cfg.ts_slots;
     t.ts_slot_bytes = c->cfg.ts_slot_bytes;
+    t.ll_region_bytes = (int64_t)ll_region_bytes(c->cfg, c->P);
     layout(t);
     PR_CUDA_TRY(cudaMalloc((void**)&c->win, t.window_bytes));
     PR_CUDA_TRY(cudaMemset(c->win, 0, t.window_bytes));
@@ -1011,6 +1219,17 @@ int launch_ring(const LaunchArgs& a, int nranks, const pr_comm_config& cfg, cuda
     const int32_t threads = cfg.threads, channels = cfg.channels;
     // algorithm: a pure function of (config, count, dtype), identical on every rank
     const int64_t bytes = a.count * (a.dtype == PR_DTYPE_F32 ? 4 : 2);
+    if ((cfg.algo == PR_ALGO_LL || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.ll_max_bytes) {
+        void* fn3 = (a.dtype == PR_DTYPE_F32) ? (void*)ring_ll_kernel<float> : (void*)ring_ll_kernel<__nv_bfloat16>;
+        void* args3[] = {(void*)&a};
+        const dim3 grid3((unsigned)channels, (unsigned)nranks), block3((unsigned)threads);
+        if (coop) {
+            PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn3, grid3, block3, args3, 0, s));
+        } else {
+            PR_CUDA_TRY(cudaLaunchKernel(fn3, grid3, block3, args3, 0, s));
+        }
+        return PR_OK;
+    }
     if (cfg.algo == PR_ALGO_TWO_SHOT || (cfg.algo == PR_ALGO_AUTO && bytes <= cfg.ts_max_bytes)) {
         void* fn2 = (a.dtype == PR_DTYPE_F32) ? (void*)twoshot_kernel<float> : (void*)twoshot_kernel<__nv_bfloat16>;
         void* args2[] = {(void*)&a};
@@ -1063,6 +1282,7 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
     me.stages = c->cfg.stages; me.tile_bytes = c->cfg.tile_bytes;
     me.algo = c->cfg.algo; me.ts_slots = c->cfg.ts_slots; me.ts_slot_bytes = c->cfg.ts_slot_bytes;
     me.ts_max_bytes = c->cfg.ts_max_bytes;
+    me.ll_max_bytes = c->cfg.ll_max_bytes;
     {
         cudaDeviceProp prop;
         if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) std::memcpy(me.uuid, &prop.uuid, 16);
@@ -1076,7 +1296,8 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
         if (h.bytes) rc = rc ? rc : PR_ERR_CUDA;
         if (h.P != P || h.rank != q || h.channels != me.channels || h.slots != me.slots || h.slot_bytes != me.slot_bytes ||
             h.threads != me.threads || h.stages != me.stages || h.tile_bytes != me.tile_bytes || h.algo != me.algo ||
-            h.ts_slots != me.ts_slots || h.ts_slot_bytes != me.ts_slot_bytes || h.ts_max_bytes != me.ts_max_bytes)
+            h.ts_slots != me.ts_slots || h.ts_slot_bytes != me.ts_slot_bytes || h.ts_max_bytes != me.ts_max_bytes ||
+            h.ll_max_bytes != me.ll_max_bytes)
             rc = rc ? rc : PR_ERR_INVALID;
     }
     if (rc) { free_comm(c); return rc; }

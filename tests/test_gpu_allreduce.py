@@ -294,7 +294,8 @@ def test_two_shot_small_slots_many_slices_and_sys_scope():
 
 
 def test_auto_mixes_algorithms_back_to_back():
-    """ALGO_AUTO: two-shot up to ts_max_bytes, ring above; interleaved calls share the handshake sequence."""
+    """ALGO_AUTO: LL ring up to ll_max_bytes (256 KiB), two-shot up to ts_max_bytes, ring above; interleaved
+    calls share the handshake sequence (the LL line flag) and the counters."""
     P = 4
     comms = group(P, algo=pr.ALGO_AUTO, ts_max_bytes=1 << 20)
     for it, L in enumerate([100, 2 ** 20, 3, 300_000, 5_000_000, 17]):   # 400 B .. 20 MB
@@ -321,3 +322,80 @@ def test_two_shot_graph_replay():
         g.replay()
         torch.cuda.synchronize()
         assert all(np.array_equal(d.cpu().numpy(), emu) for d in dev)
+
+
+# ---- LL ring: the ring's schedule and rounding with a low-latency line protocol (same bits) ------------
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 8])
+def test_ll_ring_bit_identical_to_ring_replay(P, dtype):
+    comms = group(P, algo=pr.ALGO_LL, ll_max_bytes=1 << 20)
+    rng = np.random.Generator(np.random.PCG64(200 + P))
+    for L in (1, 2, 3, 5, 7, P + 1, 1000, 4099, 65_537, 2 ** 18 - 1):   # ragged last lines (fp32 1/2, bf16 1..4)
+        n = [int(x) * 16 for x in rng.integers(1, 9, P)]
+        if L % 2:
+            n[int(rng.integers(0, P))] = 0
+        _check(P, L, dtype, n, comms, kind="mixed" if L % 3 == 0 else "gaussian", seed=L)
+
+
+def test_ll_ring_many_calls_reuse_regions_and_sys_scope():
+    """The line flag is the call's handshake sequence: back-to-back calls rewrite the same regions, and a
+    stale line from the previous call must never pass (the results would then differ from the replay)."""
+    for cfg in (dict(channels=3), dict(channels=16, sys_scope=True), dict(channels=1, threads=64)):
+        P = 4
+        comms = group(P, algo=pr.ALGO_LL, **cfg)
+        for it in range(12):
+            L = [999, 65_536, 3, 40_001][it % 4]
+            _check(P, L, "f32" if it % 3 else "bf16", [it % 5, 2, 3, 1 + it], comms, seed=100 + it)
+
+
+def test_ll_ring_above_ll_max_takes_the_ring():
+    P = 3
+    comms = group(P, algo=pr.ALGO_LL, ll_max_bytes=4096)
+    for L in (1000, 1025, 300_000):        # 4,000 B (LL), 4,100 B and 1.2 MB (ring)
+        _check(P, L, "f32", [1, 2, 3], comms, seed=L)
+
+
+def test_ll_ring_graph_replay():
+    P, L = 3, 40_000
+    comms = group(P, algo=pr.ALGO_LL)
+    host, dev = _inputs(P, L, "f32", seed=31)
+    src = [d.clone() for d in dev]
+    n = [3, 0, 2]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        pr.weighted_allreduce_local(comms, dev, n, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            pr.weighted_allreduce_local(comms, dev, n, stream=s)
+    emu = W.ring_emulate(host, n, "f32")
+    for _ in range(3):
+        for d, s0 in zip(dev, src):
+            d.copy_(s0)
+        g.replay()
+        torch.cuda.synchronize()
+        assert all(np.array_equal(d.cpu().numpy(), emu) for d in dev)
+
+
+def test_ll_ring_length_mismatch_and_timeout_latch():
+    P = 2
+    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, algo=pr.ALGO_LL, watchdog_ns=1_000_000_000))
+    a = torch.randn(1000, device="cuda")
+    b = torch.randn(1000, device="cuda")
+    a0, b0 = a.clone(), b.clone()
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    pr.weighted_allreduce(comms[0], a, 1, stream=s0, count=1000)
+    pr.weighted_allreduce(comms[1], b, 1, stream=s1, count=999)
+    torch.cuda.synchronize()
+    assert comms[0].status() == pr.PR_ERR_LENGTH_MISMATCH and comms[1].status() == pr.PR_ERR_LENGTH_MISMATCH
+    assert torch.equal(a, a0) and torch.equal(b, b0)
+    for c in comms:
+        c.destroy()
+    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, algo=pr.ALGO_LL, watchdog_ns=300_000_000))
+    pr.weighted_allreduce(comms[0], a, 1, stream=s0)
+    torch.cuda.synchronize()
+    assert comms[0].status() == pr.PR_ERR_PEER_TIMEOUT
+    for c in comms:
+        c.destroy()

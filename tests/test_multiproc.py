@@ -94,21 +94,29 @@ def _gpu_worker(rank, world, port, q):
         from oracle import wavg as W
 
         torch.cuda.set_device(0)
-        comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=2, watchdog_ns=30_000_000_000))
-        L = 4099
-        g = synth.gradients(world, L, seed_base=11)
-        buf = comm.alloc(L * 4, dtype=torch.float32)
-        buf.copy_(torch.from_numpy(g[rank]))
-        n = [3, 5]
-        pr.weighted_allreduce(comm, buf, n[rank])
-        torch.cuda.synchronize()
-        st = comm.status()
-        ok = st == 0 and np.array_equal(buf.cpu().numpy(), W.ring_emulate(g, n, "f32"))
-        t = comm.allgather_f64(1.5 + rank)
-        ok = ok and t == [1.5, 2.5]
-        dist.barrier()
-        comm.destroy()
-        q.put((rank, "ok" if ok else f"bad status={st}"))
+        bad = []
+        # every algorithm over real CUDA-IPC peer windows; the LL ring also at forced system scope
+        for algo, sys_scope in ((pr.ALGO_RING, False), (pr.ALGO_TWO_SHOT, False), (pr.ALGO_LL, False),
+                                (pr.ALGO_LL, True)):
+            comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=2, watchdog_ns=30_000_000_000,
+                                                                      algo=algo, sys_scope=sys_scope))
+            L = 4099
+            g = synth.gradients(world, L, seed_base=11)
+            buf = comm.alloc(L * 4, dtype=torch.float32)
+            n = [3, 5]
+            for _ in range(3):                      # repeated calls: counters / line flags advance
+                buf.copy_(torch.from_numpy(g[rank]))
+                pr.weighted_allreduce(comm, buf, n[rank])
+            torch.cuda.synchronize()
+            st = comm.status()
+            ok = st == 0 and np.array_equal(buf.cpu().numpy(), W.ring_emulate(g, n, "f32"))
+            t = comm.allgather_f64(1.5 + rank)
+            ok = ok and t == [1.5, 2.5]
+            if not ok:
+                bad.append(f"algo={algo} sys={sys_scope} status={st}")
+            dist.barrier()
+            comm.destroy()
+        q.put((rank, "ok" if not bad else "; ".join(bad)))
     except Exception as e:
         q.put((rank, repr(e)))
     finally:
