@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--algos", default="ring,two_shot,ll")
     ap.add_argument("--channels", type=int, default=16)
     ap.add_argument("--ll-max", type=int, default=16 << 20)
+    ap.add_argument("--slots", type=int, default=8)
+    ap.add_argument("--slot-bytes", type=int, default=256 * 1024)
     a = ap.parse_args()
     P = a.P
     n = [64 * (1 + (r % 4)) for r in range(P)]
@@ -38,7 +40,8 @@ def main():
     for algo_name in a.algos.split(","):
         algo = {"ring": pr.ALGO_RING, "two_shot": pr.ALGO_TWO_SHOT, "ll": pr.ALGO_LL}[algo_name]
         comms = pr.comm_init_local(P, 0, pr.comm_config(algo=algo, sys_scope=a.sys, channels=a.channels,
-                                                         ll_max_bytes=a.ll_max))
+                                                         ll_max_bytes=a.ll_max, slots=a.slots,
+                                                         slot_bytes=a.slot_bytes))
         zmax = max(sizes)
         if a.staged:
             raws = [torch.empty(zmax, dtype=torch.uint8, device="cuda") for _ in range(P)]
@@ -62,7 +65,8 @@ def main():
             ok = all(c.status() == 0 for c in comms)
             print(json.dumps({"algo": algo_name, "P": P, "bytes": Z, "us": round(us, 2),
                               "t_w_us": (st[1] - st[0]) / 1e3, "t_c_us": (st[2] - st[1]) / 1e3,
-                              "staged": a.staged, "sys": a.sys, "channels": a.channels, "ok": ok}), flush=True)
+                              "staged": a.staged, "sys": a.sys, "channels": a.channels, "slots": a.slots,
+                              "slot_bytes": a.slot_bytes, "ok": ok}), flush=True)
         del raws
         for c in comms:
             c.destroy()
