@@ -209,8 +209,60 @@ __device__ __forceinline__ void hwc_dispatch(const GatherParams& p, uint8_t* dro
     }
 }
 
+// Channels-last LSU loop: a warp item is 32 lanes × 8 pixels of one row.  ITEMS items per iteration: all
+// their loads (C 8-byte loads per item per lane, coalesced across the warp) are issued before any
+// conversion/store, so ITEMS·C loads are in flight per lane.  Measured (epoch gather, 49,152 DISTINCT rows,
+// tools/ab_gather.sh): ITEMS 1 / 2 / 3 at 64 regs (4 CTAs per SM) 85.6 / 89.7 / 95.3 µs; ITEMS 2 at 96 regs
+// (2 CTAs per SM) 104.8 µs — more loads in flight do not help; occupancy does, up to 4 CTAs per SM (48
+// regs, 5 CTAs: 96 µs).
+#ifndef PR_HWC_ITEMS
+#define PR_HWC_ITEMS 1
+#endif
+template <int OP, int C>
+__device__ __forceinline__ void hwc_lsu_loop(const GatherParams& p, int64_t warp, int64_t nwarps, int lane) {
+    constexpr int ITEMS = PR_HWC_ITEMS;
+    constexpr int es = OP == PR_GATHER_U8_TO_BF16_AFFINE ? 2 : 4;
+    constexpr int NV = C * 8 * es / 16;
+    const int64_t groups = p.plane / 8, gsegs = (groups + 31) / 32;
+    const int64_t total = p.n * gsegs;
+    const int64_t out_row = p.row_bytes * es;
+    for (int64_t it0 = warp; it0 < total; it0 += (int64_t)ITEMS * nwarps) {
+        uint32_t ww[ITEMS][C * 2];
+        int64_t drow_off[ITEMS];
+        bool ok[ITEMS];
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            const int64_t it = it0 + (int64_t)u * nwarps;
+            const int64_t row = it / gsegs, gi = (it - row * gsegs) * 32 + lane;
+            ok[u] = it < total && gi < groups;
+            drow_off[u] = row * out_row + gi * 8 * C * es;
+            if (ok[u]) {
+                const uint8_t* s = p.src + __ldg(p.idx + row) * p.row_bytes + gi * 8;
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const uint2 w = *reinterpret_cast<const uint2*>(s + c * p.plane);
+                    ww[u][2 * c] = w.x;
+                    ww[u][2 * c + 1] = w.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            if (!ok[u]) continue;
+            uint4 o[NV];
+            hwc_convert_words<OP, C, 8>(p, ww[u], o);
+            uint8_t* d = p.dst + drow_off[u];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) st_v4(d + 16 * q, o[q]);
+        }
+    }
+}
+
+#ifndef PR_GATHER_MINB
+#define PR_GATHER_MINB 4
+#endif
 template <int OP>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) gather_kernel(const __grid_constant__ GatherParams p) {
+__global__ void __launch_bounds__(32 * kWarpsPerCta, PR_GATHER_MINB) gather_kernel(const __grid_constant__ GatherParams p) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -231,12 +283,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) gather_kernel(const __grid_
         // per-warp smem staging for fully coalesced stores 85-86 us; ld.global.nc 3% slower; a software-
         // pipelined loop (next item's loads before this item's stores) 87.8 us; grids of 2-80 waves slower
         // than one resident wave.  A write-only probe reaches 6.6 TB/s (tools/probes/write_probe.cu).
-        const int64_t groups = p.plane / 8, gsegs = (groups + 31) / 32;
-        for (int64_t it = warp; it < p.n * gsegs; it += nwarps) {
-            const int64_t row = it / gsegs, gi = (it - row * gsegs) * 32 + lane;
-            if (gi < groups)
-                hwc_dispatch<OP>(p, p.dst + row * p.row_bytes * out_mul, gi * 8,
-                                 p.src + __ldg(p.idx + row) * p.row_bytes + gi * 8, p.plane);
+        switch (p.channels) {
+            case 1: hwc_lsu_loop<OP, 1>(p, warp, nwarps, lane); break;
+            case 2: hwc_lsu_loop<OP, 2>(p, warp, nwarps, lane); break;
+            case 3: hwc_lsu_loop<OP, 3>(p, warp, nwarps, lane); break;
+            default: hwc_lsu_loop<OP, 4>(p, warp, nwarps, lane); break;
         }
         return;
     }

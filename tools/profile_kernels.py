@@ -34,7 +34,9 @@ def timed(fn, reps):
 def gather(rows, row_bytes, nsrc, reps, plane, impls=(1, 2), layout=0):
     X = torch.randint(0, 256, (nsrc, row_bytes), dtype=torch.uint8, device="cuda")
     Y = torch.randint(0, 10, (nsrc,), dtype=torch.int64, device="cuda")
-    idx = torch.randint(0, nsrc, (rows,), device="cuda")
+    # distinct rows, like a shard of the per-epoch permutation (sampling with replacement would let
+    # repeated rows hit in L2 and flatter the kernel)
+    idx = torch.randperm(nsrc, device="cuda")[:rows] if rows <= nsrc else torch.randint(0, nsrc, (rows,), device="cuda")
     out = torch.empty((rows, row_bytes), dtype=torch.bfloat16, device="cuda")
     lab = torch.empty(rows, dtype=torch.int64, device="cuda")
     for impl in impls:
