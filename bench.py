@@ -260,12 +260,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_epoch, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "resnet18-cifar10-shaped-50k, global batch 1024 (g=16, C=64), equal start, "
-                                   "self-adaptive allocation, fp32 gradients (11,689,512), bf16 autocast compute",
-                       "model": "resnet18 (1000-class head, random init)", "global_batch": 1024,
-                       "seq_len": None, "parallelism": f"dp{world}", "step": "one epoch (S=48 aggregations)",
-                       "overlap": bool(args.overlap and world > 1),
-                       "l2": "inputs larger than L2 (153.6 MB data set streamed every epoch)"},
+            "config": bench_config(world, bool(args.overlap and world > 1)),
             "epoch_time_s": ms_epoch / 1e3,
             "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
             "roofline_detail": roof,
@@ -290,6 +285,15 @@ def run_ours(args):
         comm.destroy()
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_config(world, overlap=False):
+    """The workload both arms name (our arm and --impl reference print the same config)."""
+    return {"workload": "resnet18-cifar10-shaped-50k, global batch 1024 (g=16, C=64), equal start, "
+                        "self-adaptive allocation, fp32 gradients (11,689,512), bf16 autocast compute",
+            "model": "resnet18 (1000-class head, random init)", "global_batch": 1024,
+            "seq_len": None, "parallelism": f"dp{world}", "step": "one epoch (S=48 aggregations)",
+            "overlap": overlap, "l2": "inputs larger than L2 (153.6 MB data set streamed every epoch)"}
 
 
 def nccl_baseline(wk, world, rank, reps=20):
@@ -452,10 +456,12 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "resnet18-cifar10-shaped-50k, global batch 1024 (g=16, C=64)",
-                      "step": f"bounded sample: one aggregation step on {sample_rows} rows"},
+           "config": bench_config(args.gpus),
            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "oracle",
-                            "sample": f"{sample_rows} rows per step (oracle path + torch-CPU ResNet-18 fwd/bwd)"},
+                            "sample": f"bounded sample of the workload: each step = one aggregation step on "
+                                      f"{sample_rows} rows (oracle shard + gather, torch-CPU fp32 ResNet-18 "
+                                      f"fwd/bwd, oracle fp64 weighted average of P x 11,689,512 gradients, "
+                                      f"controller); samples/s = rows / step time"},
            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 

@@ -31,12 +31,12 @@ def timed(fn, reps):
     return a.elapsed_time(b) / reps * 1e3   # us
 
 
-def gather(rows, row_bytes, nsrc, reps, plane, impls=(1, 2), layout=0):
+def gather(rows, row_bytes, nsrc, reps, plane, impls=(1, 2), layout=0, seq=False):
     X = torch.randint(0, 256, (nsrc, row_bytes), dtype=torch.uint8, device="cuda")
     Y = torch.randint(0, 10, (nsrc,), dtype=torch.int64, device="cuda")
     # distinct rows, like a shard of the per-epoch permutation (sampling with replacement would let
     # repeated rows hit in L2 and flatter the kernel)
-    idx = torch.randperm(nsrc, device="cuda")[:rows] if rows <= nsrc else torch.randint(0, nsrc, (rows,), device="cuda")
+    idx = torch.arange(rows, device="cuda") if seq else torch.randperm(nsrc, device="cuda")[:rows] if rows <= nsrc else torch.randint(0, nsrc, (rows,), device="cuda")
     out = torch.empty((rows, row_bytes), dtype=torch.bfloat16, device="cuda")
     lab = torch.empty(rows, dtype=torch.int64, device="cuda")
     for impl in impls:
@@ -77,6 +77,8 @@ if __name__ == "__main__":
         gather(49152, 3072, 50000, reps, 1024, impls=(2, 1) if what == "all" else (2,), layout=1)
     if what == "gather_epoch_hwc_lsu":                 # exactly the bench's launch (channels-last, LSU)
         gather(49152, 3072, 50000, reps, 1024, impls=(1,), layout=1)
+    if what == "gather_epoch_hwc_lsu_seq":             # same bytes, rows in order: cost of the scatter
+        gather(49152, 3072, 50000, reps, 1024, impls=(1,), layout=1, seq=True)
     if what in ("gather_imagenet", "all"):
         gather(336, 150528, 2000, reps, 50176)
     if what in ("shard", "all"):
