@@ -499,3 +499,26 @@ class Worker:
         self.cfg.slowdown, self.cfg.slowdown_schedule = save, save_sched
         self.c0_ns = a.elapsed_time(b) * 1e6 / (steps * n_r)
         return self.c0_ns
+
+    # ---- checkpoint / resume -------------------------------------------------------------
+    # The method's state is the allocation (w, history, frozen, epoch: pr_alloc_save, POD bytes) plus the
+    # harness's epoch / step counters and last t_s; the permutation is a pure function of (seed, epoch),
+    # so a resumed run draws exactly the shards the uninterrupted run would have.  Model and optimizer
+    # state are torch state dicts.  Call between epochs (no prefetched epoch in flight).
+    def state_dict(self) -> dict:
+        torch.cuda.synchronize(self.dev)
+        return {"version": 1, "rank": self.rank, "P": self.P, "alloc": self.alloc.save(),
+                "epoch": self.epoch, "gstep": self.gstep, "last_ts": self.last_ts, "c0_ns": self.c0_ns,
+                "model": {k: v.detach().clone() for k, v in self.model.state_dict().items()},
+                "opt": self.opt.state_dict(), "history": list(self.history)}
+
+    def load_state_dict(self, sd: dict) -> None:
+        if sd.get("version") != 1 or sd["P"] != self.P or sd["rank"] != self.rank:
+            raise ValueError("checkpoint is for another job layout")
+        self.alloc = pr.Alloc.load(sd["alloc"])
+        self.epoch, self.gstep, self.last_ts, self.c0_ns = sd["epoch"], sd["gstep"], sd["last_ts"], sd["c0_ns"]
+        with torch.no_grad():
+            self.model.load_state_dict(sd["model"])
+        self.opt.load_state_dict(sd["opt"])
+        self.history = list(sd["history"])
+        self._prefetched = None

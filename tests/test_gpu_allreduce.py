@@ -103,6 +103,21 @@ def test_resnet18_size_sampled_parity_against_oracle():
     _check(P, 11_689_512, "f32", [64, 64, 64, 64, 128, 128, 256, 256], comms)
 
 
+def test_vgg16_size_C3_full_parity():
+    """Full-size C3 gradient (VGG-16, 138,357,544 fp32 = 553 MB per rank) at P=4 with the allocation C3
+    converges to (w = [11,11,21,21], g = 16): ring replay on every element + fp64 tolerance."""
+    P = 4
+    comms = group(P)
+    _check(P, 138_357_544, "f32", [16 * w for w in (11, 11, 21, 21)], comms)
+
+
+def test_resnet18_size_bf16_P8():
+    """C5's bf16 leg at the ResNet-18 size, skewed weights 1:1:1:1:2:2:4:4."""
+    P = 8
+    comms = group(P)
+    _check(P, 11_689_512, "bf16", [64, 64, 64, 64, 128, 128, 256, 256], comms, kind="mixed")
+
+
 def test_equal_weights_match_torch_mean():
     P, L = 4, 100_003
     comms = group(P)

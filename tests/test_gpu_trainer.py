@@ -81,3 +81,42 @@ def test_slowdown_schedule_lookup():
         w.gstep = s
         seen.append(w.sigma())
     assert seen == [2.0, 2.0, 3.0, 3.0, 1.5, 1.5]
+
+
+def test_checkpoint_resume_continues_the_same_run():
+    """resume from Worker.state_dict() between epochs = the uninterrupted run: same allocation
+    state and history length, same shards (π depends only on (seed, epoch)), same training up to cuDNN /
+    bf16 reassociation noise."""
+    import io
+
+    a = _worker()
+    for _ in range(2):
+        a.boundary()
+        a.run_epoch()
+    buf = io.BytesIO()
+    torch.save(a.state_dict(), buf)
+    alloc_epoch = a.alloc.view()["epoch"]
+    for _ in range(2):
+        a.boundary()
+        a.run_epoch()
+    b = _worker()
+    buf.seek(0)
+    b.load_state_dict(torch.load(buf, weights_only=False))
+    assert b.epoch == 2 and b.alloc.view()["epoch"] == alloc_epoch
+    for _ in range(2):
+        b.boundary()
+        b.run_epoch()
+    va, vb = a.alloc.view(), b.alloc.view()
+    assert (va["w"], va["epoch"], va["hist_len"], va["frozen"]) == (vb["w"], vb["epoch"], vb["hist_len"], vb["frozen"])
+    assert a.epoch == b.epoch == 4 and a.gstep == b.gstep
+    ia, ib = torch.empty_like(a.idx), torch.empty_like(b.idx)
+    pr.shard_indices(a.alloc, 0, a.epoch, a.cfg.seed, ia)
+    pr.shard_indices(b.alloc, 0, b.epoch, b.cfg.seed, ib)
+    assert torch.equal(ia, ib)
+    pa = torch.cat([p.detach().float().flatten() for p in a.model.parameters()])
+    pb = torch.cat([p.detach().float().flatten() for p in b.model.parameters()])
+    assert float((pa - pb).norm() / pa.norm()) < 1e-3
+    with pytest.raises(ValueError):
+        sd = a.state_dict()
+        sd["P"] = 2
+        b.load_state_dict(sd)
