@@ -201,6 +201,11 @@ def run_ours(args):
                    "peak_kind": peak_kind, "launches": len(g_ms), "avg_us": g_avg * 1e3,
                    "bytes_per_launch": g_bytes, "total_ms": sum(g_ms)}
     gather_roof["frac"] = gather_roof["achieved"] / hbm
+    mix = mix_ceiling()
+    if mix:
+        gather_roof["mix_ceiling"] = {"gbs": mix, "frac": gather_roof["achieved"] / mix,
+                                      "source": "tools/probes/widen_probe.cu: sequential stream with K2's 1:2 "
+                                                "read:write byte mix (profiles/round1_k2_mix_ceiling.txt)"}
     gather_roof["traffic"] = traffic_from_profiles("gather")
     roof = gather_roof
     allreduce = None
@@ -285,6 +290,17 @@ def run_ours(args):
         comm.destroy()
     if world > 1:
         dist.destroy_process_group()
+
+
+def mix_ceiling():
+    """Best GB/s of the sequential 1:2 read:write streaming probe (context for K2's roofline)."""
+    try:
+        import re
+        with open(os.path.join(ROOT, "profiles", "round1_k2_mix_ceiling.txt")) as f:
+            v = [float(m.group(1)) for m in re.finditer(r"widen .*?([0-9.]+) GB/s", f.read())]
+        return max(v) if v else None
+    except OSError:
+        return None
 
 
 def bench_config(world, overlap=False):
