@@ -52,7 +52,8 @@ def main():
     # K4
     pr.spin(10_000)
     # K3: local groups, both scopes, direct and staged, ragged counts
-    for flags in (dict(), dict(sys_scope=True), dict(force_staged=True)):
+    for flags in (dict(), dict(sys_scope=True), dict(force_staged=True), dict(algo=pr.ALGO_TWO_SHOT),
+                  dict(algo=pr.ALGO_LL), dict(algo=pr.ALGO_LL, sys_scope=True)):
         comms = pr.comm_init_local(3, 0, pr.comm_config(channels=2, slots=4, slot_bytes=4096, stages=2,
                                                         tile_bytes=2048, threads=64, **flags))
         for L in (5, 3001):
@@ -62,6 +63,13 @@ def main():
             torch.cuda.synchronize()
             assert all(c.status() == 0 for c in comms)
             assert np.array_equal(bufs[1].cpu().numpy(), OW.ring_emulate(g, [1, 0, 3], "f32"))
+            hb = OG.f32_to_bf16_bits(g)                     # bf16 leg (odd L: ragged last line / tail)
+            bb = [torch.from_numpy(hb[r].view(np.int16).copy()).cuda().view(torch.bfloat16) for r in range(3)]
+            pr.weighted_allreduce_local(comms, bb, [2, 5, 0])
+            torch.cuda.synchronize()
+            assert all(c.status() == 0 for c in comms)
+            assert np.array_equal(bb[0].view(torch.int16).cpu().numpy().view(np.uint16),
+                                  OW.ring_emulate(hb, [2, 5, 0], "bf16"))
         for c in comms:
             c.destroy()
     torch.cuda.synchronize()
