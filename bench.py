@@ -16,7 +16,8 @@ allocation; strong scaling across N.
 value   = whole-job samples/s over the K timed epochs (device time, CUDA events, max over ranks)
 e2e     = the same with the data set in pinned HOST memory: the gather reads every sampled row over
           PCIe inside the timed region, and every step's loss is read back to the host
-roofline= the library's dominant kernel in the timed region (K2 at N=1, K3 at N>1), achieved
+roofline= the library's dominant kernel in the timed region (by total live time: the fused SGD update
+          at N=1 — 48 launches per epoch — K3 at N>1; K2 and the others are reported beside it), achieved
           algorithmic bytes / live CUDA-event duration vs the measured peak
 cpu_baseline / --impl reference: the CPU oracle (oracle/) + a torch-CPU forward/backward on a bounded
           sample of one aggregation step, on the host cores.
@@ -165,6 +166,7 @@ def run_ours(args):
     wk.launches = 0
     wk.gather_events.clear()
     wk.ar_events.clear()
+    wk.sgd_events.clear()
     clocks = ClockSampler(local)
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -208,6 +210,18 @@ def run_ours(args):
                                                 "read:write byte mix (profiles/round1_k2_mix_ceiling.txt)"}
     gather_roof["traffic"] = traffic_from_profiles("gather")
     roof = gather_roof
+    sgd_roof = None
+    if wk.sgd_events:
+        u_ms = [a.elapsed_time(b) for a, b in wk.sgd_events]
+        u_avg = statistics.mean(u_ms)
+        u_bytes = 16.0 * wk.L                      # read θ, ḡ; write θ, ḡ = 0 (fp32)
+        sgd_roof = {"kernel": "sgd_kernel (a9: SGD + gradient reset, one launch per aggregation step)",
+                    "bound": "hbm", "achieved": u_bytes / (u_avg * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                    "peak_kind": peak_kind, "launches": len(u_ms), "avg_us": u_avg * 1e3,
+                    "bytes_per_launch": u_bytes, "total_ms": sum(u_ms), "traffic": traffic_from_profiles("sgd")}
+        sgd_roof["frac"] = sgd_roof["achieved"] / hbm
+        if sgd_roof["total_ms"] > roof["total_ms"]:
+            roof = sgd_roof
     allreduce = None
     if world > 1 and wk.ar_events:
         a_ms = [a.elapsed_time(b) for a, b in wk.ar_events]
@@ -218,7 +232,7 @@ def run_ours(args):
                      "unit": "GB/s", "peak_kind": "B200_PROFILING.md measured peer copy per direction",
                      "frac": bus / NVLINK_PEER_GBS, "avg_us": a_avg * 1e3, "bytes": Z, "launches": len(a_ms),
                      "frac_of_900_nominal": bus / 900.0, "total_ms": sum(a_ms), "traffic": None}
-        if allreduce["total_ms"] > gather_roof["total_ms"]:
+        if allreduce["total_ms"] > roof["total_ms"]:
             roof = allreduce
         if not shared:
             allreduce["nccl_baseline"] = nccl_baseline(wk, world, rank)
@@ -270,6 +284,7 @@ def run_ours(args):
             "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
             "roofline_detail": roof,
             "gather": gather_roof,
+            "sgd": sgd_roof,
             "allreduce": allreduce,
             "allreduce_colocated": colocated,
             "e2e": e2e,
@@ -281,6 +296,7 @@ def run_ours(args):
             # share of the timed region spent in each library kernel (live events; compare with the ncu
             # launch list of the same command in profiles/)
             "kernel_shares": {"gather_kernel": gather_roof["total_ms"] / ms,
+                              "sgd_kernel": (sgd_roof["total_ms"] / ms) if sgd_roof else 0.0,
                               "ring_kernel": (allreduce["total_ms"] / ms) if allreduce else 0.0},
         }
         if args.data_n != N_DATA:

@@ -180,6 +180,14 @@ int pr_spin(int64_t ns, void *stream);
  * Errors: PR_ERR_INVALID, PR_ERR_CUDA. */
 int pr_stamp(int64_t *d_ring, int64_t cap, void *stream);
 
+/* SGD update, §8(a) row a9: Eq. 1 with weight decay, applied to the reduced
+ * gradient, fused with the gradient reset for the next aggregation:
+ *   θ[i] ← fma(−lr, fma(wd, θ[i], g[i]), θ[i]);   if zero_grad: g[i] ← 0
+ * in fp32 (lr, wd rounded to fp32), each fma rounded once (RN).  d_theta, d_grad: device fp32 [n],
+ * 16-byte aligned, caller-owned; async on `stream`.  Errors: PR_ERR_INVALID (n < 0, null pointer),
+ * PR_ERR_ALIGN, PR_ERR_CUDA. */
+int pr_sgd_update(float *d_theta, float *d_grad, int64_t n, double lr, double wd, int32_t zero_grad, void *stream);
+
 /* =================================================================================================
  * 3. Weighted ring allreduce (K3) — §8(a) rows a6, a7, a8
  * ================================================================================================= */

@@ -221,6 +221,15 @@ def stamp(ring, stream=None):
     _check(LIB.pr_stamp(_ptr(ring), ring.numel() - 1, _stream(stream)), "pr_stamp")
 
 
+def sgd_update(theta, grad, lr: float, wd: float = 0.0, zero_grad: bool = True, stream=None):
+    """a9: θ ← θ − lr·(g + wd·θ) (two fp32 FMAs) and, if zero_grad, g ← 0 — one pass over flat fp32
+    buffers (Eq. 1; wd P:235)."""
+    if str(theta.dtype) != "torch.float32" or theta.dtype != grad.dtype or theta.numel() != grad.numel():
+        raise ValueError("theta and grad must be fp32 buffers of equal length")
+    _check(LIB.pr_sgd_update(_ptr(theta), _ptr(grad), theta.numel(), float(lr), float(wd), int(bool(zero_grad)),
+                             _stream(stream)), "pr_sgd_update")
+
+
 def test_philox(ctr, key: int, use_curand: bool, out, stream=None):
     n = ctr.numel() // 4
     _check(LIB.pr_test_philox(_ptr(ctr), n, key, 1 if use_curand else 0, _ptr(out), _stream(stream)),

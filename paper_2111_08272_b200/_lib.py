@@ -64,6 +64,7 @@ SIGNATURES = {
     "pr_gather_rows": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, ctypes.POINTER(GatherOp), c_vp, c_vp, c_vp]),
     "pr_spin": (ctypes.c_int, [c_i64, c_vp]),
     "pr_stamp": (ctypes.c_int, [c_vp, c_i64, c_vp]),
+    "pr_sgd_update": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_i32, c_vp]),
     "pr_comm_init": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, EXCHANGE_FN, c_vp,
                                     ctypes.POINTER(CommConfig)]),
     "pr_comm_init_local": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i32, c_i32, ctypes.POINTER(CommConfig)]),

@@ -20,7 +20,7 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpropring.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-CU_SOURCES = ["shard.cu", "gather.cu", "ring.cu"]
+CU_SOURCES = ["shard.cu", "gather.cu", "ring.cu", "update.cu"]
 CPP_SOURCES = ["alloc.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

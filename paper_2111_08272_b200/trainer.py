@@ -9,7 +9,9 @@ Rows of SURVEY §8(a) handled here (the rest are library calls):
       seconds per sample at σ = 1) slows rank r by the factor σ_r.
   a5  t_s capture: CUDA events around data movement + compute + spin, summed over the epoch (P:102,
       P:152; DESIGN.md §3 #4-#5); one event synchronisation per epoch, not per step.
-  a9  SGD update, Eq. 1 with weight decay: torch.optim.SGD on the reduced buffer.
+  a9  SGD update, Eq. 1 with weight decay: the library's fused pr_sgd_update over the
+      flat parameter / reduced-gradient buffers (also resets the gradient for the next aggregation);
+      fused_sgd=False uses torch.optim.SGD + a memset instead.
 Library rows: a1/a10 alloc_init / Alloc.update (+ pr_comm_allgather_f64 for the t_s exchange),
 a2 shard_indices, a3 gather_rows, a6-a8 weighted_allreduce.
 
@@ -70,6 +72,9 @@ class RunConfig:
     # Needs graphs=True (the overlapped step is one captured graph per n_r).
     overlap: bool = False
     bucket_mb: float = 8.0
+    # a9 through the library's fused kernel (pr_sgd_update: SGD + gradient reset in one pass over flat
+    # fp32 parameter / gradient buffers) instead of torch.optim.SGD + a separate memset
+    fused_sgd: bool = True
 
 
 def build_model(name: str, num_classes: int):
@@ -129,7 +134,19 @@ class Worker:
         for p in params:   # .grad = a view of the flat buffer with the parameter's own (channels-last) strides
             p.grad = self.flat[off:off + p.numel()].as_strided(p.shape, p.stride())
             off += p.numel()
-        self.opt = torch.optim.SGD(params, lr=cfg.lr, weight_decay=cfg.wd)
+        self.pflat = None
+        if cfg.fused_sgd:  # parameters become views of one flat fp32 buffer laid out like the gradient
+            self.pflat = torch.empty(self.L, dtype=torch.float32, device=self.dev)
+            off = 0
+            with torch.no_grad():
+                for p in params:
+                    v = self.pflat[off:off + p.numel()].as_strided(p.shape, p.stride())
+                    v.copy_(p.data)
+                    p.data = v
+                    off += p.numel()
+            self.opt = None
+        else:
+            self.opt = torch.optim.SGD(params, lr=cfg.lr, weight_decay=cfg.wd)
         self._overlap = bool(cfg.overlap and comm is not None and world > 1)
         if cfg.overlap and not cfg.graphs:
             raise ValueError("overlap=True needs graphs=True")
@@ -139,7 +156,7 @@ class Worker:
         self.xdt = torch.bfloat16 if cfg.bf16_compute else torch.float32
         self.c0_ns = 0.0                               # calibrated per-sample compute time (ns) at σ = 1
         self.launches = 0                              # library kernels launched (for the bench)
-        self.ar_events, self.gather_events = [], []
+        self.ar_events, self.gather_events, self.sgd_events = [], [], []
         self.epoch = 0
         self.last_ts = 0.0
         self.history = []
@@ -338,8 +355,18 @@ class Worker:
             if record:
                 a1.record(self.stream)
                 self.ar_events.append((a0, a1))
-        self.opt.step()
-        self.flat.zero_()
+        if self.pflat is not None:
+            if record:
+                u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                u0.record(self.stream)
+            pr.sgd_update(self.pflat, self.flat, self.cfg.lr, self.cfg.wd, zero_grad=True, stream=self.stream)
+            self.launches += 1
+            if record:
+                u1.record(self.stream)
+                self.sgd_events.append((u0, u1))
+        else:
+            self.opt.step()
+            self.flat.zero_()
 
     def _compute_time(self, ev) -> float:
         """Σ over the recorded steps of this rank's compute time in seconds (a5).  With N1 the step's CUDA
@@ -510,7 +537,7 @@ class Worker:
         return {"version": 1, "rank": self.rank, "P": self.P, "alloc": self.alloc.save(),
                 "epoch": self.epoch, "gstep": self.gstep, "last_ts": self.last_ts, "c0_ns": self.c0_ns,
                 "model": {k: v.detach().clone() for k, v in self.model.state_dict().items()},
-                "opt": self.opt.state_dict(), "history": list(self.history)}
+                "opt": self.opt.state_dict() if self.opt is not None else None, "history": list(self.history)}
 
     def load_state_dict(self, sd: dict) -> None:
         if sd.get("version") != 1 or sd["P"] != self.P or sd["rank"] != self.rank:
@@ -519,6 +546,7 @@ class Worker:
         self.epoch, self.gstep, self.last_ts, self.c0_ns = sd["epoch"], sd["gstep"], sd["last_ts"], sd["c0_ns"]
         with torch.no_grad():
             self.model.load_state_dict(sd["model"])
-        self.opt.load_state_dict(sd["opt"])
+        if self.opt is not None and sd["opt"] is not None:
+            self.opt.load_state_dict(sd["opt"])
         self.history = list(sd["history"])
         self._prefetched = None

@@ -290,3 +290,48 @@ def test_stamp_ring_orders_and_wraps():
     assert s3 - s2 >= 20_000 and s4 - s3 >= 20_000 and s5 - s4 >= 20_000
     with pytest.raises(pr.PropringError):
         pr.stamp(torch.zeros(1, dtype=torch.int64, device="cuda"))
+
+
+# ---- a9: fused SGD update (Eq. 1, wd P:235) ----------------------------------------------------------
+
+def _sgd_ref(theta, g, lr, wd):
+    """Oracle O7's sgd_step in fp64 on the fp32 inputs with lr, wd rounded to fp32 (the kernel's definition)."""
+    from oracle import linmodel as LM
+
+    return LM.sgd_step(theta.astype(np.float64), g.astype(np.float64), float(np.float32(lr)), float(np.float32(wd)))
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 1000, 4099, 11_689_512])
+def test_sgd_update_within_one_rounding_of_oracle(n):
+    rng = np.random.Generator(np.random.PCG64(n))
+    theta = (rng.standard_normal(n) * np.exp(rng.standard_normal(n))).astype(np.float32)
+    g = (rng.standard_normal(n) * np.exp(2 * rng.standard_normal(n))).astype(np.float32)
+    lr, wd = 1e-2, 1e-4                                   # P:235, P:239
+    dt, dg = torch.from_numpy(theta).cuda(), torch.from_numpy(g).cuda()
+    pr.sgd_update(dt, dg, lr, wd, zero_grad=True)
+    torch.cuda.synchronize()
+    out = dt.cpu().numpy().astype(np.float64)
+    ref = _sgd_ref(theta, g, lr, wd)
+    # two roundings: |err| <= u·|θ'| + lr·u·|g + wd·θ| (u = 2^-24), plus slack for the fp32 lr/wd
+    bound = 2.0 ** -24 * (np.abs(ref) + np.float32(lr) * np.abs(g.astype(np.float64) + np.float32(wd) * theta)) * 1.01
+    assert np.all(np.abs(out - ref) <= bound + 1e-45)
+    assert torch.count_nonzero(dg) == 0
+    # library routine: torch.optim.SGD on the same values, within the same bound
+    p = torch.nn.Parameter(torch.from_numpy(theta).cuda())
+    p.grad = torch.from_numpy(g).cuda()
+    torch.optim.SGD([p], lr=lr, weight_decay=wd).step()
+    assert np.all(np.abs(p.detach().cpu().numpy().astype(np.float64) - out) <= 2 * bound + 1e-45)
+
+
+def test_sgd_update_keep_grad_and_errors():
+    theta = torch.randn(1001, device="cuda")
+    g = torch.randn(1001, device="cuda")
+    g0 = g.clone()
+    pr.sgd_update(theta, g, 0.1, 0.0, zero_grad=False)
+    assert torch.equal(g, g0)
+    pr.sgd_update(theta[:0], g[:0], 0.1)                  # n = 0: no launch
+    with pytest.raises(pr.PropringError) as e:
+        pr.sgd_update(theta[1:], g[1:], 0.1)             # 4-byte offset: not 16-byte aligned
+    assert e.value.code == pr.PR_ERR_ALIGN
+    with pytest.raises(ValueError):
+        pr.sgd_update(theta.double(), g.double(), 0.1)

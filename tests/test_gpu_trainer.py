@@ -120,3 +120,19 @@ def test_checkpoint_resume_continues_the_same_run():
         sd = a.state_dict()
         sd["P"] = 2
         b.load_state_dict(sd)
+
+
+def test_fused_sgd_matches_torch_sgd_training():
+    """a9 through pr_sgd_update (flat parameter views) trains like torch.optim.SGD + memset."""
+    a = _worker(fused_sgd=True)
+    b = _worker(fused_sgd=False)
+    for _ in range(2):
+        ra, rb = a.run_epoch(), b.run_epoch()
+        assert abs(ra["loss"] - rb["loss"]) <= 2e-2 * abs(rb["loss"])
+    pa = torch.cat([p.detach().float().flatten() for p in a.model.parameters()])
+    pb = torch.cat([p.detach().float().flatten() for p in b.model.parameters()])
+    assert float((pa - pb).norm() / pb.norm()) < 1e-3
+    # the parameters really are views of the flat buffer the kernel updates
+    p0 = next(a.model.parameters())
+    assert p0.untyped_storage().data_ptr() == a.pflat.untyped_storage().data_ptr()
+    assert torch.count_nonzero(a.flat) == 0               # gradient reset fused into the update

@@ -55,6 +55,13 @@ def shard(reps):
     print(f"permute N={N}: {us:.2f} us, {N / us:.1f} M indices/s")
 
 
+def sgd(reps, L=11_689_512):
+    th = torch.randn(L, device="cuda")
+    g = torch.randn(L, device="cuda")
+    us = timed(lambda: pr.sgd_update(th, g, 1e-2, 1e-4, zero_grad=True), reps)
+    print(f"sgd L={L}: {us:.2f} us, {16 * L / us / 1e3:.1f} GB/s algorithmic")
+
+
 def ring(reps, P=8, L=11_689_512):
     comms = pr.comm_init_local(P, 0, pr.comm_config())
     bufs = [torch.randn(L, device="cuda") for _ in range(P)]
@@ -83,5 +90,7 @@ if __name__ == "__main__":
         gather(336, 150528, 2000, reps, 50176)
     if what in ("shard", "all"):
         shard(reps)
+    if what in ("sgd", "all"):
+        sgd(reps)
     if what in ("ring", "all"):
         ring(reps)

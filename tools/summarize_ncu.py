@@ -87,7 +87,8 @@ def main():
             if st:
                 lines.append("| top stall reasons (cycles/instr) | " + ", ".join(f"{n} {x:.1f}" for x, n in st) + " |")
             lines.append("")
-            kind = ("gather" if "gather" in kname else "ring_ll" if "ring_ll" in kname else
+            kind = ("gather" if "gather" in kname else "sgd" if "sgd_kernel" in kname else
+                    "ring_ll" if "ring_ll" in kname else
                     "twoshot" if "twoshot" in kname else "ring_colocated" if "ring" in kname else
                     "permute" if "permute" in kname else name)
             if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d:
@@ -113,7 +114,8 @@ def main():
             per[k][0] += 1
             per[k][1] += t
             total += t
-        mine = ("gather_tma_kernel", "gather_kernel", "permute_kernel", "ring_kernel", "spin_kernel", "allgather_f64")
+        mine = ("gather_tma_kernel", "gather_kernel", "permute_kernel", "ring_kernel", "ring_ll_kernel", "twoshot_kernel",
+                "sgd_kernel", "spin_kernel", "stamp_kernel", "allgather_f64")
         lines += ["## Launch list of the bench command (`ncu --metrics gpu__time_duration.sum`)", "",
                   f"Total kernel time {total / 1e3:.2f} ms over {sum(v[0] for v in per.values())} launches "
                   "(cold-cache, serialised: compare shares, not absolutes).", "",
