@@ -216,6 +216,8 @@ typedef struct {
     int64_t ts_max_bytes; /* PR_ALGO_AUTO: two-shot for buffers up to this many bytes (default 4 MiB)  */
     int64_t ll_max_bytes; /* largest buffer the LL ring handles (PR_ALGO_LL; PR_ALGO_AUTO picks it up to
                              here); sizes the LL regions of the window, <= 64 MiB (default 256 KiB)  */
+    int64_t os_max_bytes; /* largest buffer the one-shot LL path handles (PR_ALGO_ONESHOT; PR_ALGO_AUTO
+                             picks it up to here), <= 16 MiB (default 64 KiB)                         */
 } pr_comm_config;
 
 /* Allreduce algorithm.  Both compute the same bits (the two-shot reducer adds the contributions in the
@@ -225,13 +227,19 @@ typedef struct {
  * buffer registered (else PR_ERR_INVALID is latched on all ranks). */
 #define PR_ALGO_RING     0
 #define PR_ALGO_TWO_SHOT 1
-#define PR_ALGO_AUTO     2   /* LL ring up to ll_max_bytes, two-shot up to ts_max_bytes, ring above */
+#define PR_ALGO_AUTO     2   /* one-shot up to os_max_bytes, LL ring up to ll_max_bytes, two-shot up to
+                                 ts_max_bytes, ring above */
 /* LL ring: the ring's schedule, order and rounding (same bits) with a low-latency line protocol — every
  * 16-byte line pushed to the next rank carries 8 payload bytes and the call's sequence number in both
  * 64-bit halves, so the receiver polls the data itself (no fence / flag / credit round trip per hop).
  * Half the bandwidth of the ring, a fraction of its per-hop latency: for buffers <= ll_max_bytes
  * (larger buffers given PR_ALGO_LL take the ring).  Works with unregistered buffers. */
 #define PR_ALGO_LL       3
+/* One-shot LL: one hop — every rank pushes its raw buffer as LL lines to every peer and reduces all P
+ * contributions itself, per element in the ring's order for that element's chunk with the ring's
+ * per-hop rounding (same bits).  (P−1)·2·Z bytes sent per rank: for buffers <= os_max_bytes (larger
+ * buffers given PR_ALGO_ONESHOT take the ring).  Works with unregistered buffers. */
+#define PR_ALGO_ONESHOT  4
 
 /* Byte allgather supplied by the caller (e.g. over a torch process group): every rank passes `len`
  * bytes in `send` and receives the P·len bytes of all ranks, rank-ordered, in `recv`.  Returns 0 on

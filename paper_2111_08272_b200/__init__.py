@@ -247,19 +247,23 @@ ALGO_RING = 0
 ALGO_TWO_SHOT = 1
 ALGO_AUTO = 2
 ALGO_LL = 3
+ALGO_ONESHOT = 4
 
 
 def comm_config(channels=16, slots=8, threads=512, slot_bytes=256 * 1024, watchdog_ns=10_000_000_000,
                 force_staged=False, stages=6, tile_bytes=16384, sys_scope=False, algo=ALGO_RING, ts_slots=2,
-                ts_slot_bytes=64 * 1024, ts_max_bytes=4 << 20, ll_max_bytes=256 * 1024):
+                ts_slot_bytes=64 * 1024, ts_max_bytes=4 << 20, ll_max_bytes=256 * 1024,
+                os_max_bytes=64 * 1024):
     """K3 launch/pipeline configuration; the defaults are the best of tools/sweep_ring.py on B200.
     sys_scope=True forces system-scope synchronisation even when all ranks share one GPU (tests).
     algo: ALGO_RING (the paper's ring), ALGO_LL (the ring with the low-latency line protocol, buffers up to
-    ll_max_bytes), ALGO_TWO_SHOT, or ALGO_AUTO (LL up to ll_max_bytes, two-shot up to ts_max_bytes, ring above)."""
+    ll_max_bytes), ALGO_ONESHOT (one hop, buffers up to os_max_bytes), ALGO_TWO_SHOT, or ALGO_AUTO (one-shot up
+    to os_max_bytes, LL up to ll_max_bytes, two-shot up to ts_max_bytes, ring above)."""
     flags = (COMM_FLAG_FORCE_STAGED if force_staged else 0) | (COMM_FLAG_SYS_SCOPE if sys_scope else 0)
     return CommConfig(channels=channels, slots=slots, threads=threads, flags=flags, slot_bytes=slot_bytes,
                       watchdog_ns=watchdog_ns, stages=stages, tile_bytes=tile_bytes, algo=algo, ts_slots=ts_slots,
-                      ts_slot_bytes=ts_slot_bytes, ts_max_bytes=ts_max_bytes, ll_max_bytes=ll_max_bytes)
+                      ts_slot_bytes=ts_slot_bytes, ts_max_bytes=ts_max_bytes, ll_max_bytes=ll_max_bytes,
+                      os_max_bytes=os_max_bytes)
 
 
 class _DeviceBuffer:

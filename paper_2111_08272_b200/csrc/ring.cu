@@ -77,6 +77,8 @@ struct DevTable {
     int64_t ts_slot_bytes;
     uint64_t off_ll;                // LL ring: [channels][2P−2 phases][ll_region_bytes]
     int64_t ll_region_bytes;        // 16-byte lines, 8 payload bytes each, for one channel's share of a chunk
+    uint64_t off_os;                // one-shot LL: [channels][P sources][os_region_bytes]
+    int64_t os_region_bytes;        // LL lines for one channel's share of the whole buffer
     volatile int* status;           // host-mapped
     volatile long long* stamps;     // host-mapped [3]
     uint8_t* win[PR_MAX_RANKS];
@@ -118,6 +120,8 @@ void layout(DevTable& t) {
     o += (uint64_t)t.channels * t.P * t.ts_slots * (uint64_t)t.ts_slot_bytes;
     t.off_ll = o = align_up(o, 4096);
     o += (uint64_t)t.channels * (uint64_t)(t.P > 1 ? 2 * t.P - 2 : 0) * (uint64_t)t.ll_region_bytes;
+    t.off_os = o = align_up(o, 4096);
+    o += (uint64_t)t.channels * (uint64_t)t.P * (uint64_t)t.os_region_bytes;
     t.window_bytes = align_up(o, 4096);
 }
 
@@ -1023,6 +1027,122 @@ __global__ void __launch_bounds__(512, 1) ring_ll_kernel(const __grid_constant__
     if (t0 && ch == 0) tab->stamps[2] = (long long)gtimer();
 }
 
+// =====================================================================================================
+// One-shot LL (tiny buffers): ONE hop.  Every rank pushes its raw buffer, as LL lines, into a per-source
+// region of every peer's window; every rank then reduces all P contributions itself — per element in the
+// ring's order for that element's chunk c (c, c+1, …, c+P−1) with the ring's per-hop rounding, exactly as
+// the two-shot reducer — so all ranks compute the ring's bits without a second hop.  Traffic per rank is
+// (P−1)·2·Z bytes, so this is for buffers of a few tens of KiB, where the ring's 2P−2 hops are all latency.
+// =====================================================================================================
+template <typename T>
+__global__ void __launch_bounds__(512, 1) oneshot_ll_kernel(const __grid_constant__ LaunchArgs A) {
+    __shared__ int s_err;
+    __shared__ long long s_n[PR_MAX_RANKS];
+    __shared__ float s_w[PR_MAX_RANKS];
+    __shared__ unsigned s_flag;
+    const RankCall& rc = A.calls[blockIdx.y];
+    const DevTable* tab = rc.tab;
+    const int ch = blockIdx.x;
+    const int r = tab->rank, P = tab->P;
+    uint8_t* my = tab->win[r];
+    ChanState* st = state_of(my, tab, ch);
+    const bool t0 = threadIdx.x == 0;
+    const bool sys = tab->sysscope != 0;
+    unsigned long long deadline = ~0ull;
+    if (threadIdx.x < 32) {
+        const unsigned long long start = gtimer();
+        if (t0 && ch == 0) tab->stamps[0] = (long long)start;
+        if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
+        const HsOut hs = handshake(A, rc, tab, st, ch, sys, deadline, s_n, nullptr);
+        __syncwarp();
+        for (int q = (int)threadIdx.x; q < P; q += 32)
+            s_w[q] = hs.sumn > 0 ? (float)((double)s_n[q] / (double)hs.sumn) : 0.0f;
+        if (t0) {
+            s_err = hs.err;
+            s_flag = (unsigned)(st->seq & 0xffffffffull);
+            if (ch == 0) tab->stamps[1] = (long long)gtimer();
+        }
+    }
+    __syncthreads();
+    if (s_err) {
+        if (t0) latch(tab, s_err);
+        return;
+    }
+    if (tab->watchdog_ns > 0) deadline = gtimer() + (unsigned long long)tab->watchdog_ns;
+    constexpr int V = Vec<T>::V;
+    constexpr int E = 8 / (int)sizeof(T);
+    const int64_t count = A.count;
+    const int64_t per = (count + P - 1) / P;
+    const int64_t cs = (per + V - 1) / V * V;                      // the ring's chunk (sets the order)
+    const int64_t subp = (count + tab->channels - 1) / tab->channels;
+    const int64_t sub = (subp + V - 1) / V * V;                   // this channel's share of the buffer
+    const int64_t lo = min((int64_t)ch * sub, count);
+    const int64_t len = min(lo + sub, count) - lo;
+    const int64_t nl = (len + E - 1) / E;
+    const uint32_t flag = s_flag;
+    T* buf = reinterpret_cast<T*>(rc.buf);
+    const size_t reg = (size_t)tab->os_region_bytes;
+    // push: my raw lines -> region [ch][src = r] of every peer
+    for (int64_t j = threadIdx.x; j < nl; j += blockDim.x) {
+        const int nv = (int)min((int64_t)E, len - j * E);
+        uint32_t w0 = 0, w1 = 0;
+        ld_line<T>(buf + lo + j * E, nv, w0, w1);
+        for (int k = 1; k < P; ++k) {
+            const int q = (r + k) % P;
+            uint8_t* dst = tab->win[q] + tab->off_os + ((size_t)ch * P + r) * reg + (size_t)j * 16;
+            st_ll(dst, w0, w1, flag, sys);
+        }
+    }
+    // reduce: every element in its chunk's ring order, the ring's rounding (as twoshot_kernel)
+    bool bad = false;
+    for (int64_t j = threadIdx.x; j < nl && !bad; j += blockDim.x) {
+        const int nv = (int)min((int64_t)E, len - j * E);
+        const int64_t e0 = lo + j * E;
+        const int c = (int)(e0 / cs);                              // a line never straddles a chunk
+        float acc[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) acc[k] = 0.0f;
+        for (int h = 0; h < P; ++h) {
+            const int q = (c + h) % P;
+            if (s_n[q] <= 0) continue;                             // n_q = 0 contributes nothing
+            uint32_t w0, w1;
+            if (q == r) {
+                ld_line<T>(buf + e0, nv, w0, w1);
+            } else {
+                const uint8_t* src = my + tab->off_os + ((size_t)ch * P + q) * reg + (size_t)j * 16;
+                unsigned long long a, b;
+                for (;;) {
+                    ld_line64(src, a, b, sys);
+                    if ((uint32_t)(a >> 32) == flag && (uint32_t)(b >> 32) == flag) break;
+                    if (gtimer() > deadline) { bad = true; break; }
+                }
+                if (bad) break;
+                w0 = (uint32_t)a;
+                w1 = (uint32_t)b;
+            }
+            const uint4 xv = make_uint4(w0, w1, 0u, 0u);
+            const float sq = s_w[q];
+#pragma unroll
+            for (int k = 0; k < E; ++k)
+                acc[k] = rnd_dtype<T>(h == 0 ? __fmul_rn(sq, lane_f<T>(xv, k)) : __fmaf_rn(sq, lane_f<T>(xv, k), acc[k]));
+        }
+        if (bad) break;
+        uint32_t y0, y1;
+        if (sizeof(T) == 4) {
+            y0 = __float_as_uint(acc[0]);
+            y1 = __float_as_uint(acc[1 % E]);
+        } else {
+            y0 = Vec<__nv_bfloat16>::pack(acc[0], acc[1 % E]);
+            y1 = Vec<__nv_bfloat16>::pack(acc[2 % E], acc[3 % E]);
+        }
+        // own gradient line j was read above by this same thread (push and reduce): safe to overwrite
+        st_line<T>(buf + e0, nv, y0, y1);
+    }
+    if (bad) latch(tab, PR_ERR_PEER_TIMEOUT);
+    __syncthreads();
+    if (t0 && ch == 0) tab->stamps[2] = (long long)gtimer();
+}
+
 __global__ void allgather_f64_kernel(const DevTable* tab, unsigned long long seq, double v, double* out) {
     if (threadIdx.x != 0) return;
     const bool sys = tab->sysscope != 0;
@@ -1061,7 +1181,7 @@ struct Reg {
 struct Hello {
     cudaIpcMemHandle_t handle;
     int32_t P, rank, device, channels, slots, threads, stages, tile_bytes, algo, ts_slots;
-    int64_t ts_slot_bytes, ts_max_bytes, ll_max_bytes;
+    int64_t ts_slot_bytes, ts_max_bytes, ll_max_bytes, os_max_bytes;
     int64_t slot_bytes, window_bytes;
     uint64_t bytes;   // registration size
     unsigned char uuid[16];   // device identity: peers on another GPU need .sys-scope synchronisation
@@ -1107,6 +1227,7 @@ pr_comm_config default_config() {
     c.ts_slot_bytes = 64 * 1024;
     c.ts_max_bytes = 4ll << 20;     // measured crossover (co-located P = 4, 8): two-shot wins up to ~4 MiB
     c.ll_max_bytes = 256 * 1024;
+    c.os_max_bytes = 64 * 1024;
     return c;
 }
 
@@ -1114,8 +1235,8 @@ int check_config(const pr_comm_config& c) {
     if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
-        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_LL ||
-        c.ll_max_bytes < 0 || c.ll_max_bytes > (64ll << 20) ||
+        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_ONESHOT ||
+        c.ll_max_bytes < 0 || c.ll_max_bytes > (64ll << 20) || c.os_max_bytes < 0 || c.os_max_bytes > (16ll << 20) ||
         c.ts_slots < 2 || c.ts_slots > 16 || c.ts_slot_bytes < 256 || c.ts_slot_bytes % 256 ||
         c.ts_slot_bytes > (16ll << 20) || c.ts_max_bytes < 0)
         return PR_ERR_INVALID;
@@ -1124,6 +1245,12 @@ int check_config(const pr_comm_config& c) {
 
 // Bytes of one LL region: 2 × (one channel's share of a chunk of the largest LL buffer), for either dtype
 // (chunk and share are rounded up to 16 bytes exactly as the kernels round them in elements).
+// Bytes of one one-shot region: 2 × (one channel's share of the largest one-shot buffer).
+uint64_t os_region_bytes(const pr_comm_config& c, int P) {
+    if (P < 2 || c.os_max_bytes <= 0) return 0;
+    return 2 * align_up(((uint64_t)c.os_max_bytes + c.channels - 1) / c.channels, 16);
+}
+
 uint64_t ll_region_bytes(const pr_comm_config& c, int P) {
     if (P < 2 || c.ll_max_bytes <= 0) return 0;
     const uint64_t per = ((uint64_t)c.ll_max_bytes + P - 1) / P;
@@ -1146,6 +1273,7 @@ int alloc_common(pr_comm* c) {
     t.ts_slots = c->cfg.ts_slots;
     t.ts_slot_bytes = c->cfg.ts_slot_bytes;
     t.ll_region_bytes = (int64_t)ll_region_bytes(c->cfg, c->P);
+    t.os_region_bytes = (int64_t)os_region_bytes(c->cfg, c->P);
     layout(t);
     PR_CUDA_TRY(cudaMalloc((void**)&c->win, t.window_bytes));
     PR_CUDA_TRY(cudaMemset(c->win, 0, t.window_bytes));
@@ -1219,6 +1347,17 @@ int launch_ring(const LaunchArgs& a, int nranks, const pr_comm_config& cfg, cuda
     const int32_t threads = cfg.threads, channels = cfg.channels;
     // algorithm: a pure function of (config, count, dtype), identical on every rank
     const int64_t bytes = a.count * (a.dtype == PR_DTYPE_F32 ? 4 : 2);
+    if ((cfg.algo == PR_ALGO_ONESHOT || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.os_max_bytes) {
+        void* fn4 = (a.dtype == PR_DTYPE_F32) ? (void*)oneshot_ll_kernel<float> : (void*)oneshot_ll_kernel<__nv_bfloat16>;
+        void* args4[] = {(void*)&a};
+        const dim3 grid4((unsigned)channels, (unsigned)nranks), block4((unsigned)threads);
+        if (coop) {
+            PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn4, grid4, block4, args4, 0, s));
+        } else {
+            PR_CUDA_TRY(cudaLaunchKernel(fn4, grid4, block4, args4, 0, s));
+        }
+        return PR_OK;
+    }
     if ((cfg.algo == PR_ALGO_LL || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.ll_max_bytes) {
         void* fn3 = (a.dtype == PR_DTYPE_F32) ? (void*)ring_ll_kernel<float> : (void*)ring_ll_kernel<__nv_bfloat16>;
         void* args3[] = {(void*)&a};
@@ -1283,6 +1422,7 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
     me.algo = c->cfg.algo; me.ts_slots = c->cfg.ts_slots; me.ts_slot_bytes = c->cfg.ts_slot_bytes;
     me.ts_max_bytes = c->cfg.ts_max_bytes;
     me.ll_max_bytes = c->cfg.ll_max_bytes;
+    me.os_max_bytes = c->cfg.os_max_bytes;
     {
         cudaDeviceProp prop;
         if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) std::memcpy(me.uuid, &prop.uuid, 16);
@@ -1297,7 +1437,7 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
         if (h.P != P || h.rank != q || h.channels != me.channels || h.slots != me.slots || h.slot_bytes != me.slot_bytes ||
             h.threads != me.threads || h.stages != me.stages || h.tile_bytes != me.tile_bytes || h.algo != me.algo ||
             h.ts_slots != me.ts_slots || h.ts_slot_bytes != me.ts_slot_bytes || h.ts_max_bytes != me.ts_max_bytes ||
-            h.ll_max_bytes != me.ll_max_bytes)
+            h.ll_max_bytes != me.ll_max_bytes || h.os_max_bytes != me.os_max_bytes)
             rc = rc ? rc : PR_ERR_INVALID;
     }
     if (rc) { free_comm(c); return rc; }

@@ -341,10 +341,14 @@ def test_two_shot_graph_replay():
 
 # ---- LL ring: the ring's schedule and rounding with a low-latency line protocol (same bits) ------------
 
+LL_ALGOS = {"ll": dict(algo=pr.ALGO_LL, ll_max_bytes=1 << 20), "oneshot": dict(algo=pr.ALGO_ONESHOT, os_max_bytes=1 << 20)}
+
+
+@pytest.mark.parametrize("algo", ["ll", "oneshot"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("P", [2, 3, 4, 5, 8])
-def test_ll_ring_bit_identical_to_ring_replay(P, dtype):
-    comms = group(P, algo=pr.ALGO_LL, ll_max_bytes=1 << 20)
+def test_ll_ring_bit_identical_to_ring_replay(P, dtype, algo):
+    comms = group(P, **LL_ALGOS[algo])
     rng = np.random.Generator(np.random.PCG64(200 + P))
     for L in (1, 2, 3, 5, 7, P + 1, 1000, 4099, 65_537, 2 ** 18 - 1):   # ragged last lines (fp32 1/2, bf16 1..4)
         n = [int(x) * 16 for x in rng.integers(1, 9, P)]
@@ -353,27 +357,30 @@ def test_ll_ring_bit_identical_to_ring_replay(P, dtype):
         _check(P, L, dtype, n, comms, kind="mixed" if L % 3 == 0 else "gaussian", seed=L)
 
 
-def test_ll_ring_many_calls_reuse_regions_and_sys_scope():
+@pytest.mark.parametrize("algo", ["ll", "oneshot"])
+def test_ll_ring_many_calls_reuse_regions_and_sys_scope(algo):
     """The line flag is the call's handshake sequence: back-to-back calls rewrite the same regions, and a
     stale line from the previous call must never pass (the results would then differ from the replay)."""
     for cfg in (dict(channels=3), dict(channels=16, sys_scope=True), dict(channels=1, threads=64)):
         P = 4
-        comms = group(P, algo=pr.ALGO_LL, **cfg)
+        comms = group(P, **LL_ALGOS[algo], **cfg)
         for it in range(12):
             L = [999, 65_536, 3, 40_001][it % 4]
             _check(P, L, "f32" if it % 3 else "bf16", [it % 5, 2, 3, 1 + it], comms, seed=100 + it)
 
 
-def test_ll_ring_above_ll_max_takes_the_ring():
+@pytest.mark.parametrize("cfg", [dict(algo=pr.ALGO_LL, ll_max_bytes=4096), dict(algo=pr.ALGO_ONESHOT, os_max_bytes=4096)])
+def test_ll_ring_above_ll_max_takes_the_ring(cfg):
     P = 3
-    comms = group(P, algo=pr.ALGO_LL, ll_max_bytes=4096)
+    comms = group(P, **cfg)
     for L in (1000, 1025, 300_000):        # 4,000 B (LL), 4,100 B and 1.2 MB (ring)
         _check(P, L, "f32", [1, 2, 3], comms, seed=L)
 
 
-def test_ll_ring_graph_replay():
+@pytest.mark.parametrize("algo", ["ll", "oneshot"])
+def test_ll_ring_graph_replay(algo):
     P, L = 3, 40_000
-    comms = group(P, algo=pr.ALGO_LL)
+    comms = group(P, **LL_ALGOS[algo])
     host, dev = _inputs(P, L, "f32", seed=31)
     src = [d.clone() for d in dev]
     n = [3, 0, 2]
@@ -393,9 +400,10 @@ def test_ll_ring_graph_replay():
         assert all(np.array_equal(d.cpu().numpy(), emu) for d in dev)
 
 
-def test_ll_ring_length_mismatch_and_timeout_latch():
+@pytest.mark.parametrize("algo", [pr.ALGO_LL, pr.ALGO_ONESHOT])
+def test_ll_ring_length_mismatch_and_timeout_latch(algo):
     P = 2
-    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, algo=pr.ALGO_LL, watchdog_ns=1_000_000_000))
+    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, algo=algo, watchdog_ns=1_000_000_000))
     a = torch.randn(1000, device="cuda")
     b = torch.randn(1000, device="cuda")
     a0, b0 = a.clone(), b.clone()
@@ -408,7 +416,7 @@ def test_ll_ring_length_mismatch_and_timeout_latch():
     assert torch.equal(a, a0) and torch.equal(b, b0)
     for c in comms:
         c.destroy()
-    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, algo=pr.ALGO_LL, watchdog_ns=300_000_000))
+    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, algo=algo, watchdog_ns=300_000_000))
     pr.weighted_allreduce(comms[0], a, 1, stream=s0)
     torch.cuda.synchronize()
     assert comms[0].status() == pr.PR_ERR_PEER_TIMEOUT

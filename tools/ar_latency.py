@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--algos", default="ring,two_shot,ll")
     ap.add_argument("--channels", type=int, default=16)
     ap.add_argument("--ll-max", type=int, default=16 << 20)
+    ap.add_argument("--os-max", type=int, default=4 << 20)
     ap.add_argument("--slots", type=int, default=8)
     ap.add_argument("--slot-bytes", type=int, default=256 * 1024)
     a = ap.parse_args()
@@ -38,9 +39,11 @@ def main():
     n = [64 * (1 + (r % 4)) for r in range(P)]
     sizes = [int(s) for s in a.sizes.split(",")]
     for algo_name in a.algos.split(","):
-        algo = {"ring": pr.ALGO_RING, "two_shot": pr.ALGO_TWO_SHOT, "ll": pr.ALGO_LL}[algo_name]
+        algo = {"ring": pr.ALGO_RING, "two_shot": pr.ALGO_TWO_SHOT, "ll": pr.ALGO_LL, "oneshot": pr.ALGO_ONESHOT,
+                "auto": pr.ALGO_AUTO}[algo_name]
         comms = pr.comm_init_local(P, 0, pr.comm_config(algo=algo, sys_scope=a.sys, channels=a.channels,
-                                                         ll_max_bytes=a.ll_max, slots=a.slots,
+                                                         ll_max_bytes=a.ll_max, os_max_bytes=a.os_max,
+                                                         slots=a.slots,
                                                          slot_bytes=a.slot_bytes))
         zmax = max(sizes)
         if a.staged:
