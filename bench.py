@@ -228,7 +228,9 @@ def run_ours(args):
         a_avg = statistics.mean(a_ms)
         Z = wk.L * 4
         bus = Z * 2 * (world - 1) / world / (a_avg * 1e-3) / 1e9
-        allreduce = {"kernel": "ring_kernel<float> (K3)", "bound": "nvlink", "achieved": bus, "peak": NVLINK_PEER_GBS,
+        kname = ("ring_kernel<float> (K3 with K7 fused: weighted allreduce + SGD + gradient reset)"
+                 if getattr(wk, "pflat", None) is not None and not wk._overlap else "ring_kernel<float> (K3)")
+        allreduce = {"kernel": kname, "bound": "nvlink", "achieved": bus, "peak": NVLINK_PEER_GBS,
                      "unit": "GB/s", "peak_kind": "B200_PROFILING.md measured peer copy per direction",
                      "frac": bus / NVLINK_PEER_GBS, "avg_us": a_avg * 1e3, "bytes": Z, "launches": len(a_ms),
                      "frac_of_900_nominal": bus / 900.0, "total_ms": sum(a_ms), "traffic": None}

@@ -129,8 +129,11 @@ def run_virtual(args):
                 ar[j][0].record()
                 pr.weighted_allreduce_local(comms, bufs, n)                              # K3
                 w.flat.copy_(bufs[0])
-                w.opt.step()
-                w.flat.zero_()
+                if w.pflat is not None:                   # a9: K7 (SGD + gradient reset)
+                    pr.sgd_update(w.pflat, w.flat, cfg.lr, cfg.wd, zero_grad=True)
+                else:
+                    w.opt.step()
+                    w.flat.zero_()
                 ar[j][1].record()
                 w.gstep += 1
             torch.cuda.synchronize()

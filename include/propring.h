@@ -290,6 +290,24 @@ int pr_weighted_allreduce(pr_comm *c, void *d_buf, int64_t count, int32_t dt, in
 int pr_weighted_allreduce_local(pr_comm *const *comms, void *const *d_bufs, int64_t count, int32_t dt,
                                 const int64_t *n_local, void *stream);
 
+/* Rows a6-a9 in one call (K7 fused into K3): the weighted allreduce of the fp32 local-mean gradient
+ * d_grad (as pr_weighted_allreduce) followed by pr_sgd_update(d_theta, ḡ, lr, wd, zero_grad) — with the TMA
+ * ring and registered buffers, ONE kernel: the owner of each reduced chunk applies the update to its θ
+ * chunk and the all-gather carries θ' (into every rank's d_theta) instead of ḡ; the gradient is reset as
+ * the reduce-scatter consumes it.  d_theta must hold identical values on every rank (replicated
+ * parameters) and lie at the same byte offset from d_grad inside the same registered region on every rank
+ * (e.g. one pr_comm_alloc of 2·count floats: [grad | theta]); else — or when the configured algorithm for
+ * this size is not the ring — the call is composed of the two operations (same bits).  After the call
+ * d_theta holds θ' on every rank; d_grad holds 0 if zero_grad, else unspecified (the reduced ḡ is not
+ * materialised in the fused path).  Errors: as pr_weighted_allreduce (+ PR_ERR_INVALID latched when the
+ * ranks' θ layouts differ). */
+int pr_weighted_allreduce_sgd(pr_comm *c, float *d_grad, float *d_theta, int64_t count, int64_t n_local, double lr,
+                              double wd, int32_t zero_grad, void *stream);
+/* Local-group form of pr_weighted_allreduce_sgd (all P ranks in one launch). */
+int pr_weighted_allreduce_sgd_local(pr_comm *const *comms, float *const *d_grads, float *const *d_thetas,
+                                    int64_t count, const int64_t *n_local, double lr, double wd, int32_t zero_grad,
+                                    void *stream);
+
 /* Algorithm 1 step 1: every rank contributes `local` and receives all P values in rank
  * order into host out[P].  Synchronous (waits for `stream`). */
 int pr_comm_allgather_f64(pr_comm *c, double local, double *out, void *stream);

@@ -380,6 +380,29 @@ def weighted_allreduce(comm: Comm, buf, n_local: int, stream=None, count=None):
     return buf
 
 
+def weighted_allreduce_sgd(comm: Comm, grad, theta, n_local: int, lr: float, wd: float = 0.0, zero_grad: bool = True,
+                           stream=None):
+    """Rows a6-a9 in one call: θ ← θ − lr·(ḡ + wd·θ) with ḡ = Σ_r (n_r/Σn)·grad_r, and grad ← 0 — one fused
+    kernel (K7 in K3) when the ring takes the call and grad/theta share a registered region at the same
+    offset on every rank, else the composed pair (same bits).  fp32 only."""
+    if str(grad.dtype) != "torch.float32" or grad.dtype != theta.dtype or grad.numel() != theta.numel():
+        raise ValueError("grad and theta must be fp32 buffers of equal length")
+    _check(LIB.pr_weighted_allreduce_sgd(comm.handle, _ptr(grad), _ptr(theta), grad.numel(), int(n_local), float(lr),
+                                         float(wd), int(bool(zero_grad)), _stream(stream)), "pr_weighted_allreduce_sgd")
+
+
+def weighted_allreduce_sgd_local(comms, grads, thetas, n_local, lr: float, wd: float = 0.0, zero_grad: bool = True,
+                                 stream=None):
+    """Local-group form of weighted_allreduce_sgd (all ranks in one launch)."""
+    P = len(comms)
+    hs = (ctypes.c_void_p * P)(*[c.handle for c in comms])
+    gs = (ctypes.c_void_p * P)(*[_ptr(b) for b in grads])
+    ts = (ctypes.c_void_p * P)(*[_ptr(b) for b in thetas])
+    ns = (ctypes.c_int64 * P)(*[int(x) for x in n_local])
+    _check(LIB.pr_weighted_allreduce_sgd_local(hs, gs, ts, grads[0].numel(), ns, float(lr), float(wd),
+                                               int(bool(zero_grad)), _stream(stream)), "pr_weighted_allreduce_sgd_local")
+
+
 def weighted_allreduce_local(comms, bufs, n_local, stream=None, count=None):
     """All ranks of a comm_init_local group in one launch."""
     P = len(comms)

@@ -73,6 +73,9 @@ SIGNATURES = {
     "pr_weighted_allreduce": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_i64, c_vp]),
     "pr_weighted_allreduce_local": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i64, c_i32,
                                                    ctypes.POINTER(c_i64), c_vp]),
+    "pr_weighted_allreduce_sgd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_i64, c_dbl, c_dbl, c_i32, c_vp]),
+    "pr_weighted_allreduce_sgd_local": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
+                                                       c_i64, ctypes.POINTER(c_i64), c_dbl, c_dbl, c_i32, c_vp]),
     "pr_comm_allgather_f64": (ctypes.c_int, [c_vp, c_dbl, ctypes.POINTER(c_dbl), c_vp]),
     "pr_comm_status": (ctypes.c_int, [c_vp]),
     "pr_comm_timestamps": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64)]),
@@ -88,6 +91,8 @@ def load():
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("PROPRING_LIB") and not hasattr(lib, name):
+            continue     # an older A/B build (tools/variants.sh) may predate an entry point
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

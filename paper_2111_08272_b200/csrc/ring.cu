@@ -43,8 +43,8 @@ struct ChanFlags {          // written by peers, polled locally
     unsigned long long ag_ready;   uint64_t p2[15];   // by prev: direct all-gather slices written into my buf
 };
 struct HsEntry {            // handshake entry, written by rank q into every peer's page (slot [parity][q]):
-    uint64_t line[8];       // four LL lines: (seq32 | count, n, dtype/reg_id, offset halves), see handshake()
-};
+    uint64_t line[16];      // five LL lines: (seq32 | count, n, dtype/reg_id, offset, θ-delta halves), see
+};                          // handshake(); lines 5-7 unused (padding to 128 B)
 struct ChanState {          // local only: cumulative counters carried across calls
     unsigned long long seq;         // handshake sequence number
     unsigned long long slot_base;   // staging-slot slices produced (= consumed: uniform slicing)
@@ -62,7 +62,7 @@ struct AgEntry {
     double v;
 };
 static_assert(sizeof(ChanFlags) == 384, "flags");
-static_assert(sizeof(HsEntry) == 64, "hs");
+static_assert(sizeof(HsEntry) == 128, "hs");
 static_assert(sizeof(ChanState) == 128, "state");
 
 struct DevTable {
@@ -92,12 +92,16 @@ struct RankCall {
     int32_t reg_id;
     int32_t pad;
     int64_t reg_off;
+    int64_t th_delta;   // fused update (K7 in K3): θ = buf + th_delta bytes, identical on every rank
 };
 
 struct LaunchArgs {
     int64_t count;
     int32_t dtype;
     int32_t nranks;     // entries in calls[] (gridDim.y)
+    int32_t fuse;       // 1: the all-gather carries θ' = SGD(θ, ḡ) computed by the chunk owner (K7 in K3)
+    int32_t zero;       // fused: reset the gradient buffer as it is consumed
+    float nlr, wd;      // fused: −lr, weight decay (fp32, as pr_sgd_update)
     RankCall calls[PR_MAX_RANKS];
 };
 
@@ -344,8 +348,9 @@ __device__ __forceinline__ void ld_line64(const void* p, unsigned long long& a, 
 }
 __device__ __forceinline__ unsigned long long tag(uint32_t flag, uint32_t w) { return ((unsigned long long)flag << 32) | w; }
 __device__ __forceinline__ void hs_publish(HsEntry* e, uint32_t flag, long long count, long long n, uint32_t dtype,
-                                           int32_t reg_id, long long offset, bool sys) {
+                                           int32_t reg_id, long long offset, long long th_delta, bool sys) {
     unsigned long long* L = reinterpret_cast<unsigned long long*>(e);
+    st_line64(L + 8, tag(flag, (uint32_t)th_delta), tag(flag, (uint32_t)((unsigned long long)th_delta >> 32)), sys);
     st_line64(L + 0, tag(flag, (uint32_t)count), tag(flag, (uint32_t)((unsigned long long)count >> 32)), sys);
     st_line64(L + 2, tag(flag, (uint32_t)n), tag(flag, (uint32_t)((unsigned long long)n >> 32)), sys);
     st_line64(L + 4, tag(flag, dtype), tag(flag, (uint32_t)reg_id), sys);
@@ -354,17 +359,18 @@ __device__ __forceinline__ void hs_publish(HsEntry* e, uint32_t flag, long long 
 // Poll one entry until all eight elements carry `flag`; false on watchdog expiry.
 __device__ __forceinline__ bool hs_read(const HsEntry* e, uint32_t flag, unsigned long long deadline, bool sys,
                                         long long& count, long long& n, uint32_t& dtype, int32_t& reg_id,
-                                        long long& offset) {
+                                        long long& offset, long long& th_delta) {
     const unsigned long long* L = reinterpret_cast<const unsigned long long*>(e);
-    unsigned long long w[8];
+    unsigned long long w[10];
     for (;;) {
         ld_line64(L + 0, w[0], w[1], sys);
         ld_line64(L + 2, w[2], w[3], sys);
         ld_line64(L + 4, w[4], w[5], sys);
         ld_line64(L + 6, w[6], w[7], sys);
+        ld_line64(L + 8, w[8], w[9], sys);
         bool ok = true;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) ok = ok && (uint32_t)(w[k] >> 32) == flag;
+        for (int k = 0; k < 10; ++k) ok = ok && (uint32_t)(w[k] >> 32) == flag;
         if (ok) break;
         if (gtimer() > deadline) return false;
     }
@@ -373,6 +379,7 @@ __device__ __forceinline__ bool hs_read(const HsEntry* e, uint32_t flag, unsigne
     dtype = (uint32_t)w[4];
     reg_id = (int32_t)(uint32_t)w[5];
     offset = (long long)(((w[7] & 0xffffffffull) << 32) | (w[6] & 0xffffffffull));
+    th_delta = (long long)(((w[9] & 0xffffffffull) << 32) | (w[8] & 0xffffffffull));
     return true;
 }
 // Executed by ALL 32 lanes of warp 0: lane q publishes into rank q's page and polls entry q of this
@@ -387,19 +394,21 @@ __device__ HsOut handshake(const LaunchArgs& A, const RankCall& rc, const DevTab
     const int par = (int)(seq & 1ull);
     const uint32_t flag = (uint32_t)(seq & 0xffffffffull);
     for (int q = lane; q < P; q += 32)
-        hs_publish(hs_of(tab->win[q], tab, ch, par, r), flag, A.count, rc.n_local, (uint32_t)A.dtype, rc.reg_id,
-                   rc.reg_off, sys);
+        hs_publish(hs_of(tab->win[q], tab, ch, par, r), flag, A.count, rc.n_local,
+                   (uint32_t)A.dtype | ((uint32_t)A.fuse << 8), rc.reg_id, rc.reg_off, rc.th_delta, sys);
     int err = 0, direct = 1;
     long long sumn = 0;
     for (int q = lane; q < P; q += 32) {
-        long long cnt, n, off;
+        long long cnt, n, off, thd;
         uint32_t dt;
         int32_t rid;
-        if (!hs_read(hs_of(my, tab, ch, par, q), flag, deadline, sys, cnt, n, dt, rid, off)) {
+        if (!hs_read(hs_of(my, tab, ch, par, q), flag, deadline, sys, cnt, n, dt, rid, off, thd)) {
             err = PR_ERR_PEER_TIMEOUT;
             break;
         }
-        if (cnt != A.count || (int)dt != A.dtype) err = PR_ERR_LENGTH_MISMATCH;
+        // dtype word carries the fused-update flag in bits 8+: every rank must make the same kind of call
+        if (cnt != A.count || dt != ((uint32_t)A.dtype | ((uint32_t)A.fuse << 8))) err = PR_ERR_LENGTH_MISMATCH;
+        if (A.fuse && thd != rc.th_delta) err = err ? err : PR_ERR_INVALID;   // θ-layout differs across ranks
         sumn += n;
         if (rid < 0) direct = 0;
         if (ns) ns[q] = n;
@@ -418,7 +427,23 @@ __device__ HsOut handshake(const LaunchArgs& A, const RankCall& rc, const DevTab
     return out;
 }
 
-template <typename T>
+// K7's arithmetic on a 16-byte vector (fp32 only: the fused update requires fp32 buffers):
+// θ' = fma(−η, fma(λ, θ, ḡ), θ), exactly as pr_sgd_update.
+template <typename T> __device__ __forceinline__ uint4 sgd_v4(uint4 t, uint4 g, float nlr, float wd);
+template <> __device__ __forceinline__ uint4 sgd_v4<float>(uint4 t, uint4 g, float nlr, float wd) {
+    const uint32_t ti[4] = {t.x, t.y, t.z, t.w}, gi[4] = {g.x, g.y, g.z, g.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float tv = __uint_as_float(ti[j]);
+        o[j] = __float_as_uint(__fmaf_rn(nlr, __fmaf_rn(wd, tv, __uint_as_float(gi[j])), tv));
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+template <> __device__ __forceinline__ uint4 sgd_v4<__nv_bfloat16>(uint4, uint4 g, float, float) { return g; }
+
+// FUSE (compile time): the K7-fused variant; the plain ring is compiled without any of its code.
+template <typename T, bool FUSE>
 __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ LaunchArgs A) {
     extern __shared__ __align__(128) uint8_t smem[];   // [stages][2][tile_bytes]: g tile, recv tile
     __shared__ Shared sh;
@@ -455,7 +480,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
         __shared__ uint8_t* s_bufs[PR_MAX_RANKS];
         const HsOut hs = handshake(A, rc, tab, st, ch, sys, deadline, nullptr, s_bufs);
         if (t0) {
-            sh.err = hs.err;
+            sh.err = hs.err ? hs.err : ((A.fuse && !hs.direct) ? PR_ERR_INVALID : 0);   // fused: direct AG only
             sh.direct = hs.direct;
             sh.sumn = hs.sumn;
             sh.next_buf = hs.direct ? (void*)s_bufs[next] : nullptr;
@@ -484,6 +509,11 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
     const bool direct = sh.direct != 0;
     T* buf = reinterpret_cast<T*>(rc.buf);
     T* nbuf = reinterpret_cast<T*>(sh.next_buf);
+    // fused update (K7 in K3): the owner of a reduced chunk applies SGD to its θ and the all-gather carries
+    // θ' (own θ and the next rank's θ = buf + th_delta bytes, the same layout on every rank)
+    constexpr bool fuse = FUSE;
+    T* th = fuse ? reinterpret_cast<T*>(reinterpret_cast<uint8_t*>(rc.buf) + rc.th_delta) : buf;
+    T* nth = (fuse && nbuf) ? reinterpret_cast<T*>(reinterpret_cast<uint8_t*>(sh.next_buf) + rc.th_delta) : nbuf;
     const unsigned long long K = (unsigned long long)tab->slots;
     // Rounds of G = K/2 slices per chunk walk all 2P−1 phases:
     //   phase 0             RS hop 0     chunk r            y = s·g                 -> next's slot
@@ -543,7 +573,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 }
                 const int64_t nt = ntiles(kind, len);
                 const T* gsrc = buf + lo;
-                const T* isrc = (kind == K_AGMID && direct) ? buf + lo
+                const T* isrc = (kind == K_AGMID && direct) ? th + lo
                                                             : reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ));
                 for (int64_t t = 0; t < nt; ++t, ++tc) {
                     const int stg = (int)(tc % (uint32_t)kStages);
@@ -622,12 +652,14 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
             T* out2 = nullptr;
             T* nslot = reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ));
             if (kind == K_FIRST || kind == K_MID) out1 = nslot;
-            else if (kind == K_LAST) { out1 = buf + lo; out2 = direct ? nbuf + lo : nslot; }
-            else if (kind == K_AGMID) { if (direct) out1 = nbuf + lo; else { out1 = buf + lo; out2 = nslot; } }
+            else if (kind == K_LAST) { out1 = th + lo; out2 = direct ? nth + lo : nslot; }
+            else if (kind == K_AGMID) { if (direct) out1 = nth + lo; else { out1 = buf + lo; out2 = nslot; } }
             else out1 = buf + lo;                                   // K_AGLAST (staged)
             const T* gsrc = buf + lo;
-            const T* isrc = (kind == K_AGMID && direct) ? buf + lo
+            const T* isrc = (kind == K_AGMID && direct) ? th + lo
                                                         : reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ));
+            const bool upd = FUSE && kind == K_LAST;                // reduced chunk final here: apply SGD
+            const bool zg = FUSE && A.zero && kind <= K_LAST;        // own gradient consumed: reset it
             const bool ng = needs_g(kind), ni = needs_in(kind);
             bool ok = true;
             for (int64_t t = 0; t < nt; ++t, ++tc) {
@@ -645,7 +677,9 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                     for (int64_t v = cid; v < nv; v += nc) {
                         const uint4 a = ng ? gs[v] : make_uint4(0, 0, 0, 0);
                         const uint4 b = ni ? is[v] : make_uint4(0, 0, 0, 0);
-                        const uint4 y = Vec<T>::op(mode, s, a, b);
+                        uint4 y = Vec<T>::op(mode, s, a, b);
+                        if (upd) y = sgd_v4<T>(*reinterpret_cast<const uint4*>(th + lo + e0 + v * V), y, A.nlr, A.wd);
+                        if (zg) st_v4(buf + lo + e0 + v * V, make_uint4(0, 0, 0, 0));
                         st_v4(out1 + e0 + v * V, y);
                         if (out2) st_v4(out2 + e0 + v * V, y);
                     }
@@ -656,7 +690,12 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                         if (mode == M_SCALE) rr = __fmul_rn(s, gv);
                         else if (mode == M_FMA) rr = __fmaf_rn(s, gv, iv);
                         else rr = (mode == M_COPY) ? iv : 0.0f;
-                        const T y = (mode == M_COPY) ? Vec<T>::ld(isrc + e0 + e) : Vec<T>::from_f(rr);
+                        T y = (mode == M_COPY) ? Vec<T>::ld(isrc + e0 + e) : Vec<T>::from_f(rr);
+                        if (upd) {
+                            const float tv = Vec<T>::to_f(th[lo + e0 + e]);
+                            y = Vec<T>::from_f(__fmaf_rn(A.nlr, __fmaf_rn(A.wd, tv, Vec<T>::to_f(y)), tv));
+                        }
+                        if (zg) Vec<T>::st(buf + lo + e0 + e, Vec<T>::from_f(0.0f));
                         Vec<T>::st(out1 + e0 + e, y);
                         if (out2) Vec<T>::st(out2 + e0 + e, y);
                     }
@@ -1343,10 +1382,20 @@ int find_reg(const pr_comm* c, const void* buf, size_t bytes, int32_t* id, int64
 
 size_t dtype_size(int32_t dt) { return dt == PR_DTYPE_F32 ? 4 : (dt == PR_DTYPE_BF16 ? 2 : 0); }
 
+// The algorithm a call takes: a pure function of (config, count, dtype), identical on every rank.
+int pick_algo(const pr_comm_config& cfg, int64_t count, int32_t dtype) {
+    const int64_t bytes = count * (dtype == PR_DTYPE_F32 ? 4 : 2);
+    if ((cfg.algo == PR_ALGO_ONESHOT || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.os_max_bytes) return PR_ALGO_ONESHOT;
+    if ((cfg.algo == PR_ALGO_LL || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.ll_max_bytes) return PR_ALGO_LL;
+    if (cfg.algo == PR_ALGO_TWO_SHOT || (cfg.algo == PR_ALGO_AUTO && bytes <= cfg.ts_max_bytes)) return PR_ALGO_TWO_SHOT;
+    return PR_ALGO_RING;
+}
+
 int launch_ring(const LaunchArgs& a, int nranks, const pr_comm_config& cfg, cudaStream_t s, bool coop) {
     const int32_t threads = cfg.threads, channels = cfg.channels;
     // algorithm: a pure function of (config, count, dtype), identical on every rank
     const int64_t bytes = a.count * (a.dtype == PR_DTYPE_F32 ? 4 : 2);
+    if (a.fuse) goto ring;   // the fused update exists in the TMA ring only (callers check pick_algo)
     if ((cfg.algo == PR_ALGO_ONESHOT || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.os_max_bytes) {
         void* fn4 = (a.dtype == PR_DTYPE_F32) ? (void*)oneshot_ll_kernel<float> : (void*)oneshot_ll_kernel<__nv_bfloat16>;
         void* args4[] = {(void*)&a};
@@ -1380,10 +1429,12 @@ int launch_ring(const LaunchArgs& a, int nranks, const pr_comm_config& cfg, cuda
         }
         return PR_OK;
     }
-    void* fn = (a.dtype == PR_DTYPE_F32) ? (void*)ring_kernel<float> : (void*)ring_kernel<__nv_bfloat16>;
+ring:
+    void* fn = a.fuse ? (void*)ring_kernel<float, true>
+                      : (a.dtype == PR_DTYPE_F32) ? (void*)ring_kernel<float, false> : (void*)ring_kernel<__nv_bfloat16, false>;
     const size_t smem = (size_t)cfg.stages * 2 * cfg.tile_bytes;
-    static size_t attr_set[2] = {0, 0};
-    const int di = a.dtype == PR_DTYPE_F32 ? 0 : 1;
+    static size_t attr_set[3] = {0, 0, 0};
+    const int di = a.fuse ? 2 : (a.dtype == PR_DTYPE_F32 ? 0 : 1);
     if (attr_set[di] < smem) {
         PR_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set[di] = smem;
@@ -1605,6 +1656,93 @@ extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d
         find_reg(comms[r], d_bufs[r], 0, &a.calls[r].reg_id, &a.calls[r].reg_off);
     }
     PR_CUDA_TRY(cudaSetDevice(c0->device));
+    return launch_ring(a, P, c0->cfg, (cudaStream_t)stream, true);
+}
+
+// ---- K7 fused into K3: weighted allreduce + SGD update (+ gradient reset) ---------------------------
+extern "C" int pr_weighted_allreduce_sgd(pr_comm* c, float* d_grad, float* d_theta, int64_t count, int64_t n_local,
+                                         double lr, double wd, int32_t zero_grad, void* stream) {
+    if (!c || count < 0 || n_local < 0 || (count > 0 && (!d_grad || !d_theta))) return PR_ERR_INVALID;
+    if (((uintptr_t)d_grad & 15) || ((uintptr_t)d_theta & 15)) return PR_ERR_ALIGN;
+    if (int st = *(volatile int*)c->h_status) return st;
+    if (c->P == 1) {
+        if (n_local <= 0) return PR_ERR_ZERO_SAMPLES;
+        return pr_sgd_update(d_theta, d_grad, count, lr, wd, zero_grad, stream);
+    }
+    LaunchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.count = count;
+    a.dtype = PR_DTYPE_F32;
+    a.nranks = 1;
+    a.calls[0].tab = c->d_tab;
+    a.calls[0].buf = d_grad;
+    a.calls[0].n_local = n_local;
+    find_reg(c, d_grad, (size_t)count * 4, &a.calls[0].reg_id, &a.calls[0].reg_off);
+    int32_t trid = -1;
+    int64_t toff = 0;
+    find_reg(c, d_theta, (size_t)count * 4, &trid, &toff);
+    const bool fusable = pick_algo(c->cfg, count, PR_DTYPE_F32) == PR_ALGO_RING && a.calls[0].reg_id >= 0 &&
+                         trid == a.calls[0].reg_id && !(c->cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
+    if (!fusable) {   // composed: the same bits (the ring's ḡ, then K7's two FMAs)
+        if (int rc = pr_weighted_allreduce(c, d_grad, count, PR_DTYPE_F32, n_local, stream)) return rc;
+        return pr_sgd_update(d_theta, d_grad, count, lr, wd, zero_grad, stream);
+    }
+    a.fuse = 1;
+    a.zero = zero_grad ? 1 : 0;
+    a.nlr = (float)(-lr);
+    a.wd = (float)wd;
+    a.calls[0].th_delta = (int64_t)((const uint8_t*)d_theta - (const uint8_t*)d_grad);
+    return launch_ring(a, 1, c->cfg, (cudaStream_t)stream, false);
+}
+
+extern "C" int pr_weighted_allreduce_sgd_local(pr_comm* const* comms, float* const* d_grads, float* const* d_thetas,
+                                               int64_t count, const int64_t* n_local, double lr, double wd,
+                                               int32_t zero_grad, void* stream) {
+    if (!comms || !d_grads || !d_thetas || !n_local || count < 0) return PR_ERR_INVALID;
+    const pr_comm* c0 = comms[0];
+    if (!c0 || !c0->local) return PR_ERR_INVALID;
+    const int P = c0->P;
+    int64_t sumn = 0;
+    bool same_delta = true;
+    const int64_t d0 = (int64_t)((const uint8_t*)d_thetas[0] - (const uint8_t*)d_grads[0]);
+    for (int r = 0; r < P; ++r) {
+        const pr_comm* c = comms[r];
+        if (!c || !c->local || c->rank != r || c->P != P || c->device != c0->device) return PR_ERR_INVALID;
+        if (n_local[r] < 0 || (count > 0 && (!d_grads[r] || !d_thetas[r]))) return PR_ERR_INVALID;
+        if (((uintptr_t)d_grads[r] & 15) || ((uintptr_t)d_thetas[r] & 15)) return PR_ERR_ALIGN;
+        if (int st = *(volatile int*)c->h_status) return st;
+        sumn += n_local[r];
+        same_delta = same_delta && (int64_t)((const uint8_t*)d_thetas[r] - (const uint8_t*)d_grads[r]) == d0;
+    }
+    if (sumn <= 0) return PR_ERR_ZERO_SAMPLES;
+    PR_CUDA_TRY(cudaSetDevice(c0->device));
+    const bool fusable = P > 1 && pick_algo(c0->cfg, count, PR_DTYPE_F32) == PR_ALGO_RING && same_delta &&
+                         !(c0->cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
+    if (!fusable) {
+        if (P > 1) {
+            if (int rc = pr_weighted_allreduce_local(comms, (void* const*)d_grads, count, PR_DTYPE_F32, n_local, stream))
+                return rc;
+        }
+        for (int r = 0; r < P; ++r)
+            if (int rc = pr_sgd_update(d_thetas[r], d_grads[r], count, lr, wd, zero_grad, stream)) return rc;
+        return PR_OK;
+    }
+    LaunchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.count = count;
+    a.dtype = PR_DTYPE_F32;
+    a.nranks = P;
+    a.fuse = 1;
+    a.zero = zero_grad ? 1 : 0;
+    a.nlr = (float)(-lr);
+    a.wd = (float)wd;
+    for (int r = 0; r < P; ++r) {
+        a.calls[r].tab = comms[r]->d_tab;
+        a.calls[r].buf = d_grads[r];
+        a.calls[r].n_local = n_local[r];
+        a.calls[r].th_delta = d0;
+        find_reg(comms[r], d_grads[r], 0, &a.calls[r].reg_id, &a.calls[r].reg_off);
+    }
     return launch_ring(a, P, c0->cfg, (cudaStream_t)stream, true);
 }
 

@@ -126,7 +126,14 @@ class Worker:
         self._pool = None
         params = list(self.model.parameters())
         self.L = sum(p.numel() for p in params)
-        if comm is not None:
+        self._raw = None
+        Lp = (self.L + 3) // 4 * 4
+        if comm is not None and cfg.fused_sgd:
+            # one IPC-registered region [grad | θ], θ at the same offset on every rank: the fused a6-a9 call
+            # (K7 inside K3's ring) all-gathers θ' straight into every rank's parameters
+            self._raw = comm.alloc(2 * Lp * 4, dtype=torch.float32)
+            self.flat = self._raw[:self.L]
+        elif comm is not None:
             self.flat = comm.alloc(self.L * 4, dtype=torch.float32)   # IPC-registered: direct all-gather
         else:
             self.flat = torch.zeros(self.L, dtype=torch.float32, device=self.dev)
@@ -136,7 +143,8 @@ class Worker:
             off += p.numel()
         self.pflat = None
         if cfg.fused_sgd:  # parameters become views of one flat fp32 buffer laid out like the gradient
-            self.pflat = torch.empty(self.L, dtype=torch.float32, device=self.dev)
+            self.pflat = (self._raw[Lp:Lp + self.L] if self._raw is not None
+                          else torch.empty(self.L, dtype=torch.float32, device=self.dev))
             off = 0
             with torch.no_grad():
                 for p in params:
@@ -350,11 +358,18 @@ class Worker:
             if record:
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(self.stream)
-            pr.weighted_allreduce(self.comm, self.flat, n_r, stream=self.stream)
+            if self.pflat is not None:
+                # a6-a9 in one call: weighted ring allreduce with K7 fused (θ' all-gathered, gradient reset)
+                pr.weighted_allreduce_sgd(self.comm, self.flat, self.pflat, n_r, self.cfg.lr, self.cfg.wd,
+                                          zero_grad=True, stream=self.stream)
+            else:
+                pr.weighted_allreduce(self.comm, self.flat, n_r, stream=self.stream)
             self.launches += 1
             if record:
                 a1.record(self.stream)
                 self.ar_events.append((a0, a1))
+            if self.pflat is not None:
+                return
         if self.pflat is not None:
             if record:
                 u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -422,3 +422,96 @@ def test_ll_ring_length_mismatch_and_timeout_latch(algo):
     assert comms[0].status() == pr.PR_ERR_PEER_TIMEOUT
     for c in comms:
         c.destroy()
+
+
+# ---- rows a6-a9 fused: K7 (SGD + reset) inside K3's ring -------------------------------------------------
+
+def _fused_case(P, L, n, comms, seed, cfg_delta=True, lr=1e-2, wd=1e-4):
+    """One [grad | theta] allocation per rank (theta at the same offset everywhere), replicated theta."""
+    Lp = (L + 3) // 4 * 4
+    g = synth.gradients(P, L, seed_base=seed)
+    theta0 = synth.gradients(1, L, seed_base=seed + 500)[0]
+    store = [torch.zeros(2 * Lp + (0 if cfg_delta else 4 * (r + 1)), device="cuda") for r in range(P)]
+    off = [Lp if cfg_delta else Lp + 4 * (r + 1) for r in range(P)]
+    grads = [store[r][:L] for r in range(P)]
+    thetas = [store[r][off[r]:off[r] + L] for r in range(P)]
+    for r in range(P):
+        grads[r].copy_(torch.from_numpy(g[r]))
+        thetas[r].copy_(torch.from_numpy(theta0))
+    # composed reference on copies: ring allreduce, then K7 on every rank
+    rg = [torch.from_numpy(g[r].copy()).cuda() for r in range(P)]
+    rt = [torch.from_numpy(theta0.copy()).cuda() for r in range(P)]
+    pr.weighted_allreduce_local(comms, rg, n)
+    for r in range(P):
+        pr.sgd_update(rt[r], rg[r], lr, wd, zero_grad=True)
+    pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, lr, wd, zero_grad=True)
+    torch.cuda.synchronize()
+    assert all(c.status() == 0 for c in comms)
+    for r in range(P):
+        assert torch.equal(thetas[r], rt[r]), f"rank {r}: fused θ' differs from ring + K7"
+        assert torch.count_nonzero(grads[r]) == 0
+    return g, theta0, thetas[0].cpu().numpy()
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_fused_allreduce_sgd_bit_identical_to_composed(P):
+    comms = group(P)
+    rng = np.random.Generator(np.random.PCG64(300 + P))
+    for L in (1, 7, 1000, 4099, 2 ** 20 + 3):
+        n = [int(x) * 16 for x in rng.integers(1, 9, P)]
+        if L % 2:
+            n[int(rng.integers(0, P))] = 0
+        _fused_case(P, L, n, comms, seed=L)
+
+
+def test_fused_allreduce_sgd_resnet18_size_against_oracle():
+    """Full ResNet-18 gradient at P = 8: fused θ' = composed θ' bit for bit, and within K7's two roundings of
+    the oracle (ring replay for ḡ, fp64 SGD)."""
+    from oracle import linmodel as LM
+
+    P, L = 8, 11_689_512
+    n = [64, 64, 64, 64, 128, 128, 256, 256]
+    g, theta0, out = _fused_case(P, L, n, group(P), seed=77)
+    gbar = W.ring_emulate(g, n, "f32").astype(np.float64)
+    ref = LM.sgd_step(theta0.astype(np.float64), gbar, float(np.float32(1e-2)), float(np.float32(1e-4)))
+    bound = 2.0 ** -24 * (np.abs(ref) + np.float32(1e-2) * np.abs(gbar + np.float32(1e-4) * theta0)) * 1.01
+    assert np.all(np.abs(out.astype(np.float64) - ref) <= bound + 1e-45)
+
+
+def test_fused_allreduce_sgd_small_slices_staged_and_layout_fallbacks():
+    for cfg in (dict(channels=3, slots=4, slot_bytes=4096, tile_bytes=1024, stages=3), dict(force_staged=True),
+                dict(algo=pr.ALGO_AUTO)):
+        comms = group(4, **cfg)
+        for L in (999, 300_001):
+            _fused_case(4, L, [3, 0, 5, 1], comms, seed=L + 9)
+    # θ at different offsets on different ranks: the host composes the two operations instead
+    _fused_case(3, 5000, [1, 2, 3], group(3), seed=5, cfg_delta=False)
+
+
+def test_fused_allreduce_sgd_graph_replay():
+    P, L = 3, 40_000
+    comms = group(P)
+    Lp = L
+    store = [torch.zeros(2 * Lp, device="cuda") for _ in range(P)]
+    grads, thetas = [s_[:L] for s_ in store], [s_[Lp:] for s_ in store]
+    g = synth.gradients(P, L, seed_base=41)
+    theta0 = torch.from_numpy(synth.gradients(1, L, seed_base=42)[0]).cuda()
+    n = [3, 1, 2]
+    s = torch.cuda.Stream()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 0.1, 0.0, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gr, stream=s):
+            pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 0.1, 0.0, stream=s)
+    rg = [torch.from_numpy(g[r].copy()).cuda() for r in range(P)]
+    pr.weighted_allreduce_local(comms, rg, n)
+    ref = theta0.clone()
+    pr.sgd_update(ref, rg[0].clone(), 0.1, 0.0)
+    for _ in range(3):
+        for r in range(P):
+            grads[r].copy_(torch.from_numpy(g[r]))
+            thetas[r].copy_(theta0)
+        gr.replay()
+        torch.cuda.synchronize()
+        assert all(torch.equal(t, ref) for t in thetas)

@@ -114,6 +114,21 @@ def _gpu_worker(rank, world, port, q):
             ok = ok and t == [1.5, 2.5]
             if not ok:
                 bad.append(f"algo={algo} sys={sys_scope} status={st}")
+            if algo == pr.ALGO_RING and not sys_scope:
+                # rows a6-a9 fused (K7 in K3) over IPC: one [grad | theta] region per rank
+                raw = comm.alloc(2 * 4100 * 4, dtype=torch.float32)
+                gr, th = raw[:L], raw[4100:4100 + L]
+                theta0 = torch.from_numpy(synth.gradients(1, L, seed_base=12)[0]).cuda()
+                gr.copy_(torch.from_numpy(g[rank]))
+                th.copy_(theta0)
+                pr.weighted_allreduce_sgd(comm, gr, th, n[rank], 0.05, 1e-4)
+                torch.cuda.synchronize()
+                ref_g = torch.from_numpy(W.ring_emulate(g, n, "f32")).cuda()
+                ref = theta0.clone()
+                pr.sgd_update(ref, ref_g, 0.05, 1e-4)
+                torch.cuda.synchronize()
+                if not (comm.status() == 0 and torch.equal(th, ref) and torch.count_nonzero(gr) == 0):
+                    bad.append(f"fused status={comm.status()}")
             dist.barrier()
             comm.destroy()
         q.put((rank, "ok" if not bad else "; ".join(bad)))

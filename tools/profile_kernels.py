@@ -62,6 +62,27 @@ def sgd(reps, L=11_689_512):
     print(f"sgd L={L}: {us:.2f} us, {16 * L / us / 1e3:.1f} GB/s algorithmic")
 
 
+def ring_fused(reps, P=8, L=11_689_512):
+    """Rows a6-a9: composed (K3 ring + K7 per rank) vs fused (K7 inside K3), 8 ranks co-located."""
+    comms = pr.comm_init_local(P, 0)
+    store = [torch.randn(2 * L, device="cuda") for _ in range(P)]
+    grads, thetas = [s_[:L] for s_ in store], [s_[L:] for s_ in store]
+    n = [64, 64, 64, 64, 128, 128, 256, 256][:P]
+
+    def composed():
+        pr.weighted_allreduce_local(comms, grads, n)
+        for r in range(P):
+            pr.sgd_update(thetas[r], grads[r], 1e-6, 0.0, zero_grad=False)
+
+    def fused():
+        pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 1e-6, 0.0, zero_grad=False)
+
+    uc, uf = timed(composed, reps), timed(fused, reps)
+    print(f"a6-a9 P={P} L={L}: composed (ring + {P}x K7) {uc:.1f} us, fused {uf:.1f} us")
+    for c in comms:
+        c.destroy()
+
+
 def ring(reps, P=8, L=11_689_512):
     comms = pr.comm_init_local(P, 0, pr.comm_config())
     bufs = [torch.randn(L, device="cuda") for _ in range(P)]
@@ -92,5 +113,7 @@ if __name__ == "__main__":
         shard(reps)
     if what in ("sgd", "all"):
         sgd(reps)
+    if what in ("ring_fused", "all"):
+        ring_fused(reps)
     if what in ("ring", "all"):
         ring(reps)
