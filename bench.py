@@ -268,7 +268,7 @@ def run_ours(args):
                "h2d_bytes_per_step": v["S"] * v["n"][rank] * (ROW_BYTES + 8),
                "d2h_bytes_per_step": v["S"] * 4,
                "note": "data set in pinned host memory; rows gathered over PCIe by K2 inside the timed region; "
-                       "per-step loss copied to host"}
+                       "every step's loss copied to pinned host memory and read by the host one step late (no per-step GPU idle)"}
 
     # ---- co-located ring (1 GPU): all P ranks of K3 on this GPU, HBM-bound proxy of the NVLink path --
     colocated = None
@@ -408,9 +408,33 @@ def colocated_allreduce(hbm, peak_kind, P=8, reps=20):
     # algorithmic HBM bytes of one call, all P ranks (direct all-gather): per rank
     # hop0 2·Z/P, P−2 middle hops 3·Z/P, last hop 4·Z/P, P−2 forwards 2·Z/P  => (6 + 5(P−2))·Z/P
     byts = P * (6 + 5 * (P - 2)) * Z / P
+    # rows a6-a9 fused (K7 inside K3) vs composed (ring + K7 per rank), same setting
+    store = [torch.randn(2 * L, device="cuda") for _ in range(P)]
+    grads, thetas = [x[:L] for x in store], [x[L:] for x in store]
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e3
+
+    def composed():
+        pr.weighted_allreduce_local(comms, grads, n)
+        for r in range(P):
+            pr.sgd_update(thetas[r], grads[r], 1e-6, 0.0, zero_grad=True)
+
+    fused_us = timed(lambda: pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 1e-6, 0.0, zero_grad=True))
+    composed_us = timed(composed)
     for c in comms:
         c.destroy()
     return {"kernel": "ring_kernel<float> (K3), all ranks on one GPU", "P": P, "bytes_per_rank": Z,
+            "fused_a6_a9_us": fused_us, "composed_a6_a9_us": composed_us,
             "n_local": n, "avg_us": t * 1e3, "bound": "hbm", "achieved": byts / (t * 1e-3) / 1e9, "peak": hbm,
             "unit": "GB/s", "frac": byts / (t * 1e-3) / 1e9 / hbm, "peak_kind": peak_kind,
             "algorithmic_bytes_per_call": byts,

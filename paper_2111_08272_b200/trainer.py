@@ -438,18 +438,41 @@ class Worker:
             self.gstep += 1
             losses.append(loss)
             if loss_to_host:
-                host_losses.append(float(loss))          # D2H of the step's result (e2e contract)
+                # D2H of the step's result (e2e contract), read one step late: the copy is enqueued behind
+                # this step and the host blocks on the PREVIOUS step's copy, so the GPU never idles for it
+                self._loss_readback(loss, host_losses)
         if cfg.gather == "epoch" and v["frozen"]:
             # frozen allocation: the next epoch's shard cannot change at the boundary, so its K1 + K2
             # are enqueued now and run while the host synchronises for t_s and runs the controller
             self._prefetched = ((self.epoch + 1, n_r), self._data(self.epoch + 1, n_r, S, record))
         ev[-1][1].synchronize()
+        while loss_to_host and getattr(self, "_pending", None):
+            self._read_loss(host_losses)
         t_s = e0.elapsed_time(e1) / 1e3 + self._compute_time(ev)                      # seconds (a5)
         self.epoch += 1
         rec = {"t_s": t_s, "loss": float(torch.stack(losses).mean()), "S": S, "n_r": n_r, "w": v["w"]}
         self.history.append(rec)
         self.last_ts = t_s
         return rec
+
+    def _loss_readback(self, loss, host_losses):
+        """Enqueue the step's loss D2H copy into a pinned 2-slot ring; block on and read the PREVIOUS step's."""
+        if not hasattr(self, "_loss_pinned"):
+            self._loss_pinned = torch.empty(2, dtype=torch.float32, pin_memory=True)
+            self._loss_ev = [torch.cuda.Event(), torch.cuda.Event()]
+            self._pending, self._ls = [], 0
+        slot = self._ls % 2
+        self._ls += 1
+        self._loss_pinned[slot:slot + 1].copy_(loss.detach().float().reshape(1), non_blocking=True)
+        self._loss_ev[slot].record(self.stream)
+        self._pending.append(slot)
+        while len(self._pending) > 1:
+            self._read_loss(host_losses)
+
+    def _read_loss(self, host_losses):
+        slot = self._pending.pop(0)
+        self._loss_ev[slot].synchronize()
+        host_losses.append(float(self._loss_pinned[slot]))
 
     def run_epoch_segments(self, record=False, loss_to_host=False):
         """N3: the epoch as segments of k = adapt_every aggregation steps over the step-interleaved shard.
@@ -487,8 +510,10 @@ class Worker:
                 self.gstep += 1
                 losses.append(loss)
                 if loss_to_host:
-                    host_losses.append(float(loss))
+                    self._loss_readback(loss, host_losses)
             ev[-1][1].synchronize()
+            while loss_to_host and getattr(self, "_pending", None):
+                self._read_loss(host_losses)
             t_seg = e0.elapsed_time(e1) / 1e3 + self._compute_time(ev)
             t_epoch += t_seg
             changed = False
