@@ -1,0 +1,27 @@
+#!/bin/bash
+# Everything this round could not measure on a one-GPU box, for the first call that gets > 1 GPU.
+# Output -> gpurun_out/mg_*.  Usage: bash tools/multigpu_first_run.sh [max GPUs, default 8]
+G=${1:-8}
+mkdir -p gpurun_out
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+nvidia-smi topo -m > gpurun_out/mg_topo.txt 2>&1
+for P in 2 4 8; do
+  [ $P -gt $G ] && break
+  # C5: K3 (ring) vs NCCL premul-sum / scale+sum, 1 MiB .. 1 GiB, fp32 + bf16, parity on samples
+  timeout 1200 $TR --nproc-per-node $P --master-port $((29600 + P)) tools/ar_sweep.py --max-mib 1024 \
+      > gpurun_out/mg_ar_sweep_p$P.jsonl 2> gpurun_out/mg_ar_sweep_p$P.err
+  # the bench at N = P, without and with N1 overlap
+  timeout 1200 $TR --nproc-per-node $P --master-port $((29610 + P)) bench.py --gpus $P --steps 5 --warmup 3 \
+      > gpurun_out/mg_bench_p$P.json 2> gpurun_out/mg_bench_p$P.err
+  timeout 1200 $TR --nproc-per-node $P --master-port $((29620 + P)) bench.py --gpus $P --steps 5 --warmup 3 --overlap \
+      --no-cpu-baseline > gpurun_out/mg_bench_overlap_p$P.json 2> gpurun_out/mg_bench_overlap_p$P.err
+done
+# AUTO (one-shot / LL / two-shot / ring by size) at the largest P
+timeout 1200 $TR --nproc-per-node $G --master-port 29630 tools/ar_sweep.py --max-mib 64 --algo 2 \
+    > gpurun_out/mg_ar_sweep_auto_p$G.jsonl 2> gpurun_out/mg_ar_sweep_auto_p$G.err
+# emulated heterogeneity one rank per GPU (C4 scenarios need 8)
+[ $G -ge 8 ] && timeout 1800 $TR --nproc-per-node 8 --master-port 29640 experiments.py --scenario c4 \
+    > gpurun_out/mg_c4.jsonl 2> gpurun_out/mg_c4.err
+[ $G -ge 4 ] && timeout 1800 $TR --nproc-per-node 4 --master-port 29641 experiments.py --scenario c3 \
+    > gpurun_out/mg_c3.jsonl 2> gpurun_out/mg_c3.err
+ls -la gpurun_out/mg_*
