@@ -361,6 +361,10 @@ def nccl_baseline(wk, world, rank, reps=20):
         return {"us": us, "busbw_GBs": Z * 2 * (world - 1) / world / (us * 1e-6) / 1e9}
 
     out = {"propring_K3": timed(lambda: pr.weighted_allreduce(wk.comm, buf, n_r))}
+    if getattr(wk, "pflat", None) is not None:
+        # rows a6-a9 fused (K7 in K3); lr = 0 leaves the parameters bit-identical (θ + (−0)·d = θ)
+        out["propring_K3_K7_fused"] = timed(lambda: pr.weighted_allreduce_sgd(wk.comm, buf, wk.pflat, n_r, 0.0, 0.0,
+                                                                              zero_grad=False))
     try:
         op = dist._make_nccl_premul_sum(s)
         out["nccl_premul_sum"] = timed(lambda: dist.all_reduce(buf, op=op))
