@@ -515,3 +515,34 @@ def test_fused_allreduce_sgd_graph_replay():
         gr.replay()
         torch.cuda.synchronize()
         assert all(torch.equal(t, ref) for t in thetas)
+
+
+def test_randomized_configs_all_algorithms():
+    """Seeded sweep over communicator configurations × algorithms × P × counts × dtypes × weights: every
+    result bit-identical to the oracle's ring replay (and, for fused calls, to ring + K7)."""
+    rng = np.random.Generator(np.random.PCG64(2024))
+    algos = [pr.ALGO_RING, pr.ALGO_TWO_SHOT, pr.ALGO_LL, pr.ALGO_ONESHOT, pr.ALGO_AUTO]
+    for case in range(80):
+        P = int(rng.choice([2, 3, 4, 5, 6, 7, 8]))
+        stages = int(rng.integers(2, 7))
+        tile = int(rng.choice([256, 1024, 4096, 16384]))
+        cfg = dict(channels=int(rng.integers(1, 9)), slots=int(rng.choice([2, 4, 6, 8])),
+                   slot_bytes=int(rng.choice([256, 4096, 65536, 262144])), stages=stages, tile_bytes=tile,
+                   threads=int(rng.choice([64, 128, 256, 512])), algo=int(rng.choice(algos)),
+                   sys_scope=bool(rng.integers(0, 2)), ts_slot_bytes=int(rng.choice([256, 4096, 65536])),
+                   ll_max_bytes=int(rng.choice([4096, 262144])), os_max_bytes=int(rng.choice([1024, 65536])))
+        comms = pr.comm_init_local(P, 0, pr.comm_config(watchdog_ns=5_000_000_000, **cfg))
+        try:
+            for _ in range(2):
+                L = int(rng.choice([1, 3, 17, 1000, 4097, 65_537, 300_001]))
+                dtype = "f32" if rng.integers(0, 2) else "bf16"
+                n = [int(x) for x in rng.integers(0, 5, P)]
+                if sum(n) == 0:
+                    n[0] = 1
+                _check(P, L, dtype, n, comms, kind="mixed" if L % 2 else "gaussian", seed=case * 7 + L)
+            if cfg["algo"] in (pr.ALGO_RING, pr.ALGO_AUTO):
+                _fused_case(P, int(rng.choice([7, 5000, 200_003])), [1 + (r % 3) for r in range(P)], comms,
+                            seed=case + 900)
+        finally:
+            for c in comms:
+                c.destroy()
