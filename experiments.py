@@ -42,6 +42,10 @@ SCENARIOS = {
     "c2-5x-lin": ("resnet18", 50_000, (3, 32, 32), 2, [1, 1], 24, 256, [5.0, 1.0], True),
     "c4-lin": ("resnet18", 50_000, (3, 32, 32), 8, [1] * 8, 64, 256, [4, 4, 4, 4, 2, 2, 1, 1], True),
     "c4-replace-lin": ("resnet18", 50_000, (3, 32, 32), 8, [1] * 8, 64, 256, [1, 4, 4, 4, 2, 2, 1, 1], True),
+    # add-slow-worker pair in the same regime: 7 ranks (speeds 1:1:1:2:2:4:4), then an 8th speed-1 rank
+    # joins (separate runs); C = 256, g = 64: B = 16,384, S = 12 (rounding excess 1.1% / 0%)
+    "c4-add-base-lin": ("resnet18", 204_800, (3, 32, 32), 7, [1] * 7, 256, 64, [4, 4, 4, 2, 2, 1, 1], True),
+    "c4-add-lin": ("resnet18", 204_800, (3, 32, 32), 8, [1] * 8, 256, 64, [4, 4, 4, 2, 2, 1, 1, 4], True),
     # N4: convergence invariance under static ratios (Fig. 6, caption P:291):
     # minibatch 100, total batch 1000 (C = 10), lr 1e-2, wd 1e-4, ratios 5:5, 6:4, 3:7, 7:3
     "n4-55": ("resnet18", 50_000, (3, 32, 32), 2, [5, 5], 10, 100, [1.0, 1.0], False),
@@ -85,7 +89,7 @@ def run_virtual(args):
     if policy is not None and args.ema < 1.0:
         policy["ema_alpha"] = args.ema
     cfg = RunConfig(N=N, shape=shape, model=model, ratios=ratios, C=C, g=g, slowdown=sigma,
-                    adaptive=adaptive and not args.static, micro=256 if model == "vgg16" else 1024,
+                    adaptive=adaptive and not args.static, micro=args.micro or (256 if model == "vgg16" else 1024),
                     adapt_every=k, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario))
     w = Worker(cfg, 0, 1, 0, None)
     comms = pr.comm_init_local(P, 0, pr.comm_config())
@@ -170,6 +174,9 @@ def main():
     ap.add_argument("--epochs", type=int, default=8)
     ap.add_argument("--N", type=int, default=0, help="override the data set size (shorter epochs)")
     ap.add_argument("--static", action="store_true", help="disable the self-adaptive controller")
+    ap.add_argument("--micro", type=int, default=0,
+                    help="max rows per microbatch (default 1024 ResNet / 256 VGG); a rank whose n_r crosses a "
+                         "multiple of it pays one more fixed per-microbatch cost")
     ap.add_argument("--virtual", action="store_true", help="all ranks on one GPU, serially (see run_virtual)")
     ap.add_argument("--adapt-every", type=int, default=0,
                     help="N3: controller every k aggregation steps over the step-interleaved shard (0 = per epoch)")
@@ -203,7 +210,7 @@ def main():
     if policy is not None and args.ema < 1.0:
         policy["ema_alpha"] = args.ema
     cfg = RunConfig(N=N, shape=shape, model=model, ratios=ratios, C=C, g=g, slowdown=sigma,
-                    adaptive=adaptive and not args.static, micro=256 if model == "vgg16" else 1024,
+                    adaptive=adaptive and not args.static, micro=args.micro or (256 if model == "vgg16" else 1024),
                     adapt_every=args.adapt_every, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario))
     wk = Worker(cfg, rank, world, local, comm)
     wk.calibrate()
