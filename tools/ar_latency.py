@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--staged", action="store_true")
     ap.add_argument("--sys", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="time the calls inside one captured CUDA graph")
     ap.add_argument("--sizes", default="16384,65536,262144,1048576,4194304,16777216")
     ap.add_argument("--algos", default="ring,two_shot,ll")
     ap.add_argument("--channels", type=int, default=16)
@@ -58,17 +59,30 @@ def main():
                 pr.weighted_allreduce_local(comms, bufs, n)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(a.reps):
-                pr.weighted_allreduce_local(comms, bufs, n)
-            e1.record()
+            if a.graph:   # reps calls captured in one CUDA graph: device time per call, no host launch gaps
+                st = torch.cuda.Stream()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(st):
+                    with torch.cuda.graph(g, stream=st):
+                        for _ in range(a.reps):
+                            pr.weighted_allreduce_local(comms, bufs, n, stream=st)
+                g.replay()
+                torch.cuda.synchronize()
+                e0.record()
+                g.replay()
+                e1.record()
+            else:
+                e0.record()
+                for _ in range(a.reps):
+                    pr.weighted_allreduce_local(comms, bufs, n)
+                e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / a.reps * 1e3
             st = comms[0].timestamps()
             ok = all(c.status() == 0 for c in comms)
             print(json.dumps({"algo": algo_name, "P": P, "bytes": Z, "us": round(us, 2),
                               "t_w_us": (st[1] - st[0]) / 1e3, "t_c_us": (st[2] - st[1]) / 1e3,
-                              "staged": a.staged, "sys": a.sys, "channels": a.channels, "slots": a.slots,
+                              "staged": a.staged, "sys": a.sys, "graph": a.graph, "channels": a.channels, "slots": a.slots,
                               "slot_bytes": a.slot_bytes, "ok": ok}), flush=True)
         del raws
         for c in comms:
