@@ -246,7 +246,8 @@ def run_ours(args):
                           host_data=True, overlap=args.overlap, bucket_mb=args.bucket_mb)
         wk_h = Worker(cfg_h, rank, world, local, comm, data=wk.X.cpu(), labels=wk.Y.cpu())
         wk_h.model.load_state_dict(wk.model.state_dict())
-        epoch(w=wk_h)                                      # warm-up
+        for _ in range(3):                                 # warm-up: the allocation freezes, after
+            epoch(w=wk_h)                                  # which every epoch prefetches the next one's rows
         torch.cuda.synchronize()
         barrier()
         h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

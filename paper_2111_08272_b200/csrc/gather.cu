@@ -17,6 +17,8 @@
 // FADD2/FMUL2 (per-lane IEEE RN, identical to the scalar two-op definition), cvt.rn.bf16x2.f32.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.h"
 
 namespace {
@@ -520,7 +522,7 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
     // TMA staging pays off once a launch moves enough bytes to be bandwidth-bound; rows
     // read from pinned host memory (the e2e path) stream over PCIe through the LSU kernel.
     bool host_src = false;
-    if (impl == PR_GATHER_IMPL_AUTO) {
+    if (impl != PR_GATHER_IMPL_TMA) {
         cudaPointerAttributes at;
         if (cudaPointerGetAttributes(&at, d_src) == cudaSuccess) host_src = at.type == cudaMemoryTypeHost;
         else cudaGetLastError();
@@ -573,6 +575,17 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
     int64_t blocks = (items + kWarpsPerCta - 1) / kWarpsPerCta;
 #ifndef PR_GATHER_GRID
     if (blocks > resident[opi]) blocks = resident[opi];
+    if (host_src) {
+        // rows read over PCIe: a few CTAs keep enough loads in flight for the link, and the rest of the GPU
+        // stays free for the compute this gather runs beside (the trainer prefetches on a side stream)
+        static int host_grid = 0;
+        if (!host_grid) {
+            const char* e = getenv("PR_GATHER_HOST_GRID");
+            host_grid = e ? atoi(e) : 64;
+            if (host_grid < 1) host_grid = 64;
+        }
+        if (blocks > host_grid) blocks = host_grid;
+    }
 #else
     if (blocks > PR_GATHER_GRID) blocks = PR_GATHER_GRID;
 #endif

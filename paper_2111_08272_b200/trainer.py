@@ -213,19 +213,21 @@ class Worker:
             self._next += 1
 
     # ---- a3: data movement --------------------------------------------------------------------------
-    def gather(self, first: int, rows: int, record=False):
+    def gather(self, first: int, rows: int, record=False, stream=None):
         """K2: rows [first, first+rows) of this rank's shard -> (x [rows, C·H·W], y [rows])."""
-        x = torch.empty((max(rows, 1), self.row_bytes), dtype=self.xdt, device=self.dev)
-        y = torch.empty(max(rows, 1), dtype=torch.int64, device=self.dev)
+        st = self.stream if stream is None else stream
+        with torch.cuda.stream(st):                   # outputs allocated on (and owned by) the launching stream
+            x = torch.empty((max(rows, 1), self.row_bytes), dtype=self.xdt, device=self.dev)
+            y = torch.empty(max(rows, 1), dtype=torch.int64, device=self.dev)
         if rows > 0:
             if record:
                 g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                g0.record(self.stream)
+                g0.record(st)
             pr.gather_rows(self.X.data_ptr(), self.cfg.N, self.row_bytes, self.idx[first:], rows, x, self.gop, self.Y,
-                           y, stream=self.stream)
+                           y, stream=st)
             self.launches += 1
             if record:
-                g1.record(self.stream)
+                g1.record(st)
                 self.gather_events.append((g0, g1, rows))
         return x, y
 
@@ -394,16 +396,19 @@ class Worker:
         return sum(a.elapsed_time(b) for a, b in ev) / 1e3
 
     # ---- one epoch (Algorithm 1 outer loop) -----------------------------------------------------------
-    def _data(self, epoch: int, n_r: int, S: int, record: bool):
+    def _data(self, epoch: int, n_r: int, S: int, record: bool, stream=None):
         """a2 + a3 of `epoch`: the shard (K1) and — epoch-level gather — all S step batches (K2)."""
+        st = self.stream if stream is None else stream
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(self.stream)
-        pr.shard_indices(self.alloc, self.rank, epoch, self.cfg.seed, self.idx, stream=self.stream)
+        e0.record(st)
+        pr.shard_indices(self.alloc, self.rank, epoch, self.cfg.seed, self.idx, stream=st)
         self.launches += 1
         xe = ye = None
         if self.cfg.gather == "epoch":
-            xe, ye = self.gather(0, S * n_r, record)
-        e1.record(self.stream)
+            xe, ye = self.gather(0, S * n_r, record, stream=st)
+        e1.record(st)
+        self._idx_free = torch.cuda.Event()           # self.idx is free for the next shard once this has run
+        self._idx_free.record(st)
         return xe, ye, e0, e1
 
     def run_epoch(self, record=False, loss_to_host=False):
@@ -417,6 +422,10 @@ class Worker:
         pre, self._prefetched = getattr(self, "_prefetched", None), None
         if pre is not None and pre[0] == (self.epoch, n_r):
             xe, ye, e0, e1 = pre[1]                           # enqueued at the end of the previous epoch
+            if pre[2] is not None:                            # ... on the side stream: join it here
+                self.stream.wait_event(pre[2])
+                xe.record_stream(self.stream)
+                ye.record_stream(self.stream)
         else:
             xe, ye, e0, e1 = self._data(self.epoch, n_r, S, record)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
@@ -444,7 +453,18 @@ class Worker:
         if cfg.gather == "epoch" and v["frozen"]:
             # frozen allocation: the next epoch's shard cannot change at the boundary, so its K1 + K2
             # are enqueued now and run while the host synchronises for t_s and runs the controller
-            self._prefetched = ((self.epoch + 1, n_r), self._data(self.epoch + 1, n_r, S, record))
+            if cfg.host_data:
+                # rows come over PCIe (e2e): gather the next epoch on a side stream, beside this epoch's steps
+                # (the host is ahead of the GPU here; the side stream only waits for the last use of idx)
+                if not hasattr(self, "_side"):
+                    self._side = torch.cuda.Stream(self.dev)
+                self._side.wait_event(self._idx_free)
+                data = self._data(self.epoch + 1, n_r, S, record, stream=self._side)
+                done = torch.cuda.Event()
+                done.record(self._side)
+                self._prefetched = ((self.epoch + 1, n_r), data, done)
+            else:
+                self._prefetched = ((self.epoch + 1, n_r), self._data(self.epoch + 1, n_r, S, record), None)
         ev[-1][1].synchronize()
         while loss_to_host and getattr(self, "_pending", None):
             self._read_loss(host_losses)
