@@ -209,8 +209,19 @@ class Worker:
             ev = self._bucket_ev[self._next]
             ev.record(torch.cuda.current_stream(self.dev))
             self.comm_stream.wait_event(ev)
-            pr.weighted_allreduce(self.comm, self.flat[lo:hi], self._n_armed, stream=self.comm_stream)
+            self._bucket_call(lo, hi, self._n_armed, self.comm_stream)
             self._next += 1
+
+    def _bucket_call(self, lo, hi, n, stream):
+        """One bucket's a6-a8 — or, with the flat [grad | θ] region, a6-a9 fused (K7 inside K3): the bucket's
+        layers have finished their backward on every rank (the handshake waits for all), so their θ can be
+        updated while backward continues on earlier layers (which never read these weights again; the
+        forward's bf16 weight copies are what backward saved)."""
+        if self.pflat is not None:
+            pr.weighted_allreduce_sgd(self.comm, self.flat[lo:hi], self.pflat[lo:hi], n, self.cfg.lr, self.cfg.wd,
+                                      zero_grad=True, stream=stream)
+        else:
+            pr.weighted_allreduce(self.comm, self.flat[lo:hi], n, stream=stream)
 
     # ---- a3: data movement --------------------------------------------------------------------------
     def gather(self, first: int, rows: int, record=False, stream=None):
@@ -354,7 +365,7 @@ class Worker:
     def allreduce_and_update(self, n_r: int, record=False):
         if self._overlap and n_r == 0:                        # N1: an idle rank still joins every bucket
             for lo, hi, _ in self._buckets:
-                pr.weighted_allreduce(self.comm, self.flat[lo:hi], 0, stream=self.stream)
+                self._bucket_call(lo, hi, 0, self.stream)
                 self.launches += 1
         elif self.P > 1 and not self._overlap:
             if record:
@@ -372,6 +383,8 @@ class Worker:
                 self.ar_events.append((a0, a1))
             if self.pflat is not None:
                 return
+        if self._overlap and self.pflat is not None:
+            return                                            # every bucket's update ran fused with its allreduce
         if self.pflat is not None:
             if record:
                 u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
