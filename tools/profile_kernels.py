@@ -62,7 +62,7 @@ def sgd(reps, L=11_689_512):
     print(f"sgd L={L}: {us:.2f} us, {16 * L / us / 1e3:.1f} GB/s algorithmic")
 
 
-def ring_fused(reps, P=8, L=11_689_512):
+def ring_fused(reps, P=8, L=11_689_512, only_fused=False):
     """Rows a6-a9: composed (K3 ring + K7 per rank) vs fused (K7 inside K3), 8 ranks co-located."""
     comms = pr.comm_init_local(P, 0)
     store = [torch.randn(2 * L, device="cuda") for _ in range(P)]
@@ -77,6 +77,11 @@ def ring_fused(reps, P=8, L=11_689_512):
     def fused():
         pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 1e-6, 0.0, zero_grad=False)
 
+    if only_fused:
+        print(f"a6-a9 fused P={P} L={L}: {timed(fused, reps):.1f} us")
+        for c in comms:
+            c.destroy()
+        return
     uc, uf = timed(composed, reps), timed(fused, reps)
     print(f"a6-a9 P={P} L={L}: composed (ring + {P}x K7) {uc:.1f} us, fused {uf:.1f} us")
     for c in comms:
@@ -115,5 +120,7 @@ if __name__ == "__main__":
         sgd(reps)
     if what in ("ring_fused", "all"):
         ring_fused(reps)
+    if what == "ring_fused_only":
+        ring_fused(reps, only_fused=True)
     if what in ("ring", "all"):
         ring(reps)

@@ -88,7 +88,7 @@ def main():
                 lines.append("| top stall reasons (cycles/instr) | " + ", ".join(f"{n} {x:.1f}" for x, n in st) + " |")
             lines.append("")
             kind = ("gather" if "gather" in kname else "sgd" if "sgd_kernel" in kname else
-                    "ring_ll" if "ring_ll" in kname else
+                    "ring_ll" if "ring_ll" in kname else "ring_fused" if "ring_kernel<float, 1>" in kname else
                     "twoshot" if "twoshot" in kname else "ring_colocated" if "ring" in kname else
                     "permute" if "permute" in kname else name)
             if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d:
