@@ -274,9 +274,6 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 }
 // generic-proxy writes (peer stores observed through an acquire) -> visible to the async proxy (TMA)
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 struct Shared {
     int err;
@@ -1391,63 +1388,48 @@ int pick_algo(const pr_comm_config& cfg, int64_t count, int32_t dtype) {
     return PR_ALGO_RING;
 }
 
+// One launch of a K3 variant: grid (channels, ranks in this launch); cooperative for local groups (all P
+// ranks' CTAs must be co-resident).
+int launch_k3(void* fn, const LaunchArgs& a, int nranks, int channels, int block, size_t smem, cudaStream_t s,
+              bool coop) {
+    void* args[] = {(void*)&a};
+    const dim3 grid((unsigned)channels, (unsigned)nranks), blk((unsigned)block);
+    if (coop) {
+        PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, blk, args, smem, s));
+    } else {
+        PR_CUDA_TRY(cudaLaunchKernel(fn, grid, blk, args, smem, s));
+    }
+    return PR_OK;
+}
+
 int launch_ring(const LaunchArgs& a, int nranks, const pr_comm_config& cfg, cudaStream_t s, bool coop) {
     const int32_t threads = cfg.threads, channels = cfg.channels;
-    // algorithm: a pure function of (config, count, dtype), identical on every rank
-    const int64_t bytes = a.count * (a.dtype == PR_DTYPE_F32 ? 4 : 2);
-    if (a.fuse) goto ring;   // the fused update exists in the TMA ring only (callers check pick_algo)
-    if ((cfg.algo == PR_ALGO_ONESHOT || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.os_max_bytes) {
-        void* fn4 = (a.dtype == PR_DTYPE_F32) ? (void*)oneshot_ll_kernel<float> : (void*)oneshot_ll_kernel<__nv_bfloat16>;
-        void* args4[] = {(void*)&a};
-        const dim3 grid4((unsigned)channels, (unsigned)nranks), block4((unsigned)threads);
-        if (coop) {
-            PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn4, grid4, block4, args4, 0, s));
-        } else {
-            PR_CUDA_TRY(cudaLaunchKernel(fn4, grid4, block4, args4, 0, s));
-        }
-        return PR_OK;
+    const bool f32 = a.dtype == PR_DTYPE_F32;
+    // the fused update (K7 inside K3) exists in the TMA ring only (its callers check pick_algo)
+    const int algo = a.fuse ? PR_ALGO_RING : pick_algo(cfg, a.count, a.dtype);
+    switch (algo) {
+        case PR_ALGO_ONESHOT:
+            return launch_k3(f32 ? (void*)oneshot_ll_kernel<float> : (void*)oneshot_ll_kernel<__nv_bfloat16>, a, nranks,
+                             channels, threads, 0, s, coop);
+        case PR_ALGO_LL:
+            return launch_k3(f32 ? (void*)ring_ll_kernel<float> : (void*)ring_ll_kernel<__nv_bfloat16>, a, nranks,
+                             channels, threads, 0, s, coop);
+        case PR_ALGO_TWO_SHOT:
+            return launch_k3(f32 ? (void*)twoshot_kernel<float> : (void*)twoshot_kernel<__nv_bfloat16>, a, nranks,
+                             channels, threads, 0, s, coop);
+        default: break;
     }
-    if ((cfg.algo == PR_ALGO_LL || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.ll_max_bytes) {
-        void* fn3 = (a.dtype == PR_DTYPE_F32) ? (void*)ring_ll_kernel<float> : (void*)ring_ll_kernel<__nv_bfloat16>;
-        void* args3[] = {(void*)&a};
-        const dim3 grid3((unsigned)channels, (unsigned)nranks), block3((unsigned)threads);
-        if (coop) {
-            PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn3, grid3, block3, args3, 0, s));
-        } else {
-            PR_CUDA_TRY(cudaLaunchKernel(fn3, grid3, block3, args3, 0, s));
-        }
-        return PR_OK;
-    }
-    if (cfg.algo == PR_ALGO_TWO_SHOT || (cfg.algo == PR_ALGO_AUTO && bytes <= cfg.ts_max_bytes)) {
-        void* fn2 = (a.dtype == PR_DTYPE_F32) ? (void*)twoshot_kernel<float> : (void*)twoshot_kernel<__nv_bfloat16>;
-        void* args2[] = {(void*)&a};
-        const dim3 grid2((unsigned)channels, (unsigned)nranks), block2((unsigned)threads);
-        if (coop) {
-            PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn2, grid2, block2, args2, 0, s));
-        } else {
-            PR_CUDA_TRY(cudaLaunchKernel(fn2, grid2, block2, args2, 0, s));
-        }
-        return PR_OK;
-    }
-ring:
     void* fn = a.fuse ? (void*)ring_kernel<float, true>
-                      : (a.dtype == PR_DTYPE_F32) ? (void*)ring_kernel<float, false> : (void*)ring_kernel<__nv_bfloat16, false>;
+                      : f32 ? (void*)ring_kernel<float, false> : (void*)ring_kernel<__nv_bfloat16, false>;
     const size_t smem = (size_t)cfg.stages * 2 * cfg.tile_bytes;
     static size_t attr_set[3] = {0, 0, 0};
-    const int di = a.fuse ? 2 : (a.dtype == PR_DTYPE_F32 ? 0 : 1);
+    const int di = a.fuse ? 2 : (f32 ? 0 : 1);
     if (attr_set[di] < smem) {
         PR_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set[di] = smem;
     }
-    void* args[] = {(void*)&a};
     // producer warp + signal warp + `threads` consumer threads per channel CTA
-    const dim3 grid((unsigned)channels, (unsigned)nranks), block((unsigned)(threads + 64));
-    if (coop) {
-        PR_CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, s));
-    } else {
-        PR_CUDA_TRY(cudaLaunchKernel(fn, grid, block, args, smem, s));
-    }
-    return PR_OK;
+    return launch_k3(fn, a, nranks, channels, threads + 64, smem, s, coop);
 }
 
 }  // namespace
