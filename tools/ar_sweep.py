@@ -89,14 +89,14 @@ def run_colocated(P, max_mib, reps, algo=0):
         c.destroy()
 
 
-def run_multi(max_mib, reps, algo=0):
+def run_multi(max_mib, reps, algo=0, channels=16):
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, P = dist.get_rank(), dist.get_world_size()
-    comm = pr.comm_init(rank, P, local, config=pr.comm_config(algo=algo))
+    comm = pr.comm_init(rank, P, local, config=pr.comm_config(algo=algo, channels=channels))
     n = weights(P)
     s = n[rank] / sum(n)
     Zmax = max_mib << 20
@@ -153,8 +153,9 @@ if __name__ == "__main__":
     ap.add_argument("--max-mib", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--algo", type=int, default=0, help="0 ring, 1 two-shot, 2 auto, 3 LL ring, 4 one-shot LL")
+    ap.add_argument("--channels", type=int, default=16, help="CTAs per rank (multi-GPU mode)")
     a = ap.parse_args()
     if a.colocated:
         run_colocated(a.colocated, a.max_mib, a.reps, a.algo)
     else:
-        run_multi(a.max_mib, a.reps, a.algo)
+        run_multi(a.max_mib, a.reps, a.algo, a.channels)

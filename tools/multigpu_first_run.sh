@@ -16,6 +16,11 @@ for P in 2 4 8; do
   timeout 1200 $TR --nproc-per-node $P --master-port $((29620 + P)) bench.py --gpus $P --steps 5 --warmup 3 --overlap \
       --no-cpu-baseline > gpurun_out/mg_bench_overlap_p$P.json 2> gpurun_out/mg_bench_overlap_p$P.err
 done
+# ring channel count (CTAs per rank) at the largest P: 16 is the co-located optimum, NVLink may want more
+for ch in 8 24 32 48; do
+  timeout 900 $TR --nproc-per-node $G --master-port $((29650 + ch)) tools/ar_sweep.py --max-mib 256 --channels $ch \
+      > gpurun_out/mg_ar_sweep_ch${ch}_p$G.jsonl 2> gpurun_out/mg_ar_sweep_ch${ch}_p$G.err
+done
 # AUTO (one-shot / LL / two-shot / ring by size) at the largest P
 timeout 1200 $TR --nproc-per-node $G --master-port 29630 tools/ar_sweep.py --max-mib 64 --algo 2 \
     > gpurun_out/mg_ar_sweep_auto_p$G.jsonl 2> gpurun_out/mg_ar_sweep_auto_p$G.err
