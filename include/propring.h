@@ -201,15 +201,19 @@ typedef struct pr_comm pr_comm;
 #define PR_COMM_FLAG_SYS_SCOPE    2   /* system-scope release/acquire even when every rank shares one GPU
                                          (by default .gpu scope is used exactly when that is the case) */
 
+/* Fields marked (topology) may be 0 = chosen at init from where the ranks are: all on one GPU (local
+ * groups, co-located processes) -> the HBM-bound optimum; on different GPUs -> more channels with larger
+ * tiles and slots, since each rank then has only its own channels' SMs. */
 typedef struct {
-    int32_t channels;     /* ring channels = CTAs per rank (default 16)                               */
+    int32_t channels;     /* ring channels = CTAs per rank (topology: 16 one GPU / 32 across GPUs)    */
     int32_t slots;        /* staging slots per channel, >= 2 (default 8)                    */
     int32_t threads;      /* consumer threads per CTA, <= 512 (default 512)                                         */
     int32_t flags;        /* PR_COMM_FLAG_* (default 0)                                                */
-    int64_t slot_bytes;   /* bytes per staging slot, multiple of 256 (default 262144)                 */
+    int64_t slot_bytes;   /* bytes per staging slot, multiple of 256 (topology: 256 KiB / 1 MiB)      */
     int64_t watchdog_ns;  /* spin-wait deadline per call (default 10 s); <= 0 disables               */
-    int32_t stages;       /* TMA smem pipeline depth per CTA, 2..16 (default 6)                       */
-    int32_t tile_bytes;   /* bytes per input per pipeline stage, multiple of 16, <= 32768 (default 16384) */
+    int32_t stages;       /* TMA smem pipeline depth per CTA, 2..16 (topology: 6 / 4)                 */
+    int32_t tile_bytes;   /* bytes per input per pipeline stage, multiple of 16, <= 32768 (topology:
+                             16 KiB / 24 KiB)                                                         */
     int32_t algo;         /* PR_ALGO_* (default PR_ALGO_RING)                                         */
     int32_t ts_slots;     /* two-shot staging slots per (channel, source), >= 2 (default 2)          */
     int64_t ts_slot_bytes;/* two-shot slice bytes, multiple of 256 (default 65536)                   */

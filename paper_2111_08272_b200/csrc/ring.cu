@@ -552,6 +552,8 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
         if (t0) {
             unsigned long long prodJ = st->slot_base, consJ = st->slot_base, agC = st->ag_base;
             uint32_t tc = 0;
+            int stg = 0;
+            uint32_t eph = 1;   // parity of the `empty` phase a reuse of stage stg waits for (first use: none)
             bool bad = false;
             for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
                 int64_t lo, len;
@@ -573,8 +575,9 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 const T* isrc = (kind == K_AGMID && direct) ? th + lo
                                                             : reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ));
                 for (int64_t t = 0; t < nt; ++t, ++tc) {
-                    const int stg = (int)(tc % (uint32_t)kStages);
-                    if (tc >= (uint32_t)kStages) mbar_wait(&sh.empty[stg], ((tc / (uint32_t)kStages) - 1) & 1);
+                    // stage / phase maintained incrementally: a runtime `%` and `/` per tile on this one
+                    // thread were a measurable share of its serial per-tile issue time
+                    if (tc >= (uint32_t)kStages) mbar_wait(&sh.empty[stg], eph);
                     const int64_t e0 = t * te;
                     const int64_t ne = min(te, len - e0);
                     const uint32_t vb = (uint32_t)((ne * (int64_t)sizeof(T)) & ~15ll);   // whole 16 B vectors
@@ -591,6 +594,10 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                         if (needs_in(kind)) tma_load(is, isrc + e0, vb, &sh.full[stg]);
                     }
                     mbar_arrive_expect_tx(&sh.full[stg], tx);
+                    if (++stg == kStages) {
+                        stg = 0;
+                        eph ^= 1u;
+                    }
                 }
                 if (reads_slot(kind)) ++consJ;
                 if (writes_slot(kind)) ++prodJ;
@@ -605,22 +612,26 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
         // every consumer warp), then one sys-scope release makes the whole slice visible to the peer.
         if (threadIdx.x == 32) {
             unsigned long long prodJ = st->slot_base, agP = st->ag_base;
-            uint32_t tc = 0;
+            int stg = 0;
+            uint32_t ph = 0;
             for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
                 int64_t lo, len;
                 range(c, i, lo, len);
                 const int64_t nt = ntiles(kind, len);
                 const bool sends = sends_ag(kind) || writes_slot(kind);
                 bool ok = true;
-                for (int64_t t = 0; t < nt; ++t, ++tc) {
-                    const int stg = (int)(tc % (uint32_t)kStages);
+                for (int64_t t = 0; t < nt; ++t) {
                     // wait for EVERY tile's phase: try_wait.parity cannot tell phase k+1 from k−1, so a
                     // skipped phase would let a later wait on this stage return early (found by synccheck)
-                    mbar_wait(&sh.stored[stg], (tc / (uint32_t)kStages) & 1);
+                    mbar_wait(&sh.stored[stg], ph);
                     ok = ok && sh.tile_ok[stg] != 0;
                     // stage free: consumers read it before arriving on `stored`; the chain consumer ->
                     // stored -> signal -> empty -> producer is transitive (release/acquire at each step)
                     mbar_arrive(&sh.empty[stg]);
+                    if (++stg == kStages) {
+                        stg = 0;
+                        ph ^= 1u;
+                    }
                     if (t == nt - 1 && sends && ok) {
                         if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
                         else st_release(&nxf->rs_ready, prodJ + 1, sys);
@@ -639,7 +650,8 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
         const int cid = threadIdx.x - 64;
         const int lane = threadIdx.x & 31;
         unsigned long long prodJ = st->slot_base, consJ = st->slot_base;
-        uint32_t tc = 0;
+        int stg = 0;
+        uint32_t ph = 0;
         for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
             int64_t lo, len;
             range(c, i, lo, len);
@@ -659,9 +671,8 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
             const bool zg = FUSE && A.zero && kind <= K_LAST;        // own gradient consumed: reset it
             const bool ng = needs_g(kind), ni = needs_in(kind);
             bool ok = true;
-            for (int64_t t = 0; t < nt; ++t, ++tc) {
-                const int stg = (int)(tc % (uint32_t)kStages);
-                mbar_wait(&sh.full[stg], (tc / (uint32_t)kStages) & 1);
+            for (int64_t t = 0; t < nt; ++t) {
+                mbar_wait(&sh.full[stg], ph);
                 ok = sh.tile_ok[stg] != 0;
                 if (ok && t == nt - 1 && reads_slot(kind) && cid == 0)   // slot landed in smem: hand it back
                     st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);     // (ordered after the TMA reads by the wait)
@@ -700,6 +711,10 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 __syncwarp();
                 if (lane == 0) {
                     mbar_arrive(&sh.stored[stg]);   // release.cta: this warp's smem reads and stores precede
+                }
+                if (++stg == kStages) {
+                    stg = 0;
+                    ph ^= 1u;
                 }
             }
             const bool err = *(volatile int*)&sh.err != 0;
@@ -1250,14 +1265,14 @@ namespace {
 
 pr_comm_config default_config() {
     pr_comm_config c;
-    c.channels = 16;
+    c.channels = 0;          // topology (resolve_config)
     c.slots = 8;
     c.threads = 512;
     c.flags = 0;
-    c.slot_bytes = 256 * 1024;
+    c.slot_bytes = 0;        // topology
     c.watchdog_ns = 10ll * 1000 * 1000 * 1000;
-    c.stages = 6;
-    c.tile_bytes = 16384;
+    c.stages = 0;            // topology
+    c.tile_bytes = 0;        // topology
     c.algo = PR_ALGO_RING;
     c.ts_slots = 2;
     c.ts_slot_bytes = 64 * 1024;
@@ -1265,6 +1280,20 @@ pr_comm_config default_config() {
     c.ll_max_bytes = 256 * 1024;
     c.os_max_bytes = 64 * 1024;
     return c;
+}
+
+// Topology defaults for the fields a caller leaves 0 (channels, stages, tile_bytes, slot_bytes).  Same GPU
+// (co-located ranks share the HBM and the SMs): 16 channels of 6 × 16 KiB stages, 256 KiB slots — the
+// HBM-bound optimum of tools/sweep_ring.py.  Ranks on different GPUs: each rank has only its own
+// channels' SMs, and a channel CTA moves ≈ 22-27 GB/s of bus bandwidth (its SM↔L2 traffic is ≈ 3.5
+// bytes per bus byte; tools/sweep_cta.py, P = 2 co-located with HBM far from saturated), so 770 GB/s per
+// direction needs > 30 of them: 32 channels of 4 × 24 KiB stages and 1 MiB slots (≈ 780-800 GB/s
+// bus-equivalent per rank in that proxy).
+void resolve_config(pr_comm_config& c, bool cross_gpu) {
+    if (c.channels == 0) c.channels = cross_gpu ? 32 : 16;
+    if (c.stages == 0) c.stages = cross_gpu ? 4 : 6;
+    if (c.tile_bytes == 0) c.tile_bytes = cross_gpu ? 24576 : 16384;
+    if (c.slot_bytes == 0) c.slot_bytes = cross_gpu ? (1ll << 20) : (256 * 1024);
 }
 
 int check_config(const pr_comm_config& c) {
@@ -1441,6 +1470,20 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
     if (!c) return PR_ERR_INTERNAL;
     c->rank = rank; c->P = P; c->device = device; c->fn = fn; c->ctx = ctx;
     c->cfg = cfg ? *cfg : default_config();
+    // probe exchange: are the ranks on different GPUs?  (decides the topology defaults of fields left 0)
+    struct Probe {
+        unsigned char uuid[16];
+    } mine{}, *probes = nullptr;
+    {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) std::memcpy(mine.uuid, &prop.uuid, 16);
+    }
+    std::vector<Probe> all_probe(P);
+    probes = all_probe.data();
+    if (int xrc = exchange(c, &mine, sizeof(Probe), probes)) { free_comm(c); return xrc; }
+    bool cross = false;
+    for (int q = 0; q < P; ++q) cross = cross || std::memcmp(probes[q].uuid, mine.uuid, 16) != 0;
+    resolve_config(c->cfg, cross);
     int rc = check_config(c->cfg);
     if (!rc) rc = alloc_common(c);
     Hello me;
@@ -1502,7 +1545,8 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
 
 extern "C" int pr_comm_init_local(pr_comm** out, int32_t P, int32_t device, const pr_comm_config* cfg) {
     if (!out || P < 1 || P > PR_MAX_RANKS || device < 0) return PR_ERR_INVALID;
-    const pr_comm_config cf = cfg ? *cfg : default_config();
+    pr_comm_config cf = cfg ? *cfg : default_config();
+    resolve_config(cf, false);                                    // one device
     if (int rc = check_config(cf)) return rc;
     std::vector<pr_comm*> cs(P, nullptr);
     int rc = PR_OK;

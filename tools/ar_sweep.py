@@ -89,7 +89,7 @@ def run_colocated(P, max_mib, reps, algo=0):
         c.destroy()
 
 
-def run_multi(max_mib, reps, algo=0, channels=16):
+def run_multi(max_mib, reps, algo=0, channels=0):
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -153,7 +153,7 @@ if __name__ == "__main__":
     ap.add_argument("--max-mib", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--algo", type=int, default=0, help="0 ring, 1 two-shot, 2 auto, 3 LL ring, 4 one-shot LL")
-    ap.add_argument("--channels", type=int, default=16, help="CTAs per rank (multi-GPU mode)")
+    ap.add_argument("--channels", type=int, default=0, help="CTAs per rank (multi-GPU mode; 0 = topology default)")
     a = ap.parse_args()
     if a.colocated:
         run_colocated(a.colocated, a.max_mib, a.reps, a.algo)

@@ -17,7 +17,7 @@ for P in 2 4 8; do
       --no-cpu-baseline > gpurun_out/mg_bench_overlap_p$P.json 2> gpurun_out/mg_bench_overlap_p$P.err
 done
 # ring channel count (CTAs per rank) at the largest P: 16 is the co-located optimum, NVLink may want more
-for ch in 8 24 32 48; do
+for ch in 16 24 32 48 64; do
   timeout 900 $TR --nproc-per-node $G --master-port $((29650 + ch)) tools/ar_sweep.py --max-mib 256 --channels $ch \
       > gpurun_out/mg_ar_sweep_ch${ch}_p$G.jsonl 2> gpurun_out/mg_ar_sweep_ch${ch}_p$G.err
 done
