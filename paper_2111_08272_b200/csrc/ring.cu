@@ -439,6 +439,26 @@ template <> __device__ __forceinline__ uint4 sgd_v4<float>(uint4 t, uint4 g, flo
 }
 template <> __device__ __forceinline__ uint4 sgd_v4<__nv_bfloat16>(uint4, uint4 g, float, float) { return g; }
 
+// The consumers' per-tile inner loop with the hop's arithmetic fixed at compile time: a runtime `mode`
+// inside the loop compiled to a branch + reconvergence per element (≈ 50 instructions per 16-byte vector
+// in the ncu source view of a CTA-bound run); with MODE constant it is ≈ 15 (2 LDS, 4 FFMA, 1-3 STG).
+// out1/out2/zg/thp are already offset to the tile's first element; out2, zg, thp may be null (uniform).
+template <typename T, int MODE, bool FUSE>
+__device__ __forceinline__ void tile_vectors(const uint4* __restrict__ gs, const uint4* __restrict__ is, int nv, int cid,
+                                             int nc, float s, T* out1, T* out2, T* zg, const T* thp, float nlr,
+                                             float wd) {
+    constexpr int V = Vec<T>::V;
+    for (int v = cid; v < nv; v += nc) {
+        const uint4 a = (MODE == M_SCALE || MODE == M_FMA) ? gs[v] : make_uint4(0, 0, 0, 0);
+        const uint4 b = (MODE == M_FMA || MODE == M_COPY) ? is[v] : make_uint4(0, 0, 0, 0);
+        uint4 y = Vec<T>::op(MODE, s, a, b);
+        if (FUSE && thp) y = sgd_v4<T>(*reinterpret_cast<const uint4*>(thp + (int64_t)v * V), y, nlr, wd);
+        if (FUSE && zg) st_v4(zg + (int64_t)v * V, make_uint4(0, 0, 0, 0));
+        st_v4(out1 + (int64_t)v * V, y);
+        if (out2) st_v4(out2 + (int64_t)v * V, y);
+    }
+}
+
 // FUSE (compile time): the K7-fused variant; the plain ring is compiled without any of its code.
 template <typename T, bool FUSE>
 __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ LaunchArgs A) {
@@ -682,14 +702,20 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 const uint4* gs = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes);
                 const uint4* is = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes + kTileBytes);
                 if (ok) {
-                    for (int64_t v = cid; v < nv; v += nc) {
-                        const uint4 a = ng ? gs[v] : make_uint4(0, 0, 0, 0);
-                        const uint4 b = ni ? is[v] : make_uint4(0, 0, 0, 0);
-                        uint4 y = Vec<T>::op(mode, s, a, b);
-                        if (upd) y = sgd_v4<T>(*reinterpret_cast<const uint4*>(th + lo + e0 + v * V), y, A.nlr, A.wd);
-                        if (zg) st_v4(buf + lo + e0 + v * V, make_uint4(0, 0, 0, 0));
-                        st_v4(out1 + e0 + v * V, y);
-                        if (out2) st_v4(out2 + e0 + v * V, y);
+                    {
+                        T* o1 = out1 + e0;
+                        T* o2 = out2 ? out2 + e0 : nullptr;
+                        T* zp = zg ? buf + lo + e0 : nullptr;
+                        const T* tp = upd ? th + lo + e0 : nullptr;
+                        const int inv = (int)nv;
+                        // (ng / ni follow from the mode: SCALE reads g, FMA reads g and the received
+                        // slice, COPY the received slice, ZERO nothing)
+                        switch (mode) {
+                            case M_SCALE: tile_vectors<T, M_SCALE, FUSE>(gs, is, inv, cid, nc, s, o1, o2, zp, tp, A.nlr, A.wd); break;
+                            case M_FMA: tile_vectors<T, M_FMA, FUSE>(gs, is, inv, cid, nc, s, o1, o2, zp, tp, A.nlr, A.wd); break;
+                            case M_COPY: tile_vectors<T, M_COPY, FUSE>(gs, is, inv, cid, nc, s, o1, o2, zp, tp, A.nlr, A.wd); break;
+                            default: tile_vectors<T, M_ZERO, FUSE>(gs, is, inv, cid, nc, s, o1, o2, zp, tp, A.nlr, A.wd); break;
+                        }
                     }
                     for (int64_t e = nv * V + cid; e < ne; e += nc) {   // ragged tail: end of the buffer only
                         const float gv = ng ? Vec<T>::to_f(Vec<T>::ld(gsrc + e0 + e)) : 0.0f;
@@ -1287,12 +1313,12 @@ pr_comm_config default_config() {
 // HBM-bound optimum of tools/sweep_ring.py.  Ranks on different GPUs: each rank has only its own
 // channels' SMs, and a channel CTA moves ≈ 22-27 GB/s of bus bandwidth (its SM↔L2 traffic is ≈ 3.5
 // bytes per bus byte; tools/sweep_cta.py, P = 2 co-located with HBM far from saturated), so 770 GB/s per
-// direction needs > 30 of them: 32 channels of 4 × 24 KiB stages and 1 MiB slots (≈ 780-800 GB/s
+// direction needs > 30 of them: 32 channels of 6 × 16 KiB stages and 1 MiB slots (≈ 860 GB/s
 // bus-equivalent per rank in that proxy).
 void resolve_config(pr_comm_config& c, bool cross_gpu) {
     if (c.channels == 0) c.channels = cross_gpu ? 32 : 16;
-    if (c.stages == 0) c.stages = cross_gpu ? 4 : 6;
-    if (c.tile_bytes == 0) c.tile_bytes = cross_gpu ? 24576 : 16384;
+    if (c.stages == 0) c.stages = 6;
+    if (c.tile_bytes == 0) c.tile_bytes = 16384;
     if (c.slot_bytes == 0) c.slot_bytes = cross_gpu ? (1ll << 20) : (256 * 1024);
 }
 
