@@ -459,6 +459,79 @@ __device__ __forceinline__ void tile_vectors(const uint4* __restrict__ gs, const
     }
 }
 
+template <typename T>
+struct SliceArgs {
+    T* out1;                     // destination of the slice (next rank's slot, or a buffer)
+    T* out2;                     // second destination or null
+    T* zg;                       // fused: own gradient to reset, or null
+    const T* thp;                // fused: own θ of the reduced chunk, or null
+    const T* gsrc;               // own gradient of the slice (ragged tail only)
+    const T* isrc;               // received data of the slice (ragged tail only)
+    int64_t len, te, nt;         // slice elements, tile elements, tiles
+    float s, nlr, wd;
+    unsigned long long* credit;  // slot credit to return to the previous rank after the last tile (or null)
+    unsigned long long credit_val;
+    bool sys;
+};
+
+// Consumers' loop over one slice's tiles with the hop's arithmetic fixed (MODE).  Per tile: wait for the
+// TMA bytes, compute + store the full 16-byte vectors (tile_vectors), the ragged tail (only at the end of
+// the buffer), then one arrive per warp on `stored`.  Pointers advance by a tile; no per-tile branching on
+// the mode, no 64-bit multiplies (these dominated a CTA-bound run once the element loop was tight).
+template <typename T, int MODE, bool FUSE>
+__device__ __forceinline__ void consume_slice(Shared& sh, uint8_t* smem, int kTileBytes, int kStages, int& stg, uint32_t& ph,
+                                              int cid, int nc, int lane, const SliceArgs<T>& a) {
+    constexpr int V = Vec<T>::V;
+    T* o1 = a.out1;
+    T* o2 = a.out2;
+    T* zp = a.zg;
+    const T* tp = a.thp;
+    int64_t left = a.len;
+    for (int64_t t = 0; t < a.nt; ++t) {
+        mbar_wait(&sh.full[stg], ph);
+        const bool ok = sh.tile_ok[stg] != 0;
+        if (ok && t == a.nt - 1 && a.credit)   // slot landed in smem: hand it back (ordered after the TMA reads)
+            st_relaxed_u64(a.credit, a.credit_val, a.sys);
+        const int ne = (int)(left < a.te ? left : a.te);
+        const int nv = (ne * (int)sizeof(T)) / 16;
+        const uint4* gs = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes);
+        const uint4* is = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes + kTileBytes);
+        if (ok) {
+            tile_vectors<T, MODE, FUSE>(gs, is, nv, cid, nc, a.s, o1, o2, zp, tp, a.nlr, a.wd);
+            if (nv * V < ne) {                                      // ragged tail: end of the buffer only
+                const int64_t e0 = a.len - left;
+                for (int e = nv * V + cid; e < ne; e += nc) {
+                    const float gv = (MODE == M_SCALE || MODE == M_FMA) ? Vec<T>::to_f(Vec<T>::ld(a.gsrc + e0 + e)) : 0.0f;
+                    const float iv = (MODE == M_FMA || MODE == M_COPY) ? Vec<T>::to_f(Vec<T>::ld(a.isrc + e0 + e)) : 0.0f;
+                    float rr;
+                    if (MODE == M_SCALE) rr = __fmul_rn(a.s, gv);
+                    else if (MODE == M_FMA) rr = __fmaf_rn(a.s, gv, iv);
+                    else rr = (MODE == M_COPY) ? iv : 0.0f;
+                    T y = (MODE == M_COPY) ? Vec<T>::ld(a.isrc + e0 + e) : Vec<T>::from_f(rr);
+                    if (FUSE && tp) {
+                        const float tv = Vec<T>::to_f(tp[e]);
+                        y = Vec<T>::from_f(__fmaf_rn(a.nlr, __fmaf_rn(a.wd, tv, Vec<T>::to_f(y)), tv));
+                    }
+                    if (FUSE && zp) Vec<T>::st(zp + e, Vec<T>::from_f(0.0f));
+                    Vec<T>::st(o1 + e, y);
+                    if (o2) Vec<T>::st(o2 + e, y);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.stored[stg]);   // release.cta: this warp's smem reads and stores precede
+        if (++stg == kStages) {
+            stg = 0;
+            ph ^= 1u;
+        }
+        left -= ne;
+        o1 += ne;
+        if (o2) o2 += ne;
+        if (FUSE && zp) zp += ne;
+        if (FUSE && tp) tp += ne;
+    }
+}
+
 // FUSE (compile time): the K7-fused variant; the plain ring is compiled without any of its code.
 template <typename T, bool FUSE>
 __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ LaunchArgs A) {
@@ -689,59 +762,14 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                                                         : reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ));
             const bool upd = FUSE && kind == K_LAST;                // reduced chunk final here: apply SGD
             const bool zg = FUSE && A.zero && kind <= K_LAST;        // own gradient consumed: reset it
-            const bool ng = needs_g(kind), ni = needs_in(kind);
-            bool ok = true;
-            for (int64_t t = 0; t < nt; ++t) {
-                mbar_wait(&sh.full[stg], ph);
-                ok = sh.tile_ok[stg] != 0;
-                if (ok && t == nt - 1 && reads_slot(kind) && cid == 0)   // slot landed in smem: hand it back
-                    st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);     // (ordered after the TMA reads by the wait)
-                const int64_t e0 = t * te;
-                const int64_t ne = min(te, len - e0);
-                const int64_t nv = (ne * (int64_t)sizeof(T)) / 16;
-                const uint4* gs = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes);
-                const uint4* is = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes + kTileBytes);
-                if (ok) {
-                    {
-                        T* o1 = out1 + e0;
-                        T* o2 = out2 ? out2 + e0 : nullptr;
-                        T* zp = zg ? buf + lo + e0 : nullptr;
-                        const T* tp = upd ? th + lo + e0 : nullptr;
-                        const int inv = (int)nv;
-                        // (ng / ni follow from the mode: SCALE reads g, FMA reads g and the received
-                        // slice, COPY the received slice, ZERO nothing)
-                        switch (mode) {
-                            case M_SCALE: tile_vectors<T, M_SCALE, FUSE>(gs, is, inv, cid, nc, s, o1, o2, zp, tp, A.nlr, A.wd); break;
-                            case M_FMA: tile_vectors<T, M_FMA, FUSE>(gs, is, inv, cid, nc, s, o1, o2, zp, tp, A.nlr, A.wd); break;
-                            case M_COPY: tile_vectors<T, M_COPY, FUSE>(gs, is, inv, cid, nc, s, o1, o2, zp, tp, A.nlr, A.wd); break;
-                            default: tile_vectors<T, M_ZERO, FUSE>(gs, is, inv, cid, nc, s, o1, o2, zp, tp, A.nlr, A.wd); break;
-                        }
-                    }
-                    for (int64_t e = nv * V + cid; e < ne; e += nc) {   // ragged tail: end of the buffer only
-                        const float gv = ng ? Vec<T>::to_f(Vec<T>::ld(gsrc + e0 + e)) : 0.0f;
-                        const float iv = ni ? Vec<T>::to_f(Vec<T>::ld(isrc + e0 + e)) : 0.0f;
-                        float rr;
-                        if (mode == M_SCALE) rr = __fmul_rn(s, gv);
-                        else if (mode == M_FMA) rr = __fmaf_rn(s, gv, iv);
-                        else rr = (mode == M_COPY) ? iv : 0.0f;
-                        T y = (mode == M_COPY) ? Vec<T>::ld(isrc + e0 + e) : Vec<T>::from_f(rr);
-                        if (upd) {
-                            const float tv = Vec<T>::to_f(th[lo + e0 + e]);
-                            y = Vec<T>::from_f(__fmaf_rn(A.nlr, __fmaf_rn(A.wd, tv, Vec<T>::to_f(y)), tv));
-                        }
-                        if (zg) Vec<T>::st(buf + lo + e0 + e, Vec<T>::from_f(0.0f));
-                        Vec<T>::st(out1 + e0 + e, y);
-                        if (out2) Vec<T>::st(out2 + e0 + e, y);
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&sh.stored[stg]);   // release.cta: this warp's smem reads and stores precede
-                }
-                if (++stg == kStages) {
-                    stg = 0;
-                    ph ^= 1u;
-                }
+            SliceArgs<T> sa{out1, out2, zg ? buf + lo : nullptr, upd ? th + lo : nullptr, gsrc, isrc, len, te, nt, s,
+                            A.nlr, A.wd, (reads_slot(kind) && cid == 0) ? &pvf->rs_credit : nullptr, consJ + 1, sys};
+            // the hop's arithmetic is fixed per instantiation: one switch per slice, none per tile / element
+            switch (mode) {
+                case M_SCALE: consume_slice<T, M_SCALE, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
+                case M_FMA: consume_slice<T, M_FMA, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
+                case M_COPY: consume_slice<T, M_COPY, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
+                default: consume_slice<T, M_ZERO, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
             }
             const bool err = *(volatile int*)&sh.err != 0;
             if (nt == 0 && reads_slot(kind) && cid == 0 && !err) st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);
