@@ -438,13 +438,38 @@ def colocated_allreduce(hbm, peak_kind, P=8, reps=20):
     composed_us = timed(composed)
     for c in comms:
         c.destroy()
+    # C1 (BASELINE configs[0]): the logistic-regression gradient (1,024 fp32 = 4 KiB), 2 ranks, n = [25, 75];
+    # AUTO takes the one-shot LL path; 20 calls captured in one CUDA graph = device time per call
+    c1 = pr.comm_init_local(2, torch.cuda.current_device(), pr.comm_config(algo=pr.ALGO_AUTO))
+    g1 = [torch.randn(1024, device="cuda") for _ in range(2)]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        pr.weighted_allreduce_local(c1, g1, [25, 75], stream=st)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=st):
+            for _ in range(20):
+                pr.weighted_allreduce_local(c1, g1, [25, 75], stream=st)
+    gr.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    c1_us = e0.elapsed_time(e1) / 20 * 1e3
+    del gr
+    for c in c1:
+        c.destroy()
     return {"kernel": "ring_kernel<float> (K3), all ranks on one GPU", "P": P, "bytes_per_rank": Z,
             "fused_a6_a9_us": fused_us, "composed_a6_a9_us": composed_us,
+            "c1_allreduce_4KiB_P2_us": c1_us,
             "n_local": n, "avg_us": t * 1e3, "bound": "hbm", "achieved": byts / (t * 1e-3) / 1e9, "peak": hbm,
             "unit": "GB/s", "frac": byts / (t * 1e-3) / 1e9 / hbm, "peak_kind": peak_kind,
             "algorithmic_bytes_per_call": byts,
             "note": "P virtual ranks co-resident on one GPU exercise the same kernel and protocol; peer stores "
-                    "land in local HBM, so this is an HBM roofline, not an NVLink number"}
+                    "land in local HBM, so this is an HBM roofline, not an NVLink number (the algorithmic bytes "
+                    "count every staging round trip at HBM, part of which the 126 MB L2 serves: frac can exceed 1)"}
 
 
 # ---------------------------------------------------------------------------------------------------
