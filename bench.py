@@ -11,7 +11,8 @@ aggregation steps of gather (a3, K2) -> ResNet-18 forward/backward with gradient
 -> weighted ring allreduce of the 11,689,512-element fp32 gradient (a6-a8, K3; identity at N=1) ->
 SGD (a9).  Workload: CIFAR-10-shaped synthetic data 50,000×3×32×32 u8 resident in HBM (153.6 MB >
 L2 126 MB, so every epoch streams it from HBM), global batch B = 1024 (g = 16, C = 64) split by the
-allocation; strong scaling across N.
+allocation at N = 1; across N weak scaling by default (1,024 samples per GPU per aggregation, C = 64·N,
+the epoch shrinks to 50,000 // (1,024·N) aggregations), --strong keeps B = 1,024 for every N.
 
 value   = whole-job samples/s over the K timed epochs (device time, CUDA events, max over ranks)
 e2e     = the same with the data set in pinned HOST memory: the gather reads every sampled row over
@@ -39,6 +40,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "epoch throughput (samples/s; epoch time = S·B/value) of the proportional-allocation + weighted-ring-allreduce training step"
 N_DATA, G_UNIT, C_UNITS = 50_000, 16, 64
+STRONG = "--strong" in sys.argv          # the oracle legs follow the same batch rule as the timed arm
 ROW_BYTES = 3 * 32 * 32
 L_RESNET18 = 11_689_512
 NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction (900 nominal)
@@ -58,6 +60,9 @@ def parse():
     ap.add_argument("--no-colocated", action="store_true")
     ap.add_argument("--data-n", type=int, default=N_DATA,
                     help="data-set rows (default 50,000; smaller only for profiling runs: S = N // 1024)")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: keep the global batch at 1,024 for every N (default: weak — 1,024 "
+                         "samples per GPU per aggregation, global batch 1,024·N)")
     ap.add_argument("--kernel-shares", action="store_true",
                     help="also report each library kernel's share of the timed step (live CUDA events)")
     return ap.parse_args()
@@ -147,7 +152,8 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = pr.comm_init(rank, world, local) if world > 1 else None
-    cfg = RunConfig(N=args.data_n, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024,
+    units = units_for(world, args.strong)
+    cfg = RunConfig(N=args.data_n, ratios=[1] * world, C=units, g=G_UNIT, adaptive=True, micro=1024,
                     overlap=args.overlap, bucket_mb=args.bucket_mb)
     wk = Worker(cfg, rank, world, local, comm)
 
@@ -242,7 +248,7 @@ def run_ours(args):
     # ---- e2e: host-resident data set, per-step loss read back --------------------------------------
     e2e = None
     if args.e2e_epochs > 0:
-        cfg_h = RunConfig(N=args.data_n, ratios=[1] * world, C=C_UNITS, g=G_UNIT, adaptive=True, micro=1024,
+        cfg_h = RunConfig(N=args.data_n, ratios=[1] * world, C=units, g=G_UNIT, adaptive=True, micro=1024,
                           host_data=True, overlap=args.overlap, bucket_mb=args.bucket_mb)
         wk_h = Worker(cfg_h, rank, world, local, comm, data=wk.X.cpu(), labels=wk.Y.cpu())
         wk_h.model.load_state_dict(wk.model.state_dict())
@@ -280,9 +286,10 @@ def run_ours(args):
         cpu = None if args.no_cpu_baseline else cpu_baseline(world)
         out = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_epoch, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_epoch, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": bench_config(world, bool(args.overlap and world > 1)),
+            "config": bench_config(world, bool(args.overlap and world > 1), args.strong),
             "epoch_time_s": ms_epoch / 1e3,
             "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
             "roofline_detail": roof,
@@ -322,12 +329,20 @@ def mix_ceiling():
         return None
 
 
-def bench_config(world, overlap=False):
+def units_for(world, strong=False):
+    """Allocation units C per aggregation: 64 units of g = 16 samples per GPU (weak scaling: 1,024 samples
+    per GPU per step at equal speeds), or 64 in total (strong: the global batch stays 1,024)."""
+    return C_UNITS if strong else C_UNITS * world
+
+
+def bench_config(world, overlap=False, strong=False):
     """The workload both arms name (our arm and --impl reference print the same config)."""
-    return {"workload": "resnet18-cifar10-shaped-50k, global batch 1024 (g=16, C=64), equal start, "
+    C = units_for(world, strong)
+    B = G_UNIT * C
+    return {"workload": f"resnet18-cifar10-shaped-50k, global batch {B} (g={G_UNIT}, C={C}), equal start, "
                         "self-adaptive allocation, fp32 gradients (11,689,512), bf16 autocast compute",
-            "model": "resnet18 (1000-class head, random init)", "global_batch": 1024,
-            "seq_len": None, "parallelism": f"dp{world}", "step": "one epoch (S=48 aggregations)",
+            "model": "resnet18 (1000-class head, random init)", "global_batch": B,
+            "seq_len": None, "parallelism": f"dp{world}", "step": f"one epoch (S={N_DATA // B} aggregations)",
             "overlap": overlap, "l2": "inputs larger than L2 (153.6 MB data set streamed every epoch)"}
 
 
@@ -486,7 +501,7 @@ def oracle_step(P, sample_rows, X, Y, grads, model, rank=0, a=None, epoch=0):
     from oracle import wavg as OW
 
     if a is None:
-        a = OA.alloc_init(N_DATA, [1] * P, C=C_UNITS, g=G_UNIT)
+        a = OA.alloc_init(N_DATA, [1] * P, C=units_for(P, STRONG), g=G_UNIT)
     n_r = a.n[rank]
     idx = OP.shard_indices(N_DATA, a.off[rank] + 0, min(a.len[rank], n_r), 1234, epoch)
     xb, yb = OG.gather_rows(X, idx[:sample_rows], OG.U8_TO_F32_AFFINE, scale=np.float32([1 / 51.5865, 1 / 50.847, 1 / 51.255]),
@@ -543,8 +558,9 @@ def run_reference(args):
     value = args.steps * sample_rows / dt
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": bench_config(args.gpus),
+           "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic",
+           "config": bench_config(args.gpus, False, args.strong),
            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "oracle",
                             "sample": f"bounded sample of the workload: each step = one aggregation step on "
                                       f"{sample_rows} rows (oracle shard + gather, torch-CPU fp32 ResNet-18 "

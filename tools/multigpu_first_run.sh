@@ -15,6 +15,8 @@ for P in 2 4 8; do
       > gpurun_out/mg_bench_p$P.json 2> gpurun_out/mg_bench_p$P.err
   timeout 1200 $TR --nproc-per-node $P --master-port $((29620 + P)) bench.py --gpus $P --steps 5 --warmup 3 --overlap \
       --no-cpu-baseline > gpurun_out/mg_bench_overlap_p$P.json 2> gpurun_out/mg_bench_overlap_p$P.err
+  timeout 1200 $TR --nproc-per-node $P --master-port $((29660 + P)) bench.py --gpus $P --steps 5 --warmup 3 --strong \
+      --no-cpu-baseline > gpurun_out/mg_bench_strong_p$P.json 2> gpurun_out/mg_bench_strong_p$P.err
 done
 # ring channel count (CTAs per rank) at the largest P: 16 is the co-located optimum, NVLink may want more
 for ch in 16 24 32 48 64; do
