@@ -476,9 +476,30 @@ def colocated_allreduce(hbm, peak_kind, P=8, reps=20):
     del gr
     for c in c1:
         c.destroy()
+    # per-rank CTA throughput with the cross-GPU configuration (32 channels, 1 MiB slots): 2 ranks on this
+    # GPU leave HBM far from saturated, so this is what one rank's channels can push — the bound a real
+    # NVLink run would face before the link's 770 GB/s (tools/sweep_cta.py)
+    cx = pr.comm_init_local(2, torch.cuda.current_device(), pr.comm_config(channels=32, slot_bytes=1 << 20))
+    Lx = (256 << 20) // 4
+    gx = [torch.randn(Lx, device="cuda") for _ in range(2)]
+    for _ in range(2):
+        pr.weighted_allreduce_local(cx, gx, [1, 2])
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(5):
+        pr.weighted_allreduce_local(cx, gx, [1, 2])
+    e1.record()
+    torch.cuda.synchronize()
+    x_us = e0.elapsed_time(e1) / 5 * 1e3
+    per_rank_bus = Lx * 4 * 2 * (2 - 1) / 2 / (x_us * 1e-6) / 1e9
+    del gx
+    for c in cx:
+        c.destroy()
     return {"kernel": "ring_kernel<float> (K3), all ranks on one GPU", "P": P, "bytes_per_rank": Z,
             "fused_a6_a9_us": fused_us, "composed_a6_a9_us": composed_us,
             "c1_allreduce_4KiB_P2_us": c1_us,
+            "cross_gpu_config_per_rank_busbw_equiv": {"GBs": per_rank_bus, "us": x_us, "bytes": Lx * 4, "P": 2,
+                                                      "channels": 32, "vs_nvlink_770": per_rank_bus / NVLINK_PEER_GBS},
             "n_local": n, "avg_us": t * 1e3, "bound": "hbm", "achieved": byts / (t * 1e-3) / 1e9, "peak": hbm,
             "unit": "GB/s", "frac": byts / (t * 1e-3) / 1e9 / hbm, "peak_kind": peak_kind,
             "algorithmic_bytes_per_call": byts,
