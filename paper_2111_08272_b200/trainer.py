@@ -224,12 +224,25 @@ class Worker:
             pr.weighted_allreduce(self.comm, self.flat[lo:hi], n, stream=stream)
 
     # ---- a3: data movement --------------------------------------------------------------------------
-    def gather(self, first: int, rows: int, record=False, stream=None):
-        """K2: rows [first, first+rows) of this rank's shard -> (x [rows, C·H·W], y [rows])."""
+    def gather(self, first: int, rows: int, record=False, stream=None, persistent=False):
+        """K2: rows [first, first+rows) of this rank's shard -> (x [rows, C·H·W], y [rows]).
+        persistent: write into one of two epoch buffers kept for the run (ping-pong: the next epoch's
+        prefetch never touches the buffer the current epoch reads), so no allocation happens per epoch."""
         st = self.stream if stream is None else stream
-        with torch.cuda.stream(st):                   # outputs allocated on (and owned by) the launching stream
-            x = torch.empty((max(rows, 1), self.row_bytes), dtype=self.xdt, device=self.dev)
-            y = torch.empty(max(rows, 1), dtype=torch.int64, device=self.dev)
+        if persistent:
+            if not hasattr(self, "_ebuf"):
+                self._ebuf, self._eflip = [None, None], 0
+            self._eflip ^= 1
+            b = self._ebuf[self._eflip]
+            if b is None or b[0].shape[0] < max(rows, 1):
+                b = (torch.empty((max(rows, 1), self.row_bytes), dtype=self.xdt, device=self.dev),
+                     torch.empty(max(rows, 1), dtype=torch.int64, device=self.dev))
+                self._ebuf[self._eflip] = b
+            x, y = b[0][:max(rows, 1)], b[1][:max(rows, 1)]
+        else:
+            with torch.cuda.stream(st):               # outputs allocated on (and owned by) the launching stream
+                x = torch.empty((max(rows, 1), self.row_bytes), dtype=self.xdt, device=self.dev)
+                y = torch.empty(max(rows, 1), dtype=torch.int64, device=self.dev)
         if rows > 0:
             if record:
                 g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -418,7 +431,7 @@ class Worker:
         self.launches += 1
         xe = ye = None
         if self.cfg.gather == "epoch":
-            xe, ye = self.gather(0, S * n_r, record, stream=st)
+            xe, ye = self.gather(0, S * n_r, record, stream=st, persistent=True)
         e1.record(st)
         self._idx_free = torch.cuda.Event()           # self.idx is free for the next shard once this has run
         self._idx_free.record(st)
@@ -437,8 +450,6 @@ class Worker:
             xe, ye, e0, e1 = pre[1]                           # enqueued at the end of the previous epoch
             if pre[2] is not None:                            # ... on the side stream: join it here
                 self.stream.wait_event(pre[2])
-                xe.record_stream(self.stream)
-                ye.record_stream(self.stream)
         else:
             xe, ye, e0, e1 = self._data(self.epoch, n_r, S, record)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
