@@ -18,8 +18,14 @@
 //   * monotone 64-bit counters (ready / credit / ag_ready) — never reset, so back-to-back calls and
 //     CUDA-graph replays need no host involvement; handshake entries are double-buffered by seq parity;
 //   * every spin has a %globaltimer deadline (watchdog) that latches PR_ERR_PEER_TIMEOUT.
-// Data path per slice: 16-byte vector loads (ld.global.cg: peer-written data bypasses the non-coherent
-// L1), fp32 math, RNE to the storage dtype, 16-byte vector stores to local and peer memory.
+// Data path per slice (ring_kernel): a producer warp polls the flags and TMA-loads the rank's own tile and
+// the received tile into a shared-memory ring; 16 consumer warps do the fp32 math (one instantiation per
+// hop arithmetic) and push 16-byte vectors to the peer; a signal warp publishes each slice's flag off the
+// data path.  The handshake is written in fence-free LL lines (seq | payload per 64-bit element).
+// Variants with the same bits: ring_ll_kernel (LL lines per hop, small buffers),
+// oneshot_ll_kernel (one hop, tiny buffers), twoshot_kernel (2 phases), and ring_kernel<float, true>
+// (K7's SGD fused into the last reduce-scatter hop; the all-gather carries θ').  Channel count, tile and
+// slot sizes default from the topology (resolve_config): CTAs per rank are the bound across GPUs.
 #include <cuda_bf16.h>
 
 #include <algorithm>
