@@ -182,11 +182,12 @@ def run_ours(args):
     e0.record()
     samples = 0
     recs = []
-    marks = []
+    marks, host_ms = [], []
     for _ in range(args.steps):
         rec = epoch(record=True)
         marks.append(torch.cuda.Event(enable_timing=True))
         marks[-1].record()
+        host_ms.append(round(wk.host_enqueue_s * 1e3, 2))
         recs.append(rec)
         samples += rec["S"] * wk.alloc.view()["B"]
     e1.record()
@@ -297,6 +298,7 @@ def run_ours(args):
             "config": bench_config(world, bool(args.overlap and world > 1), args.strong),
             "epoch_time_s": ms_epoch / 1e3,
             "epoch_ms_each": [round(a.elapsed_time(b), 2) for a, b in zip([e0] + marks[:-1], marks)],
+            "host_enqueue_ms_each": host_ms,
             "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
             "roofline_detail": roof,
             "gather": gather_roof,

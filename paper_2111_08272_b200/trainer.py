@@ -26,6 +26,7 @@ registered), so backward() accumulates straight into the buffer the ring reduces
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass, field
 
 import torch
@@ -445,6 +446,7 @@ class Worker:
         n_r, S = v["n"][self.rank], v["S"]
         if cfg.graphs:
             self.prepare(n_r)                                 # capture + t1(n_r) outside the timed region
+        t_host0 = time.perf_counter()
         pre, self._prefetched = getattr(self, "_prefetched", None), None
         if pre is not None and pre[0] == (self.epoch, n_r):
             xe, ye, e0, e1 = pre[1]                           # enqueued at the end of the previous epoch
@@ -489,6 +491,7 @@ class Worker:
                 self._prefetched = ((self.epoch + 1, n_r), data, done)
             else:
                 self._prefetched = ((self.epoch + 1, n_r), self._data(self.epoch + 1, n_r, S, record), None)
+        self.host_enqueue_s = time.perf_counter() - t_host0   # diagnostics: host time to enqueue the epoch
         ev[-1][1].synchronize()
         while loss_to_host and getattr(self, "_pending", None):
             self._read_loss(host_losses)
