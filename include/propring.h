@@ -221,6 +221,9 @@ typedef struct {
                              here); sizes the LL regions of the window, <= 64 MiB (default 256 KiB)  */
     int64_t os_max_bytes; /* largest buffer the one-shot LL path handles (PR_ALGO_ONESHOT; PR_ALGO_AUTO
                              picks it up to here), <= 16 MiB (default 64 KiB)                         */
+    int64_t min_slice_bytes; /* ring: 0 = slot-sized slices (default); > 0 (multiple of 16) = cut each
+                             channel's share of a chunk into up to slots/2 slices of >= this many bytes,
+                             so every phase keeps several slices in flight (an A/B knob for NVLink)  */
 } pr_comm_config;
 
 /* Allreduce algorithm.  Both compute the same bits (the two-shot reducer adds the contributions in the

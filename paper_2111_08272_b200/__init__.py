@@ -253,7 +253,7 @@ ALGO_ONESHOT = 4
 def comm_config(channels=0, slots=8, threads=512, slot_bytes=0, watchdog_ns=10_000_000_000,
                 force_staged=False, stages=0, tile_bytes=0, sys_scope=False, algo=ALGO_RING, ts_slots=2,
                 ts_slot_bytes=64 * 1024, ts_max_bytes=4 << 20, ll_max_bytes=256 * 1024,
-                os_max_bytes=64 * 1024):
+                os_max_bytes=64 * 1024, min_slice_bytes=0):
     """K3 launch/pipeline configuration.  channels / slot_bytes / stages / tile_bytes = 0: chosen at init from
     the topology (one GPU: 16 / 256 KiB / 6 / 16 KiB, the co-located optimum of tools/sweep_ring.py; ranks
     on different GPUs: 32 / 1 MiB / 6 / 16 KiB, from the per-channel throughput of tools/sweep_cta.py).
@@ -265,7 +265,7 @@ def comm_config(channels=0, slots=8, threads=512, slot_bytes=0, watchdog_ns=10_0
     return CommConfig(channels=channels, slots=slots, threads=threads, flags=flags, slot_bytes=slot_bytes,
                       watchdog_ns=watchdog_ns, stages=stages, tile_bytes=tile_bytes, algo=algo, ts_slots=ts_slots,
                       ts_slot_bytes=ts_slot_bytes, ts_max_bytes=ts_max_bytes, ll_max_bytes=ll_max_bytes,
-                      os_max_bytes=os_max_bytes)
+                      os_max_bytes=os_max_bytes, min_slice_bytes=min_slice_bytes)
 
 
 class _DeviceBuffer:

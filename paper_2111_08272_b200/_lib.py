@@ -41,7 +41,7 @@ class CommConfig(ctypes.Structure):
     _fields_ = [("channels", c_i32), ("slots", c_i32), ("threads", c_i32), ("flags", c_i32),
                 ("slot_bytes", c_i64), ("watchdog_ns", c_i64), ("stages", c_i32), ("tile_bytes", c_i32),
                 ("algo", c_i32), ("ts_slots", c_i32), ("ts_slot_bytes", c_i64), ("ts_max_bytes", c_i64),
-                ("ll_max_bytes", c_i64), ("os_max_bytes", c_i64)]
+                ("ll_max_bytes", c_i64), ("os_max_bytes", c_i64), ("min_slice_bytes", c_i64)]
 
 
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, c_sz, c_vp)

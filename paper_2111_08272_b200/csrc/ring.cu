@@ -83,6 +83,7 @@ struct DevTable {
     int64_t ts_slot_bytes;
     uint64_t off_ll;                // LL ring: [channels][2P−2 phases][ll_region_bytes]
     int64_t ll_region_bytes;        // 16-byte lines, 8 payload bytes each, for one channel's share of a chunk
+    int64_t min_slice_bytes;        // > 0: cut each chunk share into up to slots/2 slices of >= this (ring)
     uint64_t off_os;                // one-shot LL: [channels][P sources][os_region_bytes]
     int64_t os_region_bytes;        // LL lines for one channel's share of the whole buffer
     volatile int* status;           // host-mapped
@@ -597,7 +598,16 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
     const int64_t cs = (per + V - 1) / V * V;                      // chunk elements
     const int64_t subp = (cs + tab->channels - 1) / tab->channels;
     const int64_t sub = (subp + V - 1) / V * V;                   // this channel's share of a chunk
-    const int64_t sl = tab->slot_bytes / (int64_t)sizeof(T);       // slice elements (one staging slot)
+    // slice elements: one staging slot; with min_slice_bytes > 0 the chunk share is cut into up to
+    // G = slots/2 slices (each >= min_slice_bytes) so that a phase keeps G slices in flight — per phase
+    // max(G·τ, τ + L) instead of τ + L when the share fits one slot (a latency-bound regime on NVLink;
+    // co-located it did not pay).  A pure function of (count, P, config): same on every rank.
+    int64_t sl = tab->slot_bytes / (int64_t)sizeof(T);
+    if (tab->min_slice_bytes > 0) {
+        const int64_t G0 = (int64_t)(tab->slots / 2);
+        const int64_t want = ((sub + G0 - 1) / G0 + V - 1) / V * V;
+        sl = min(sl, max(want, (int64_t)(tab->min_slice_bytes / (int64_t)sizeof(T))));
+    }
     const int64_t te = min(TE, sl);
     const int64_t nsl = sub > 0 ? (sub + sl - 1) / sl : 0;
     const float s = (float)((double)rc.n_local / (double)sh.sumn);  // n_r/Σn: fp64 division, fp32 weight
@@ -1292,7 +1302,7 @@ struct Reg {
 struct Hello {
     cudaIpcMemHandle_t handle;
     int32_t P, rank, device, channels, slots, threads, stages, tile_bytes, algo, ts_slots;
-    int64_t ts_slot_bytes, ts_max_bytes, ll_max_bytes, os_max_bytes;
+    int64_t ts_slot_bytes, ts_max_bytes, ll_max_bytes, os_max_bytes, min_slice_bytes;
     int64_t slot_bytes, window_bytes;
     uint64_t bytes;   // registration size
     unsigned char uuid[16];   // device identity: peers on another GPU need .sys-scope synchronisation
@@ -1339,6 +1349,7 @@ pr_comm_config default_config() {
     c.ts_max_bytes = 4ll << 20;     // measured crossover (co-located P = 4, 8): two-shot wins up to ~4 MiB
     c.ll_max_bytes = 256 * 1024;
     c.os_max_bytes = 64 * 1024;
+    c.min_slice_bytes = 0;
     return c;
 }
 
@@ -1362,6 +1373,7 @@ int check_config(const pr_comm_config& c) {
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
         (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_ONESHOT ||
         c.ll_max_bytes < 0 || c.ll_max_bytes > (64ll << 20) || c.os_max_bytes < 0 || c.os_max_bytes > (16ll << 20) ||
+        c.min_slice_bytes < 0 || c.min_slice_bytes % 16 ||
         c.ts_slots < 2 || c.ts_slots > 16 || c.ts_slot_bytes < 256 || c.ts_slot_bytes % 256 ||
         c.ts_slot_bytes > (16ll << 20) || c.ts_max_bytes < 0)
         return PR_ERR_INVALID;
@@ -1398,6 +1410,7 @@ int alloc_common(pr_comm* c) {
     t.ts_slots = c->cfg.ts_slots;
     t.ts_slot_bytes = c->cfg.ts_slot_bytes;
     t.ll_region_bytes = (int64_t)ll_region_bytes(c->cfg, c->P);
+    t.min_slice_bytes = c->cfg.min_slice_bytes;
     t.os_region_bytes = (int64_t)os_region_bytes(c->cfg, c->P);
     layout(t);
     PR_CUDA_TRY(cudaMalloc((void**)&c->win, t.window_bytes));
@@ -1559,6 +1572,7 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
     me.ts_max_bytes = c->cfg.ts_max_bytes;
     me.ll_max_bytes = c->cfg.ll_max_bytes;
     me.os_max_bytes = c->cfg.os_max_bytes;
+    me.min_slice_bytes = c->cfg.min_slice_bytes;
     {
         cudaDeviceProp prop;
         if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) std::memcpy(me.uuid, &prop.uuid, 16);
@@ -1573,7 +1587,8 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
         if (h.P != P || h.rank != q || h.channels != me.channels || h.slots != me.slots || h.slot_bytes != me.slot_bytes ||
             h.threads != me.threads || h.stages != me.stages || h.tile_bytes != me.tile_bytes || h.algo != me.algo ||
             h.ts_slots != me.ts_slots || h.ts_slot_bytes != me.ts_slot_bytes || h.ts_max_bytes != me.ts_max_bytes ||
-            h.ll_max_bytes != me.ll_max_bytes || h.os_max_bytes != me.os_max_bytes)
+            h.ll_max_bytes != me.ll_max_bytes || h.os_max_bytes != me.os_max_bytes ||
+            h.min_slice_bytes != me.min_slice_bytes)
             rc = rc ? rc : PR_ERR_INVALID;
     }
     if (rc) { free_comm(c); return rc; }

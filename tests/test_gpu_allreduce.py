@@ -546,3 +546,13 @@ def test_randomized_configs_all_algorithms():
         finally:
             for c in comms:
                 c.destroy()
+
+
+@pytest.mark.parametrize("min_slice", [4096, 65536])
+def test_ring_min_slice_bit_identical(min_slice):
+    """min_slice_bytes > 0 slices each chunk share into up to slots/2 slices: same bits (plain and fused)."""
+    for P in (2, 4, 8):
+        comms = group(P, min_slice_bytes=min_slice, slots=8)
+        for L in (7, 4099, 300_001, 2 ** 21 + 5):
+            _check(P, L, "f32" if L % 2 else "bf16", [1 + (r % 3) for r in range(P)], comms, seed=L + P)
+        _fused_case(P, 200_003, [2] * P, comms, seed=P + 77)

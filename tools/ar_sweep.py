@@ -89,14 +89,14 @@ def run_colocated(P, max_mib, reps, algo=0):
         c.destroy()
 
 
-def run_multi(max_mib, reps, algo=0, channels=0):
+def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0):
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, P = dist.get_rank(), dist.get_world_size()
-    comm = pr.comm_init(rank, P, local, config=pr.comm_config(algo=algo, channels=channels))
+    comm = pr.comm_init(rank, P, local, config=pr.comm_config(algo=algo, channels=channels, min_slice_bytes=min_slice))
     n = weights(P)
     s = n[rank] / sum(n)
     Zmax = max_mib << 20
@@ -154,8 +154,9 @@ if __name__ == "__main__":
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--algo", type=int, default=0, help="0 ring, 1 two-shot, 2 auto, 3 LL ring, 4 one-shot LL")
     ap.add_argument("--channels", type=int, default=0, help="CTAs per rank (multi-GPU mode; 0 = topology default)")
+    ap.add_argument("--min-slice", type=int, default=0, help="ring min_slice_bytes (0 = slot-sized slices)")
     a = ap.parse_args()
     if a.colocated:
         run_colocated(a.colocated, a.max_mib, a.reps, a.algo)
     else:
-        run_multi(a.max_mib, a.reps, a.algo, a.channels)
+        run_multi(a.max_mib, a.reps, a.algo, a.channels, a.min_slice)

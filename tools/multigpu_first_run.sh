@@ -23,6 +23,11 @@ for ch in 16 24 32 48 64; do
   timeout 900 $TR --nproc-per-node $G --master-port $((29650 + ch)) tools/ar_sweep.py --max-mib 256 --channels $ch \
       > gpurun_out/mg_ar_sweep_ch${ch}_p$G.jsonl 2> gpurun_out/mg_ar_sweep_ch${ch}_p$G.err
 done
+# ring slicing A/B on NVLink: G slices per phase (min_slice_bytes) vs slot-sized slices
+for ms in 65536 262144; do
+  timeout 900 $TR --nproc-per-node $G --master-port $((29700 + ms / 65536)) tools/ar_sweep.py --max-mib 256 --min-slice $ms \
+      > gpurun_out/mg_ar_sweep_ms${ms}_p$G.jsonl 2> gpurun_out/mg_ar_sweep_ms${ms}_p$G.err
+done
 # AUTO (one-shot / LL / two-shot / ring by size) at the largest P
 timeout 1200 $TR --nproc-per-node $G --master-port 29630 tools/ar_sweep.py --max-mib 64 --algo 2 \
     > gpurun_out/mg_ar_sweep_auto_p$G.jsonl 2> gpurun_out/mg_ar_sweep_auto_p$G.err
