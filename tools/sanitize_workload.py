@@ -53,7 +53,8 @@ def main():
     pr.spin(10_000)
     # K3: local groups, both scopes, direct and staged, ragged counts
     for flags in (dict(), dict(sys_scope=True), dict(force_staged=True), dict(algo=pr.ALGO_TWO_SHOT),
-                  dict(algo=pr.ALGO_LL), dict(algo=pr.ALGO_LL, sys_scope=True), dict(algo=pr.ALGO_ONESHOT)):
+                  dict(algo=pr.ALGO_LL), dict(algo=pr.ALGO_LL, sys_scope=True), dict(algo=pr.ALGO_ONESHOT),
+                  dict(min_slice_bytes=512)):
         comms = pr.comm_init_local(3, 0, pr.comm_config(channels=2, slots=4, slot_bytes=4096, stages=2,
                                                         tile_bytes=2048, threads=64, **flags))
         for L in (5, 3001):
