@@ -476,9 +476,6 @@ struct SliceArgs {
     const T* isrc;               // received data of the slice (ragged tail only)
     int64_t len, te, nt;         // slice elements, tile elements, tiles
     float s, nlr, wd;
-    unsigned long long* credit;  // slot credit to return to the previous rank after the last tile (or null)
-    unsigned long long credit_val;
-    bool sys;
 };
 
 // Consumers' loop over one slice's tiles with the hop's arithmetic fixed (MODE).  Per tile: wait for the
@@ -495,11 +492,9 @@ __device__ __forceinline__ void consume_slice(Shared& sh, uint8_t* smem, int kTi
     const T* tp = a.thp;
     int64_t left = a.len;
     for (int64_t t = 0; t < a.nt; ++t) {
+        const int ne = (int)(left < a.te ? left : a.te);
         mbar_wait(&sh.full[stg], ph);
         const bool ok = sh.tile_ok[stg] != 0;
-        if (ok && t == a.nt - 1 && a.credit)   // slot landed in smem: hand it back (ordered after the TMA reads)
-            st_relaxed_u64(a.credit, a.credit_val, a.sys);
-        const int ne = (int)(left < a.te ? left : a.te);
         const int nv = (ne * (int)sizeof(T)) / 16;
         const uint4* gs = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes);
         const uint4* is = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes + kTileBytes);
@@ -720,7 +715,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
         // Waits until the consumers' stores of a slice's tiles are issued (stored barrier, release.cta by
         // every consumer warp), then one sys-scope release makes the whole slice visible to the peer.
         if (threadIdx.x == 32) {
-            unsigned long long prodJ = st->slot_base, agP = st->ag_base;
+            unsigned long long prodJ = st->slot_base, agP = st->ag_base, consJ = st->slot_base;
             int stg = 0;
             uint32_t ph = 0;
             for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
@@ -745,13 +740,20 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                         if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
                         else st_release(&nxf->rs_ready, prodJ + 1, sys);
                     }
+                    // the slice's received slot is consumed (every tile's TMA landed before its consumers
+                    // arrived on `stored`): hand it back to the previous rank
+                    if (t == nt - 1 && reads_slot(kind) && ok) st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);
                 }
-                if (nt == 0 && sends && !*(volatile int*)&sh.err) {   // empty slice: nothing to wait for
-                    if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
-                    else st_release(&nxf->rs_ready, prodJ + 1, sys);
+                if (nt == 0 && !*(volatile int*)&sh.err) {   // empty slice: nothing to wait for
+                    if (sends) {
+                        if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
+                        else st_release(&nxf->rs_ready, prodJ + 1, sys);
+                    }
+                    if (reads_slot(kind)) st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);
                 }
                 if (sends_ag(kind)) ++agP;
                 else if (writes_slot(kind)) ++prodJ;
+                if (reads_slot(kind)) ++consJ;
             });
         }
     } else {
@@ -779,7 +781,7 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
             const bool upd = FUSE && kind == K_LAST;                // reduced chunk final here: apply SGD
             const bool zg = FUSE && A.zero && kind <= K_LAST;        // own gradient consumed: reset it
             SliceArgs<T> sa{out1, out2, zg ? buf + lo : nullptr, upd ? th + lo : nullptr, gsrc, isrc, len, te, nt, s,
-                            A.nlr, A.wd, (reads_slot(kind) && cid == 0) ? &pvf->rs_credit : nullptr, consJ + 1, sys};
+                            A.nlr, A.wd};   // (slot credits are returned by the signal warp)
             // the hop's arithmetic is fixed per instantiation: one switch per slice, none per tile / element
             switch (mode) {
                 case M_SCALE: consume_slice<T, M_SCALE, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
@@ -787,8 +789,6 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                 case M_COPY: consume_slice<T, M_COPY, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
                 default: consume_slice<T, M_ZERO, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
             }
-            const bool err = *(volatile int*)&sh.err != 0;
-            if (nt == 0 && reads_slot(kind) && cid == 0 && !err) st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);
             if (reads_slot(kind)) ++consJ;
             if (writes_slot(kind)) ++prodJ;
         });
