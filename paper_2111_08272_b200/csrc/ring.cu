@@ -861,6 +861,46 @@ __device__ __forceinline__ bool warp_wait_peers(const unsigned long long* arr, u
     return __all_sync(0xffffffffu, ok);
 }
 
+// Two-shot phase B on one slice: every element reduced over the P sources in the ring's order for chunk r
+// with the ring's per-hop rounding.  Source pointers, weights and activity are resolved once per slice into
+// shared memory (src[h] is source h = rank (r+h) mod P: the own gradient or its staging slot), so the
+// vector loop does P cache-global loads, P FMAs per element and P stores — no slot-address arithmetic or
+// modulo per element (that was most of the instructions).  PP > 0: P known at compile time (unrolled).
+template <typename T, int PP>
+__device__ __forceinline__ void ts_reduce(int P, int64_t nv, const uint8_t* const* src, const float* wt, const int* act,
+                                          uint8_t* const* dst) {
+    constexpr int V = Vec<T>::V;
+    const int np = PP > 0 ? PP : P;
+    for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+        float acc[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = 0.0f;
+#pragma unroll
+        for (int h = 0; h < (PP > 0 ? PP : 1); ++h) {
+            if (PP == 0) break;
+            if (!act[h]) continue;                            // n_q = 0 contributes nothing (never multiplied)
+            const uint4 x = ld_cg_v4(src[h] + (size_t)v * 16);
+            const float sq = wt[h];
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                acc[j] = rnd_dtype<T>(h == 0 ? __fmul_rn(sq, lane_f<T>(x, j)) : __fmaf_rn(sq, lane_f<T>(x, j), acc[j]));
+        }
+        if (PP == 0) {
+            for (int h = 0; h < np; ++h) {
+                if (!act[h]) continue;
+                const uint4 x = ld_cg_v4(src[h] + (size_t)v * 16);
+                const float sq = wt[h];
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    acc[j] = rnd_dtype<T>(h == 0 ? __fmul_rn(sq, lane_f<T>(x, j)) : __fmaf_rn(sq, lane_f<T>(x, j), acc[j]));
+            }
+        }
+        const uint4 y = pack_f<T>(acc);
+#pragma unroll 8
+        for (int q = 0; q < np; ++q) st_v4(dst[q] + (size_t)v * 16, y);
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__ LaunchArgs A) {
     __shared__ int s_err;
@@ -868,6 +908,10 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__
     __shared__ long long s_n[PR_MAX_RANKS];
     __shared__ uint8_t* s_bufs[PR_MAX_RANKS];
     __shared__ float s_w[PR_MAX_RANKS];
+    __shared__ const uint8_t* s_src[PR_MAX_RANKS];
+    __shared__ uint8_t* s_dst[PR_MAX_RANKS];
+    __shared__ float s_wt[PR_MAX_RANKS];
+    __shared__ int s_act[PR_MAX_RANKS];
     const RankCall& rc = A.calls[blockIdx.y];
     const DevTable* tab = rc.tab;
     const int ch = blockIdx.x;
@@ -954,23 +998,18 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__
             if (!warp_wait_peers(mf->ready, J + 1, r, P, deadline, sys) && t0) fail();
         if (!sync_ok()) return;
         const int64_t nv = len / V;
-        for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
-            float acc[V];
-#pragma unroll
-            for (int j = 0; j < V; ++j) acc[j] = 0.0f;
-            for (int h = 0; h < P; ++h) {
-                const int q = (r + h) % P;
-                const uint4 x = (q == r) ? *reinterpret_cast<const uint4*>(buf + lo + v * V)
-                                         : ld_cg_v4(ts_slot_of(my, tab, ch, q, J) + (size_t)v * 16);
-                if (s_n[q] <= 0) continue;                   // n_q = 0 contributes nothing (never multiplied)
-                const float sq = s_w[q];
-#pragma unroll
-                for (int j = 0; j < V; ++j)
-                    acc[j] = rnd_dtype<T>(h == 0 ? __fmul_rn(sq, lane_f<T>(x, j)) : __fmaf_rn(sq, lane_f<T>(x, j), acc[j]));
-            }
-            const uint4 y = pack_f<T>(acc);
-            for (int q = 0; q < P; ++q) st_v4(reinterpret_cast<T*>(s_bufs[q]) + lo + v * V, y);
+        for (int h = (int)threadIdx.x; h < P; h += (int)blockDim.x) {     // resolve the P sources once
+            const int q = (r + h) % P;
+            s_src[h] = q == r ? reinterpret_cast<const uint8_t*>(buf + lo) : ts_slot_of(my, tab, ch, q, J);
+            s_wt[h] = s_w[q];
+            s_act[h] = s_n[q] > 0 ? 1 : 0;
+            s_dst[h] = reinterpret_cast<uint8_t*>(reinterpret_cast<T*>(s_bufs[h]) + lo);
         }
+        __syncthreads();
+        if (P == 8) ts_reduce<T, 8>(P, nv, s_src, s_wt, s_act, s_dst);
+        else if (P == 4) ts_reduce<T, 4>(P, nv, s_src, s_wt, s_act, s_dst);
+        else if (P == 2) ts_reduce<T, 2>(P, nv, s_src, s_wt, s_act, s_dst);
+        else ts_reduce<T, 0>(P, nv, s_src, s_wt, s_act, s_dst);
         for (int64_t e = nv * V + threadIdx.x; e < len; e += blockDim.x) {   // ragged tail: end of buffer
             float acc = 0.0f;
             for (int h = 0; h < P; ++h) {
