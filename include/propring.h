@@ -215,7 +215,7 @@ typedef struct {
     int32_t tile_bytes;   /* bytes per input per pipeline stage, multiple of 16, <= 32768 (0: 16 KiB) */
     int32_t algo;         /* PR_ALGO_* (default PR_ALGO_RING)                                         */
     int32_t ts_slots;     /* two-shot staging slots per (channel, source), >= 2 (default 2)          */
-    int64_t ts_slot_bytes;/* two-shot slice bytes, multiple of 256 (default 65536)                   */
+    int64_t ts_slot_bytes;/* two-shot slice bytes, multiple of 256 (default 262144)                  */
     int64_t ts_max_bytes; /* PR_ALGO_AUTO: two-shot for buffers up to this many bytes (default 4 MiB)  */
     int64_t ll_max_bytes; /* largest buffer the LL ring handles (PR_ALGO_LL; PR_ALGO_AUTO picks it up to
                              here); sizes the LL regions of the window, <= 64 MiB (default 256 KiB)  */

@@ -252,7 +252,7 @@ ALGO_ONESHOT = 4
 
 def comm_config(channels=0, slots=8, threads=512, slot_bytes=0, watchdog_ns=10_000_000_000,
                 force_staged=False, stages=0, tile_bytes=0, sys_scope=False, algo=ALGO_RING, ts_slots=2,
-                ts_slot_bytes=64 * 1024, ts_max_bytes=4 << 20, ll_max_bytes=256 * 1024,
+                ts_slot_bytes=256 * 1024, ts_max_bytes=4 << 20, ll_max_bytes=256 * 1024,
                 os_max_bytes=64 * 1024, min_slice_bytes=0):
     """K3 launch/pipeline configuration.  channels / slot_bytes / stages / tile_bytes = 0: chosen at init from
     the topology (one GPU: 16 / 256 KiB / 6 / 16 KiB, the co-located optimum of tools/sweep_ring.py; ranks

@@ -1384,7 +1384,7 @@ pr_comm_config default_config() {
     c.tile_bytes = 0;        // topology
     c.algo = PR_ALGO_RING;
     c.ts_slots = 2;
-    c.ts_slot_bytes = 64 * 1024;
+    c.ts_slot_bytes = 256 * 1024;   // tools/sweep_twoshot.py: P = 2, 16 MiB 92 -> 67 us vs 64 KiB; P = 8 neutral
     c.ts_max_bytes = 4ll << 20;     // measured crossover (co-located P = 4, 8): two-shot wins up to ~4 MiB
     c.ll_max_bytes = 256 * 1024;
     c.os_max_bytes = 64 * 1024;
