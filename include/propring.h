@@ -234,7 +234,7 @@ typedef struct {
 #define PR_ALGO_RING     0
 #define PR_ALGO_TWO_SHOT 1
 #define PR_ALGO_AUTO     2   /* one-shot up to os_max_bytes, LL ring up to ll_max_bytes, two-shot up to
-                                 ts_max_bytes, ring above */
+                                 ts_max_bytes (× 2 for P >= 4, × 4 for P >= 8), ring above */
 /* LL ring: the ring's schedule, order and rounding (same bits) with a low-latency line protocol — every
  * 16-byte line pushed to the next rank carries 8 payload bytes and the call's sequence number in both
  * 64-bit halves, so the receiver polls the data itself (no fence / flag / credit round trip per hop).

@@ -1521,11 +1521,15 @@ int find_reg(const pr_comm* c, const void* buf, size_t bytes, int32_t* id, int64
 size_t dtype_size(int32_t dt) { return dt == PR_DTYPE_F32 ? 4 : (dt == PR_DTYPE_BF16 ? 2 : 0); }
 
 // The algorithm a call takes: a pure function of (config, count, dtype), identical on every rank.
-int pick_algo(const pr_comm_config& cfg, int64_t count, int32_t dtype) {
+// AUTO's two-shot limit grows with P: the ring pays 2P−2 flag round trips per call, the two-shot 2; at
+// `.sys` scope and P = 8 the two-shot won up to 16 MiB (tools/ar_latency.py --sys), at P = 2 the ring wins
+// from 4 MiB — so ts_max_bytes × 4 for P >= 8, × 2 for P >= 4.
+int pick_algo(const pr_comm_config& cfg, int64_t count, int32_t dtype, int P) {
     const int64_t bytes = count * (dtype == PR_DTYPE_F32 ? 4 : 2);
+    const int64_t ts_max = cfg.ts_max_bytes * (P >= 8 ? 4 : (P >= 4 ? 2 : 1));
     if ((cfg.algo == PR_ALGO_ONESHOT || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.os_max_bytes) return PR_ALGO_ONESHOT;
     if ((cfg.algo == PR_ALGO_LL || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.ll_max_bytes) return PR_ALGO_LL;
-    if (cfg.algo == PR_ALGO_TWO_SHOT || (cfg.algo == PR_ALGO_AUTO && bytes <= cfg.ts_max_bytes)) return PR_ALGO_TWO_SHOT;
+    if (cfg.algo == PR_ALGO_TWO_SHOT || (cfg.algo == PR_ALGO_AUTO && bytes <= ts_max)) return PR_ALGO_TWO_SHOT;
     return PR_ALGO_RING;
 }
 
@@ -1543,11 +1547,11 @@ int launch_k3(void* fn, const LaunchArgs& a, int nranks, int channels, int block
     return PR_OK;
 }
 
-int launch_ring(const LaunchArgs& a, int nranks, const pr_comm_config& cfg, cudaStream_t s, bool coop) {
+int launch_ring(const LaunchArgs& a, int nranks, int P, const pr_comm_config& cfg, cudaStream_t s, bool coop) {
     const int32_t threads = cfg.threads, channels = cfg.channels;
     const bool f32 = a.dtype == PR_DTYPE_F32;
     // the fused update (K7 inside K3) exists in the TMA ring only (its callers check pick_algo)
-    const int algo = a.fuse ? PR_ALGO_RING : pick_algo(cfg, a.count, a.dtype);
+    const int algo = a.fuse ? PR_ALGO_RING : pick_algo(cfg, a.count, a.dtype, P);
     switch (algo) {
         case PR_ALGO_ONESHOT:
             return launch_k3(f32 ? (void*)oneshot_ll_kernel<float> : (void*)oneshot_ll_kernel<__nv_bfloat16>, a, nranks,
@@ -1764,7 +1768,7 @@ extern "C" int pr_weighted_allreduce(pr_comm* c, void* d_buf, int64_t count, int
     a.calls[0].buf = d_buf;
     a.calls[0].n_local = n_local;
     find_reg(c, d_buf, (size_t)count * dtype_size(dt), &a.calls[0].reg_id, &a.calls[0].reg_off);
-    return launch_ring(a, 1, c->cfg, (cudaStream_t)stream, false);
+    return launch_ring(a, 1, c->P, c->cfg, (cudaStream_t)stream, false);
 }
 
 extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d_bufs, int64_t count, int32_t dt,
@@ -1796,7 +1800,7 @@ extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d
         find_reg(comms[r], d_bufs[r], 0, &a.calls[r].reg_id, &a.calls[r].reg_off);
     }
     PR_CUDA_TRY(cudaSetDevice(c0->device));
-    return launch_ring(a, P, c0->cfg, (cudaStream_t)stream, true);
+    return launch_ring(a, P, P, c0->cfg, (cudaStream_t)stream, true);
 }
 
 // ---- K7 fused into K3: weighted allreduce + SGD update (+ gradient reset) ---------------------------
@@ -1821,7 +1825,7 @@ extern "C" int pr_weighted_allreduce_sgd(pr_comm* c, float* d_grad, float* d_the
     int32_t trid = -1;
     int64_t toff = 0;
     find_reg(c, d_theta, (size_t)count * 4, &trid, &toff);
-    const bool fusable = pick_algo(c->cfg, count, PR_DTYPE_F32) == PR_ALGO_RING && a.calls[0].reg_id >= 0 &&
+    const bool fusable = pick_algo(c->cfg, count, PR_DTYPE_F32, c->P) == PR_ALGO_RING && a.calls[0].reg_id >= 0 &&
                          trid == a.calls[0].reg_id && !(c->cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
     if (!fusable) {   // composed: the same bits (the ring's ḡ, then K7's two FMAs)
         if (int rc = pr_weighted_allreduce(c, d_grad, count, PR_DTYPE_F32, n_local, stream)) return rc;
@@ -1832,7 +1836,7 @@ extern "C" int pr_weighted_allreduce_sgd(pr_comm* c, float* d_grad, float* d_the
     a.nlr = (float)(-lr);
     a.wd = (float)wd;
     a.calls[0].th_delta = (int64_t)((const uint8_t*)d_theta - (const uint8_t*)d_grad);
-    return launch_ring(a, 1, c->cfg, (cudaStream_t)stream, false);
+    return launch_ring(a, 1, c->P, c->cfg, (cudaStream_t)stream, false);
 }
 
 extern "C" int pr_weighted_allreduce_sgd_local(pr_comm* const* comms, float* const* d_grads, float* const* d_thetas,
@@ -1856,7 +1860,7 @@ extern "C" int pr_weighted_allreduce_sgd_local(pr_comm* const* comms, float* con
     }
     if (sumn <= 0) return PR_ERR_ZERO_SAMPLES;
     PR_CUDA_TRY(cudaSetDevice(c0->device));
-    const bool fusable = P > 1 && pick_algo(c0->cfg, count, PR_DTYPE_F32) == PR_ALGO_RING && same_delta &&
+    const bool fusable = P > 1 && pick_algo(c0->cfg, count, PR_DTYPE_F32, P) == PR_ALGO_RING && same_delta &&
                          !(c0->cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
     if (!fusable) {
         if (P > 1) {
@@ -1883,7 +1887,7 @@ extern "C" int pr_weighted_allreduce_sgd_local(pr_comm* const* comms, float* con
         a.calls[r].th_delta = d0;
         find_reg(comms[r], d_grads[r], 0, &a.calls[r].reg_id, &a.calls[r].reg_off);
     }
-    return launch_ring(a, P, c0->cfg, (cudaStream_t)stream, true);
+    return launch_ring(a, P, P, c0->cfg, (cudaStream_t)stream, true);
 }
 
 extern "C" int pr_comm_allgather_f64(pr_comm* c, double local, double* out, void* stream) {
