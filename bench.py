@@ -153,7 +153,8 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    comm = pr.comm_init(rank, world, local) if world > 1 else None
+    # AUTO: the 46.76 MB step buffer takes the ring (with K7 fused); N1's buckets take the two-shot at P >= 8
+    comm = pr.comm_init(rank, world, local, config=pr.comm_config(algo=pr.ALGO_AUTO)) if world > 1 else None
     units = units_for(world, args.strong)
     cfg = RunConfig(N=args.data_n, ratios=[1] * world, C=units, g=G_UNIT, adaptive=True, micro=1024,
                     overlap=args.overlap, bucket_mb=args.bucket_mb)

@@ -205,7 +205,7 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("gloo" if shared else "nccl", **({} if shared else {"device_id": torch.device("cuda", local)}))
     tdev = "cpu" if shared else "cuda"
-    comm = pr.comm_init(rank, world, local)
+    comm = pr.comm_init(rank, world, local, config=pr.comm_config(algo=pr.ALGO_AUTO))
     policy = {"never_freeze": True} if (args.never_freeze or args.scenario in SCHEDULES) else None
     if policy is not None and args.ema < 1.0:
         policy["ema_alpha"] = args.ema
