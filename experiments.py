@@ -4,7 +4,7 @@
     python -m torch.distributed.run --nproc-per-node P --master-addr 127.0.0.1 experiments.py --scenario c4
 
 Heterogeneity is emulated (the box is homogeneous): rank r is slowed by σ_r through a K4 spin of
-(σ_r − 1)·c0·n_r ns per aggregation, c0 = its calibrated compute seconds per sample.
+(σ_r − 1)·t1(n_r) per aggregation, t1(n_r) = its own measured step time for its n_r rows.
 Each epoch rank 0 prints one JSON line: w (units), t_s per rank, t_w per rank (barrier wait,
 from the allreduce time above the fastest rank's), epoch time T, and the Σspeed-balanced bound
 T_ideal = S·(B/Σv + t_c) with v_r = S·n_r/t_s^r measured under the slowdown and t_c the measured

@@ -5,8 +5,9 @@ Rows of SURVEY §8(a) handled here (the rest are library calls):
       a parameter update] ... until w_i samples are transferred" (P:69 steps (1)-(3)).  The rank's n_r
       samples are processed in microbatches of at most `micro` rows; each microbatch loss is scaled by
       mb/n_r so the flat gradient buffer ends up holding the LOCAL MEAN gradient (DESIGN.md §3 #11).
-      Emulated heterogeneity: after the backward pass a K4 spin of (σ_r − 1)·c0·n_r ns (c0 = calibrated
-      seconds per sample at σ = 1) slows rank r by the factor σ_r.
+      Emulated heterogeneity: a K4 spin of (σ_r − 1)·t1(n_r) after each step's graph replay, t1(n_r) the
+      rank's own measured step time for its n_r rows at σ = 1 (prepare()), slows rank r by the factor σ_r
+      (the eager path without graphs falls back to a per-sample calibration, c0·n_r).
   a5  t_s capture: CUDA events around data movement + compute + spin, summed over the epoch (P:102,
       P:152; DESIGN.md §3 #4-#5); one event synchronisation per epoch, not per step.
   a9  SGD update, Eq. 1 with weight decay: the library's fused pr_sgd_update over the
