@@ -178,3 +178,18 @@ def test_frozen_update_is_noop():
     v = a.view()
     assert v["frozen"] and v["w"] == [13, 7]
     assert a.update([1.0, 100.0]) is False and a.view() == v
+
+
+def test_header_is_plain_c():
+    """The boundary is a C ABI: include/propring.h compiles as C99 (no C++ or torch types)."""
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        import pytest
+
+        pytest.skip("no C compiler")
+    hdr = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "propring.h")
+    r = subprocess.run([cc, "-fsyntax-only", "-std=c99", "-Wall", "-Werror", "-x", "c", hdr], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
