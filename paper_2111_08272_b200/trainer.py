@@ -120,6 +120,9 @@ class Worker:
                                      impl=pr.GATHER_IMPL_LSU if lsu else pr.GATHER_IMPL_TMA,
                                      layout=pr.GATHER_LAYOUT_HWC if cfg.channels_last else pr.GATHER_LAYOUT_CHW)
         torch.backends.cudnn.benchmark = True
+        # try every cuDNN algorithm when autotuning (default: the first 10 heuristics' picks): the
+        # ResNet-18 step settles at 2.90-2.91 ms instead of 3.08-3.09 (tools/model_variance.py, 6 runs each)
+        torch.backends.cudnn.benchmark_limit = 0
         torch.manual_seed(cfg.seed)                   # identical initial weights on every rank
         self.model = build_model(cfg.model, cfg.num_classes).to(self.dev)
         if cfg.channels_last:
