@@ -93,8 +93,14 @@ def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0):
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    shared = os.environ.get("PR_BENCH_SHARED_GPU") == "1"   # functional check: every rank on cuda:0, gloo
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, P = dist.get_rank(), dist.get_world_size()
     comm = pr.comm_init(rank, P, local, config=pr.comm_config(algo=algo, channels=channels, min_slice_bytes=min_slice))
     n = weights(P)
@@ -117,7 +123,7 @@ def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0):
                     fn()
                 b.record()
                 torch.cuda.synchronize()
-                t = torch.tensor([a.elapsed_time(b) / reps], device="cuda")
+                t = torch.tensor([a.elapsed_time(b) / reps], device="cpu" if shared else "cuda")
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 return float(t) * 1e3
 
@@ -129,6 +135,10 @@ def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0):
             res = {"mode": "nvlink", "P": P, "dtype": str(dtype).split(".")[-1], "bytes": Z, "us": us,
                    "busbw_GBs": Z * 2 * (P - 1) / P / (us * 1e-6) / 1e9, "max_err": err, "zero_violations": zb}
             res["frac_of_770"] = res["busbw_GBs"] / 770.0
+            if shared:
+                if rank == 0:
+                    print(json.dumps(res), flush=True)
+                continue
             try:
                 op = dist._make_nccl_premul_sum(s)
                 t = timed(lambda: dist.all_reduce(buf, op=op))
