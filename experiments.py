@@ -110,7 +110,7 @@ def run_virtual(args):
                     pr.shard_steps(w.alloc, r, e, cfg.seed, s0, ns, idx[r])
                 else:
                     pr.shard_indices(w.alloc, r, e, cfg.seed, idx[r])
-                x = torch.empty((max(1, ns * n[r]), w.row_bytes), dtype=w.xdt, device="cuda")
+                x = torch.empty((max(1, ns * n[r]), w.row_elems), dtype=w.xdt, device="cuda")
                 y = torch.empty(max(1, ns * n[r]), dtype=torch.int64, device="cuda")
                 pr.gather_rows(w.X.data_ptr(), N, w.row_bytes, idx[r], ns * n[r], x, w.gop, w.Y, y)
                 xs.append(x)

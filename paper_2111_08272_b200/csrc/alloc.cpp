@@ -266,26 +266,60 @@ extern "C" int pr_alloc_save(const pr_alloc* a, void* buf, size_t cap, size_t* s
     return PR_OK;
 }
 
+// Validates everything pr_alloc_init / pr_alloc_set_policy would have refused, so a corrupt or hostile
+// buffer cannot reach a division by zero (C or g = 0), an N·w overflow, or an allocation failure that
+// would throw across the C ABI.
 extern "C" int pr_alloc_load(pr_alloc** out, const void* buf, size_t size) {
     if (!out || !buf || size < sizeof(SaveHeader)) return PR_ERR_INVALID;
     SaveHeader h;
     std::memcpy(&h, buf, sizeof(h));
     if (h.magic != kMagic || h.version != PR_VERSION || h.P < 1 || h.P > PR_MAX_RANKS || h.hist_len < 1)
         return PR_ERR_INVALID;
-    const size_t need = sizeof(SaveHeader) + sizeof(int64_t) * h.P * (1 + (size_t)h.hist_len) + sizeof(double) * h.P;
-    if (size != need) return PR_ERR_INVALID;
+    // same bounds as pr_alloc_init
+    if (h.N < 1 || h.N > ((int64_t)1 << 40) || h.C < 1 || h.C > ((int64_t)1 << 20) || h.g < 1 ||
+        h.g > ((int64_t)1 << 30) || h.floor < 0 || h.C < (int64_t)h.P * h.floor || h.N < h.g * h.C || h.epoch < 0 ||
+        (h.frozen != 0 && h.frozen != 1) || (h.has_tprev != 0 && h.has_tprev != 1))
+        return PR_ERR_INVALID;
+    // same bounds as pr_alloc_set_policy
+    if (h.policy.window < 2 || h.policy.tol < 0 || !(h.policy.ema_alpha > 0.0) || !(h.policy.ema_alpha <= 1.0))
+        return PR_ERR_INVALID;
+    // size check without overflow: the vectors are (1 + hist_len)·P int64 + P doubles
+    const size_t row = sizeof(int64_t) * h.P;
+    const size_t fixed = sizeof(SaveHeader) + row + sizeof(double) * h.P;
+    if (size < fixed || (uint64_t)h.hist_len > (size - fixed) / row || size != fixed + row * (size_t)h.hist_len)
+        return PR_ERR_INVALID;
+    const char* p = (const char*)buf + sizeof(h);
+    // every allocation vector (current and history) must be one pr_alloc could have produced: Σw = C, w >= floor
+    auto valid_w = [&](const char* q) {
+        int64_t sum = 0;
+        for (uint32_t i = 0; i < h.P; ++i) {
+            int64_t w;
+            std::memcpy(&w, q + sizeof(int64_t) * i, sizeof(w));
+            if (w < h.floor || w > h.C) return false;
+            sum += w;
+        }
+        return sum == h.C;
+    };
+    for (int64_t k = 0; k <= h.hist_len; ++k)
+        if (!valid_w(p + row * (size_t)k)) return PR_ERR_INVALID;
+    std::vector<double> tp(h.P);
+    std::memcpy(tp.data(), p + row * (size_t)(1 + h.hist_len), sizeof(double) * h.P);
+    if (h.has_tprev)
+        for (double t : tp)
+            if (!std::isfinite(t) || !(t > 0.0)) return PR_ERR_INVALID;
     pr_alloc* a = new (std::nothrow) pr_alloc();
     if (!a) return PR_ERR_INTERNAL;
-    a->N = h.N; a->P = (int32_t)h.P; a->C = h.C; a->g = h.g; a->floor = h.floor; a->epoch = h.epoch;
-    a->frozen = h.frozen; a->policy = h.policy;
-    const char* p = (const char*)buf + sizeof(h);
-    a->w.resize(h.P);
-    std::memcpy(a->w.data(), p, sizeof(int64_t) * h.P); p += sizeof(int64_t) * h.P;
-    a->hist.resize((size_t)h.hist_len, std::vector<int64_t>(h.P));
-    for (auto& v : a->hist) { std::memcpy(v.data(), p, sizeof(int64_t) * h.P); p += sizeof(int64_t) * h.P; }
-    if (h.has_tprev) {
-        a->t_prev.resize(h.P);
-        std::memcpy(a->t_prev.data(), p, sizeof(double) * h.P);
+    try {
+        a->N = h.N; a->P = (int32_t)h.P; a->C = h.C; a->g = h.g; a->floor = h.floor; a->epoch = h.epoch;
+        a->frozen = h.frozen; a->policy = h.policy;
+        a->w.resize(h.P);
+        std::memcpy(a->w.data(), p, row); p += row;
+        a->hist.resize((size_t)h.hist_len, std::vector<int64_t>(h.P));
+        for (auto& v : a->hist) { std::memcpy(v.data(), p, row); p += row; }
+        if (h.has_tprev) a->t_prev = tp;
+    } catch (...) {   // std::bad_alloc must not cross the C ABI
+        delete a;
+        return PR_ERR_INTERNAL;
     }
     *out = a;
     return PR_OK;

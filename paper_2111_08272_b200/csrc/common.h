@@ -4,8 +4,13 @@
 
 #include "../../include/propring.h"
 
+// Per-device caches (function attributes, occupancy-derived grids) are indexed by device ordinal.
+#define PR_MAX_DEVICES 64
+
 #ifdef __CUDACC__
 #include <cuda_runtime.h>
+
+#include <mutex>
 #define PR_CUDA_TRY(expr)                                   \
     do {                                                    \
         cudaError_t _e = (expr);                            \

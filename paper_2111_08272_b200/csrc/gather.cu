@@ -536,15 +536,23 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
         const TmaGeom geo = tma_geom(n, row_bytes, p.hwc, p.channels, p.plane);
         const int64_t blocks = geo.units < 148 * 2 ? geo.units : 148 * 2;
         const dim3 block(32 * (kTmaConsumerWarps + 1));
-        static bool attr = false;
-        if (!attr) {
-            PR_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel<PR_GATHER_COPY>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            PR_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel<PR_GATHER_U8_TO_F32_AFFINE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            PR_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel<PR_GATHER_U8_TO_BF16_AFFINE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
+        // the dynamic-smem opt-in is a per-device function attribute: set once per device
+        static std::mutex mu;
+        static bool attr[PR_MAX_DEVICES];
+        int dev = 0;
+        PR_CUDA_TRY(cudaGetDevice(&dev));
+        if (dev < 0 || dev >= PR_MAX_DEVICES) return PR_ERR_INVALID;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!attr[dev]) {
+                PR_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel<PR_GATHER_COPY>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                PR_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel<PR_GATHER_U8_TO_F32_AFFINE>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                PR_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel<PR_GATHER_U8_TO_BF16_AFFINE>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                attr[dev] = true;
+            }
         }
         switch (p.op) {
             case PR_GATHER_COPY: gather_tma_kernel<PR_GATHER_COPY><<<(unsigned)blocks, block, smem, s>>>(p); break;
@@ -560,30 +568,38 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
     const int64_t items = n * ((vpr + kSegVec - 1) / kSegVec);
     // grid = one resident wave (SMs × CTAs per SM from the occupancy calculator): a grid-stride loop over
     // a grid larger than what fits leaves the second wave of CTAs as a tail
-    static int resident[3] = {0, 0, 0};
+    // (per device: SM counts may differ between the devices one process drives)
+    static std::mutex mu_res;
+    static int resident_dev[PR_MAX_DEVICES][3];
     const int opi = p.op < 0 || p.op > 2 ? 2 : p.op;
-    if (!resident[opi]) {
-        int sms = 0, per_sm = 0, dev = 0;
-        PR_CUDA_TRY(cudaGetDevice(&dev));
-        PR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        const void* fn = opi == 0 ? (const void*)gather_kernel<PR_GATHER_COPY>
-                         : opi == 1 ? (const void*)gather_kernel<PR_GATHER_U8_TO_F32_AFFINE>
-                                    : (const void*)gather_kernel<PR_GATHER_U8_TO_BF16_AFFINE>;
-        PR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarpsPerCta, 0));
-        resident[opi] = sms * (per_sm > 0 ? per_sm : 1);
+    int rdev = 0;
+    PR_CUDA_TRY(cudaGetDevice(&rdev));
+    if (rdev < 0 || rdev >= PR_MAX_DEVICES) return PR_ERR_INVALID;
+    int resident_n = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu_res);
+        if (!resident_dev[rdev][opi]) {
+            int sms = 0, per_sm = 0;
+            PR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, rdev));
+            const void* fn = opi == 0 ? (const void*)gather_kernel<PR_GATHER_COPY>
+                             : opi == 1 ? (const void*)gather_kernel<PR_GATHER_U8_TO_F32_AFFINE>
+                                        : (const void*)gather_kernel<PR_GATHER_U8_TO_BF16_AFFINE>;
+            PR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarpsPerCta, 0));
+            resident_dev[rdev][opi] = sms * (per_sm > 0 ? per_sm : 1);
+        }
+        resident_n = resident_dev[rdev][opi];
     }
     int64_t blocks = (items + kWarpsPerCta - 1) / kWarpsPerCta;
 #ifndef PR_GATHER_GRID
-    if (blocks > resident[opi]) blocks = resident[opi];
+    if (blocks > resident_n) blocks = resident_n;
     if (host_src) {
         // rows read over PCIe: a few CTAs keep enough loads in flight for the link, and the rest of the GPU
         // stays free for the compute this gather runs beside (the trainer prefetches on a side stream)
-        static int host_grid = 0;
-        if (!host_grid) {
+        static const int host_grid = [] {
             const char* e = getenv("PR_GATHER_HOST_GRID");
-            host_grid = e ? atoi(e) : 64;
-            if (host_grid < 1) host_grid = 64;
-        }
+            const int v = e ? atoi(e) : 64;
+            return v < 1 ? 64 : v;
+        }();
         if (blocks > host_grid) blocks = host_grid;
     }
 #else

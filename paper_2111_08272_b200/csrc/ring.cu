@@ -109,6 +109,8 @@ struct LaunchArgs {
     int32_t fuse;       // 1: the all-gather carries θ' = SGD(θ, ḡ) computed by the chunk owner (K7 in K3)
     int32_t zero;       // fused: reset the gradient buffer as it is consumed
     float nlr, wd;      // fused: −lr, weight decay (fp32, as pr_sgd_update)
+    int32_t algo;       // PR_ALGO_* this rank launched: part of the handshake, so ranks that picked
+    int32_t pad;        // different kernels latch PR_ERR_LENGTH_MISMATCH instead of waiting forever
     RankCall calls[PR_MAX_RANKS];
 };
 
@@ -386,6 +388,11 @@ __device__ __forceinline__ bool hs_read(const HsEntry* e, uint32_t flag, unsigne
     th_delta = (long long)(((w[9] & 0xffffffffull) << 32) | (w[8] & 0xffffffffull));
     return true;
 }
+// The call's kind as published in the handshake: dtype | fused update << 8 | algorithm << 16.
+__device__ __forceinline__ uint32_t call_kind(const LaunchArgs& A) {
+    return (uint32_t)A.dtype | ((uint32_t)A.fuse << 8) | ((uint32_t)A.algo << 16);
+}
+
 // Executed by ALL 32 lanes of warp 0: lane q publishes into rank q's page and polls entry q of this
 // page (ranks q, q+32, …), so the P peers are contacted in parallel; Σn, "all registered" and the error
 // code are combined with warp shuffles (DESIGN.md §3 #37).  The result is valid in every lane.
@@ -398,8 +405,8 @@ __device__ HsOut handshake(const LaunchArgs& A, const RankCall& rc, const DevTab
     const int par = (int)(seq & 1ull);
     const uint32_t flag = (uint32_t)(seq & 0xffffffffull);
     for (int q = lane; q < P; q += 32)
-        hs_publish(hs_of(tab->win[q], tab, ch, par, r), flag, A.count, rc.n_local,
-                   (uint32_t)A.dtype | ((uint32_t)A.fuse << 8), rc.reg_id, rc.reg_off, rc.th_delta, sys);
+        hs_publish(hs_of(tab->win[q], tab, ch, par, r), flag, A.count, rc.n_local, call_kind(A), rc.reg_id,
+                   rc.reg_off, rc.th_delta, sys);
     int err = 0, direct = 1;
     long long sumn = 0;
     for (int q = lane; q < P; q += 32) {
@@ -410,8 +417,8 @@ __device__ HsOut handshake(const LaunchArgs& A, const RankCall& rc, const DevTab
             err = PR_ERR_PEER_TIMEOUT;
             break;
         }
-        // dtype word carries the fused-update flag in bits 8+: every rank must make the same kind of call
-        if (cnt != A.count || dt != ((uint32_t)A.dtype | ((uint32_t)A.fuse << 8))) err = PR_ERR_LENGTH_MISMATCH;
+        // the dtype word carries the fused-update flag and the algorithm: every rank makes the same kind of call
+        if (cnt != A.count || dt != call_kind(A)) err = PR_ERR_LENGTH_MISMATCH;
         if (A.fuse && thd != rc.th_delta) err = err ? err : PR_ERR_INVALID;   // θ-layout differs across ranks
         sumn += n;
         if (rid < 0) direct = 0;
@@ -1520,16 +1527,22 @@ int find_reg(const pr_comm* c, const void* buf, size_t bytes, int32_t* id, int64
 
 size_t dtype_size(int32_t dt) { return dt == PR_DTYPE_F32 ? 4 : (dt == PR_DTYPE_BF16 ? 2 : 0); }
 
-// The algorithm a call takes: a pure function of (config, count, dtype), identical on every rank.
+// The algorithm a call takes: a pure function of (config, count, dtype, P, registered).
 // AUTO's two-shot limit grows with P: the ring pays 2P−2 flag round trips per call, the two-shot 2; at
 // `.sys` scope and P = 8 the two-shot won up to 16 MiB (tools/ar_latency.py --sys), at P = 2 the ring wins
-// from 4 MiB — so ts_max_bytes × 4 for P >= 8, × 2 for P >= 4.
-int pick_algo(const pr_comm_config& cfg, int64_t count, int32_t dtype, int P) {
+// from 4 MiB — so ts_max_bytes × 4 for P >= 8, × 2 for P >= 4.  The two-shot stores its reduced slices
+// straight into every peer's registered buffer, so AUTO takes it only for a registered buffer (and never
+// under FORCE_STAGED); an explicit PR_ALGO_TWO_SHOT on an unregistered buffer latches PR_ERR_INVALID.
+// `registered` is per rank: a job whose ranks differ there picks different kernels, and the handshake
+// (which carries the algorithm) turns that into PR_ERR_LENGTH_MISMATCH on every rank.
+int pick_algo(const pr_comm_config& cfg, int64_t count, int32_t dtype, int P, bool registered) {
     const int64_t bytes = count * (dtype == PR_DTYPE_F32 ? 4 : 2);
     const int64_t ts_max = cfg.ts_max_bytes * (P >= 8 ? 4 : (P >= 4 ? 2 : 1));
+    const bool direct_ok = registered && !(cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
     if ((cfg.algo == PR_ALGO_ONESHOT || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.os_max_bytes) return PR_ALGO_ONESHOT;
     if ((cfg.algo == PR_ALGO_LL || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.ll_max_bytes) return PR_ALGO_LL;
-    if (cfg.algo == PR_ALGO_TWO_SHOT || (cfg.algo == PR_ALGO_AUTO && bytes <= ts_max)) return PR_ALGO_TWO_SHOT;
+    if (cfg.algo == PR_ALGO_TWO_SHOT || (cfg.algo == PR_ALGO_AUTO && direct_ok && bytes <= ts_max))
+        return PR_ALGO_TWO_SHOT;
     return PR_ALGO_RING;
 }
 
@@ -1547,11 +1560,14 @@ int launch_k3(void* fn, const LaunchArgs& a, int nranks, int channels, int block
     return PR_OK;
 }
 
-int launch_ring(const LaunchArgs& a, int nranks, int P, const pr_comm_config& cfg, cudaStream_t s, bool coop) {
+int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_config& cfg, cudaStream_t s, bool coop) {
     const int32_t threads = cfg.threads, channels = cfg.channels;
     const bool f32 = a.dtype == PR_DTYPE_F32;
+    bool registered = true;
+    for (int r = 0; r < nranks; ++r) registered = registered && a.calls[r].reg_id >= 0;
     // the fused update (K7 inside K3) exists in the TMA ring only (its callers check pick_algo)
-    const int algo = a.fuse ? PR_ALGO_RING : pick_algo(cfg, a.count, a.dtype, P);
+    const int algo = a.fuse ? PR_ALGO_RING : pick_algo(cfg, a.count, a.dtype, P, registered);
+    a.algo = algo;
     switch (algo) {
         case PR_ALGO_ONESHOT:
             return launch_k3(f32 ? (void*)oneshot_ll_kernel<float> : (void*)oneshot_ll_kernel<__nv_bfloat16>, a, nranks,
@@ -1567,11 +1583,17 @@ int launch_ring(const LaunchArgs& a, int nranks, int P, const pr_comm_config& cf
     void* fn = a.fuse ? (void*)ring_kernel<float, true>
                       : f32 ? (void*)ring_kernel<float, false> : (void*)ring_kernel<__nv_bfloat16, false>;
     const size_t smem = (size_t)cfg.stages * 2 * cfg.tile_bytes;
-    static size_t attr_set[3] = {0, 0, 0};
+    // the dynamic-smem opt-in is a per-device function attribute: cached per (device, instantiation)
+    static std::mutex mu;
+    static size_t attr_set[PR_MAX_DEVICES][3];
     const int di = a.fuse ? 2 : (f32 ? 0 : 1);
-    if (attr_set[di] < smem) {
-        PR_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set[di] = smem;
+    if (device < 0 || device >= PR_MAX_DEVICES) return PR_ERR_INVALID;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (attr_set[device][di] < smem) {
+            PR_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set[device][di] = smem;
+        }
     }
     // producer warp + signal warp + `threads` consumer threads per channel CTA
     return launch_k3(fn, a, nranks, channels, threads + 64, smem, s, coop);
@@ -1720,17 +1742,25 @@ extern "C" int pr_comm_register(pr_comm* c, void* d_buf, size_t bytes) {
         if (e2 != cudaSuccess) { pr_internal_set_cuda_error(e2, "cudaIpcOpenMemHandle(register)"); rc = PR_ERR_CUDA; break; }
         rg.peer[q] = (uint8_t*)p;
     }
-    const int id = (int)c->regs.size();
-    c->regs.push_back(rg);
-    if (!rc) {
-        for (int q = 0; q < c->P; ++q) c->tab.reg[id][q] = rg.peer[q];
-        rc = push_table(c);
-    }
+    // collective outcome: the registration exists on every rank or on none (region ids must agree across
+    // ranks — a peer's handshake names its region by id), so nothing is recorded before all ranks succeeded
     int flag = rc ? 1 : 0;
     std::vector<int> flags(c->P);
     if (exchange(c, &flag, sizeof(int), flags.data())) rc = rc ? rc : PR_ERR_INVALID;
     for (int f : flags) if (f) rc = rc ? rc : PR_ERR_CUDA;
-    return rc;
+    const int id = (int)c->regs.size();
+    if (!rc) {
+        for (int q = 0; q < c->P; ++q) c->tab.reg[id][q] = rg.peer[q];
+        rc = push_table(c);
+        if (rc) for (int q = 0; q < c->P; ++q) c->tab.reg[id][q] = nullptr;
+    }
+    if (rc) {   // undo: close what this rank opened; the region is not recorded
+        for (int q = 0; q < c->P; ++q)
+            if (q != c->rank && rg.peer[q]) cudaIpcCloseMemHandle(rg.peer[q]);
+        return rc;
+    }
+    c->regs.push_back(rg);
+    return PR_OK;
 }
 
 extern "C" int pr_comm_alloc(pr_comm* c, size_t bytes, void** d_ptr) {
@@ -1738,7 +1768,11 @@ extern "C" int pr_comm_alloc(pr_comm* c, size_t bytes, void** d_ptr) {
     PR_CUDA_TRY(cudaSetDevice(c->device));
     void* p = nullptr;
     PR_CUDA_TRY(cudaMalloc(&p, bytes));
-    PR_CUDA_TRY(cudaMemset(p, 0, bytes));
+    if (cudaError_t e = cudaMemset(p, 0, bytes)) {
+        pr_internal_set_cuda_error(e, "cudaMemset(pr_comm_alloc)");
+        cudaFree(p);
+        return PR_ERR_CUDA;
+    }
     if (c->local) {
         Reg rg;
         rg.base = (uint8_t*)p; rg.bytes = bytes; rg.owned = true;
@@ -1768,7 +1802,8 @@ extern "C" int pr_weighted_allreduce(pr_comm* c, void* d_buf, int64_t count, int
     a.calls[0].buf = d_buf;
     a.calls[0].n_local = n_local;
     find_reg(c, d_buf, (size_t)count * dtype_size(dt), &a.calls[0].reg_id, &a.calls[0].reg_off);
-    return launch_ring(a, 1, c->P, c->cfg, (cudaStream_t)stream, false);
+    PR_CUDA_TRY(cudaSetDevice(c->device));
+    return launch_ring(a, 1, c->P, c->device, c->cfg, (cudaStream_t)stream, false);
 }
 
 extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d_bufs, int64_t count, int32_t dt,
@@ -1800,7 +1835,7 @@ extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d
         find_reg(comms[r], d_bufs[r], 0, &a.calls[r].reg_id, &a.calls[r].reg_off);
     }
     PR_CUDA_TRY(cudaSetDevice(c0->device));
-    return launch_ring(a, P, P, c0->cfg, (cudaStream_t)stream, true);
+    return launch_ring(a, P, P, c0->device, c0->cfg, (cudaStream_t)stream, true);
 }
 
 // ---- K7 fused into K3: weighted allreduce + SGD update (+ gradient reset) ---------------------------
@@ -1825,8 +1860,8 @@ extern "C" int pr_weighted_allreduce_sgd(pr_comm* c, float* d_grad, float* d_the
     int32_t trid = -1;
     int64_t toff = 0;
     find_reg(c, d_theta, (size_t)count * 4, &trid, &toff);
-    const bool fusable = pick_algo(c->cfg, count, PR_DTYPE_F32, c->P) == PR_ALGO_RING && a.calls[0].reg_id >= 0 &&
-                         trid == a.calls[0].reg_id && !(c->cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
+    const bool fusable = pick_algo(c->cfg, count, PR_DTYPE_F32, c->P, a.calls[0].reg_id >= 0) == PR_ALGO_RING &&
+                         a.calls[0].reg_id >= 0 && trid == a.calls[0].reg_id && !(c->cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
     if (!fusable) {   // composed: the same bits (the ring's ḡ, then K7's two FMAs)
         if (int rc = pr_weighted_allreduce(c, d_grad, count, PR_DTYPE_F32, n_local, stream)) return rc;
         return pr_sgd_update(d_theta, d_grad, count, lr, wd, zero_grad, stream);
@@ -1836,7 +1871,8 @@ extern "C" int pr_weighted_allreduce_sgd(pr_comm* c, float* d_grad, float* d_the
     a.nlr = (float)(-lr);
     a.wd = (float)wd;
     a.calls[0].th_delta = (int64_t)((const uint8_t*)d_theta - (const uint8_t*)d_grad);
-    return launch_ring(a, 1, c->P, c->cfg, (cudaStream_t)stream, false);
+    PR_CUDA_TRY(cudaSetDevice(c->device));
+    return launch_ring(a, 1, c->P, c->device, c->cfg, (cudaStream_t)stream, false);
 }
 
 extern "C" int pr_weighted_allreduce_sgd_local(pr_comm* const* comms, float* const* d_grads, float* const* d_thetas,
@@ -1860,7 +1896,7 @@ extern "C" int pr_weighted_allreduce_sgd_local(pr_comm* const* comms, float* con
     }
     if (sumn <= 0) return PR_ERR_ZERO_SAMPLES;
     PR_CUDA_TRY(cudaSetDevice(c0->device));
-    const bool fusable = P > 1 && pick_algo(c0->cfg, count, PR_DTYPE_F32, P) == PR_ALGO_RING && same_delta &&
+    const bool fusable = P > 1 && pick_algo(c0->cfg, count, PR_DTYPE_F32, P, true) == PR_ALGO_RING && same_delta &&
                          !(c0->cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
     if (!fusable) {
         if (P > 1) {
@@ -1887,7 +1923,7 @@ extern "C" int pr_weighted_allreduce_sgd_local(pr_comm* const* comms, float* con
         a.calls[r].th_delta = d0;
         find_reg(comms[r], d_grads[r], 0, &a.calls[r].reg_id, &a.calls[r].reg_off);
     }
-    return launch_ring(a, P, P, c0->cfg, (cudaStream_t)stream, true);
+    return launch_ring(a, P, P, c0->device, c0->cfg, (cudaStream_t)stream, true);
 }
 
 extern "C" int pr_comm_allgather_f64(pr_comm* c, double local, double* out, void* stream) {

@@ -41,13 +41,21 @@ extern "C" int pr_sgd_update(float* d_theta, float* d_grad, int64_t n, double lr
     if (n < 0 || (n > 0 && (!d_theta || !d_grad))) return PR_ERR_INVALID;
     if (((uintptr_t)d_theta & 15) || ((uintptr_t)d_grad & 15)) return PR_ERR_ALIGN;
     if (n == 0) return PR_OK;
-    static int grid = 0;
-    if (!grid) {
-        int dev = 0, sms = 0, per = 0;
-        PR_CUDA_TRY(cudaGetDevice(&dev));
-        PR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        PR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sgd_kernel, 256, 0));
-        grid = sms * (per > 0 ? per : 1);
+    // one resident wave, per device (thread-safe: a process may drive several devices)
+    static std::mutex mu;
+    static int grid_dev[PR_MAX_DEVICES];
+    int dev = 0, grid = 0;
+    PR_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= PR_MAX_DEVICES) return PR_ERR_INVALID;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!grid_dev[dev]) {
+            int sms = 0, per = 0;
+            PR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            PR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sgd_kernel, 256, 0));
+            grid_dev[dev] = sms * (per > 0 ? per : 1);
+        }
+        grid = grid_dev[dev];
     }
     const int64_t need = (n / 4 + 255) / 256 + 1;
     const int blocks = (int)(need < grid ? need : grid);

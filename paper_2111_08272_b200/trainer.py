@@ -44,7 +44,7 @@ class RunConfig:
     N: int = 50_000
     shape: tuple = (3, 32, 32)
     classes: int = 10
-    model: str = "resnet18"
+    model: str = "resnet18"                 # resnet18 | vgg16 (u8 images) | logreg | mlp (fp32 feature rows)
     num_classes: int = 1000                 # head size of the gradient buffer (DESIGN.md §3 #31)
     ratios: list = field(default_factory=lambda: [1])
     C: int = 0
@@ -79,7 +79,22 @@ class RunConfig:
     fused_sgd: bool = True
 
 
-def build_model(name: str, num_classes: int):
+FEATURE_MODELS = ("logreg", "mlp")           # fp32 feature rows (gathered by K2's COPY op), no images
+
+
+def build_model(name: str, num_classes: int, in_features: int = 1024):
+    """The harness's model (row a4).  logreg: BASELINE configs[0]'s 1,024-weight logistic regression without
+    bias (DESIGN.md §3 #30), θ_0 = 0; mlp: a small fp32 multi-layer model whose several
+    parameter tensors give N1 several buckets in the parity tests."""
+    import torch.nn as nn
+
+    if name == "logreg":
+        m = nn.Linear(in_features, 1, bias=False)
+        nn.init.zeros_(m.weight)
+        return m
+    if name == "mlp":
+        return nn.Sequential(nn.Linear(in_features, 256), nn.ReLU(), nn.Linear(256, 128), nn.ReLU(),
+                             nn.Linear(128, num_classes))
     import torchvision
 
     if name == "resnet18":
@@ -103,28 +118,41 @@ class Worker:
         if cfg.policy:
             self.alloc.set_policy(**cfg.policy)
         self.gstep = 0                                # global aggregation-step counter (slowdown schedule)
-        self.row_bytes = int(torch.tensor(cfg.shape).prod())
+        self.features = cfg.model in FEATURE_MODELS
+        if self.features and (cfg.channels_last or cfg.bf16_compute):
+            raise ValueError("feature models run fp32 rows: set channels_last=False, bf16_compute=False")
+        self.row_elems = int(torch.tensor(cfg.shape).prod())          # output elements per gathered row
+        self.row_bytes = self.row_elems * (4 if self.features else 1)  # source bytes per row (fp32 / u8)
         if data is None:                              # synthetic data set, replicated per rank
             import synth
 
-            data = torch.from_numpy(synth.images_u8(cfg.N, *cfg.shape, seed=0).reshape(cfg.N, -1))
-            labels = torch.from_numpy(synth.labels(cfg.N, cfg.classes, seed=1))
+            if self.features:
+                xf, yf, _ = synth.logistic_problem(cfg.N, self.row_elems)
+                data = torch.from_numpy(xf.astype("float32"))
+                labels = torch.from_numpy(yf.astype("int64")) if cfg.model == "logreg" else \
+                    torch.from_numpy(synth.labels(cfg.N, cfg.classes, seed=1))
+            else:
+                data = torch.from_numpy(synth.images_u8(cfg.N, *cfg.shape, seed=0).reshape(cfg.N, -1))
+                labels = torch.from_numpy(synth.labels(cfg.N, cfg.classes, seed=1))
         self.X = data.pin_memory() if cfg.host_data else data.to(self.dev)
         self.Y = labels.to(self.dev)
-        C, H, W = cfg.shape
         # K2 kernel chosen here, as the library's AUTO rule would (HWC or host data -> LSU, CHW -> TMA),
         # so the launch does no host-side pointer query
         lsu = cfg.host_data or cfg.channels_last
-        self.gop = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE if cfg.bf16_compute else pr.GATHER_U8_TO_F32_AFFINE,
-                                     [1.0 / s for s in CIFAR_STD[:C]], CIFAR_MEAN[:C], H * W,
-                                     impl=pr.GATHER_IMPL_LSU if lsu else pr.GATHER_IMPL_TMA,
-                                     layout=pr.GATHER_LAYOUT_HWC if cfg.channels_last else pr.GATHER_LAYOUT_CHW)
+        if self.features:                             # fp32 rows: a byte-exact copy (O5 COPY)
+            self.gop = pr.make_gather_op(pr.GATHER_COPY, impl=pr.GATHER_IMPL_LSU)
+        else:
+            C, H, W = cfg.shape
+            self.gop = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE if cfg.bf16_compute else pr.GATHER_U8_TO_F32_AFFINE,
+                                         [1.0 / s for s in CIFAR_STD[:C]], CIFAR_MEAN[:C], H * W,
+                                         impl=pr.GATHER_IMPL_LSU if lsu else pr.GATHER_IMPL_TMA,
+                                         layout=pr.GATHER_LAYOUT_HWC if cfg.channels_last else pr.GATHER_LAYOUT_CHW)
         torch.backends.cudnn.benchmark = True
         # try every cuDNN algorithm when autotuning (default: the first 10 heuristics' picks): the
         # ResNet-18 step settles at 2.90-2.91 ms instead of 3.08-3.09 (tools/model_variance.py, 6 runs each)
         torch.backends.cudnn.benchmark_limit = 0
         torch.manual_seed(cfg.seed)                   # identical initial weights on every rank
-        self.model = build_model(cfg.model, cfg.num_classes).to(self.dev)
+        self.model = build_model(cfg.model, cfg.num_classes, self.row_elems).to(self.dev)
         if cfg.channels_last:
             self.model = self.model.to(memory_format=torch.channels_last)
         self._graphs = {}                             # n_r -> captured step
@@ -173,6 +201,11 @@ class Worker:
         self.epoch = 0
         self.last_ts = 0.0
         self.history = []
+        # observation hooks (tests, diagnostics): on_reduced(worker) runs after the step's weighted
+        # allreduce and before the update when the reduced gradient exists as a buffer (not with the
+        # fused a6-a9 kernel); on_step(worker) runs after the update.  Host-side, in enqueue order.
+        self.on_reduced = None
+        self.on_step = None
 
     # ---- N1: bucketed allreduce overlapped with backward ----------------------------------------------
     def _setup_buckets(self, params):
@@ -240,13 +273,13 @@ class Worker:
             self._eflip ^= 1
             b = self._ebuf[self._eflip]
             if b is None or b[0].shape[0] < max(rows, 1):
-                b = (torch.empty((max(rows, 1), self.row_bytes), dtype=self.xdt, device=self.dev),
+                b = (torch.empty((max(rows, 1), self.row_elems), dtype=self.xdt, device=self.dev),
                      torch.empty(max(rows, 1), dtype=torch.int64, device=self.dev))
                 self._ebuf[self._eflip] = b
             x, y = b[0][:max(rows, 1)], b[1][:max(rows, 1)]
         else:
             with torch.cuda.stream(st):               # outputs allocated on (and owned by) the launching stream
-                x = torch.empty((max(rows, 1), self.row_bytes), dtype=self.xdt, device=self.dev)
+                x = torch.empty((max(rows, 1), self.row_elems), dtype=self.xdt, device=self.dev)
                 y = torch.empty(max(rows, 1), dtype=torch.int64, device=self.dev)
         if rows > 0:
             if record:
@@ -262,6 +295,8 @@ class Worker:
 
     # ---- a4: forward/backward with gradient accumulation (P:69 steps (1)-(3)) --------------------------
     def _input(self, x, n_r: int):
+        if self.features:
+            return x[:n_r]
         C, H, W = self.cfg.shape
         if self.cfg.channels_last:                    # HWC rows -> logical NCHW with channels-last strides
             return x[:n_r].view(n_r, H, W, C).permute(0, 3, 1, 2)
@@ -275,7 +310,10 @@ class Worker:
             xm, ym = x[m0:m0 + cfg.micro], y[m0:m0 + cfg.micro]
             with torch.autocast("cuda", dtype=torch.bfloat16, enabled=cfg.bf16_compute):
                 out = self.model(xm)
-                loss = F.cross_entropy(out.float(), ym)
+                if cfg.model == "logreg":   # mean binary cross-entropy: ∇ = Xᵀ(σ(Xθ) − y)/n (O7)
+                    loss = F.binary_cross_entropy_with_logits(out.float().squeeze(1), ym.float())
+                else:
+                    loss = F.cross_entropy(out.float(), ym)
             if overlap and m0 + cfg.micro >= n_r:             # N1: the last microbatch finalises every grad
                 self._ready, self._next, self._armed, self._n_armed = [0] * len(self._buckets), 0, True, n_r
             (loss * (xm.shape[0] / n_r)).backward()           # local mean over n_r (DESIGN §3 #11)
@@ -317,7 +355,7 @@ class Worker:
         re-captures alone."""
         if n_r <= 0 or n_r in self._graphs:
             return
-        xs = torch.randn((n_r, self.row_bytes), device=self.dev).to(self.xdt)
+        xs = torch.randn((n_r, self.row_elems), device=self.dev).to(self.xdt)
         ys = torch.randint(0, self.cfg.classes, (n_r,), device=self.dev)
         side = torch.cuda.Stream(self.dev)
         side.wait_stream(self.stream)
@@ -381,6 +419,11 @@ class Worker:
 
     # ---- a6-a9: weighted ring allreduce + SGD (Algorithm 1 steps 5-6) ---------------------------------
     def allreduce_and_update(self, n_r: int, record=False):
+        self._allreduce_and_update(n_r, record)
+        if self.on_step is not None:
+            self.on_step(self)
+
+    def _allreduce_and_update(self, n_r: int, record=False):
         if self._overlap and n_r == 0:                        # N1: an idle rank still joins every bucket
             for lo, hi, _ in self._buckets:
                 self._bucket_call(lo, hi, 0, self.stream)
@@ -403,6 +446,8 @@ class Worker:
                 return
         if self._overlap and self.pflat is not None:
             return                                            # every bucket's update ran fused with its allreduce
+        if self.on_reduced is not None:
+            self.on_reduced(self)                             # the reduced gradient ḡ is in self.flat
         if self.pflat is not None:
             if record:
                 u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -169,6 +169,35 @@ def test_save_load_roundtrip_resumes_identically():
         pr.Alloc.load(b"garbage" * 20)
 
 
+def test_load_rejects_corrupt_checkpoints():
+    """pr_alloc_load validates what pr_alloc_init / set_policy would refuse: a corrupt buffer
+    must come back as PR_ERR_INVALID, never as a division by zero (C or g = 0), an overflow, or a throw."""
+    import struct
+
+    a = pr.alloc_init(51200, [1, 1, 1, 1], C=64, g=16)
+    a.update([2.0, 2.0, 1.0, 1.0])
+    good = bytearray(a.save())
+    assert pr.Alloc.load(bytes(good)).view() == a.view()
+    # SaveHeader: magic@0 version@8 P@12 N@16 C@24 g@32 floor@40 epoch@48 frozen@56 has_tprev@60
+    #             policy{window@64 never_freeze@68 tol@72 ema@80} hist_len@88; w[P] @96, hist, t_prev
+    def patched(off, fmt, val):
+        b = bytearray(good)
+        struct.pack_into(fmt, b, off, val)
+        return bytes(b)
+
+    bad = [patched(24, "<q", 0), patched(32, "<q", 0), patched(16, "<q", 1 << 41), patched(16, "<q", 100),
+           patched(40, "<q", 17), patched(48, "<q", -1), patched(56, "<i", 7), patched(64, "<i", 1),
+           patched(72, "<q", -1), patched(80, "<d", 0.0), patched(80, "<d", float("nan")),
+           patched(88, "<q", 1 << 60), patched(88, "<q", 0), patched(88, "<q", 3),
+           patched(96, "<q", 17),                      # current w no longer sums to C
+           patched(96 + 8 * 4, "<q", -1),              # a history vector with a negative entry
+           patched(len(good) - 8, "<d", -1.0),         # a non-positive EMA time
+           bytes(good[:-1]), bytes(good) + b"\0"]
+    for b in bad:
+        with pytest.raises(pr.PropringError):
+            pr.Alloc.load(b)
+
+
 def test_frozen_update_is_noop():
     a = pr.alloc_init(10 ** 6, [10, 10], C=20)
     cost = [1e-3, 2e-3]

@@ -14,14 +14,45 @@ def _bench():
 
 
 def test_weak_and_strong_batch_rule():
+    """Default = strong scaling (SURVEY §8(d) Scaling row: fixed global batch 1,024 for every N)."""
     b = _bench()
     for n in (1, 2, 4, 8):
-        assert b.units_for(n) == 64 * n and b.units_for(n, strong=True) == 64
-        cw, cs = b.bench_config(n), b.bench_config(n, strong=True)
+        assert b.units_for(n) == 64 and b.units_for(n, strong=False) == 64 * n
+        cs, cw = b.bench_config(n), b.bench_config(n, strong=False)
         assert cw["global_batch"] == 1024 * n and cs["global_batch"] == 1024
         assert cw["step"] == f"one epoch (S={50_000 // (1024 * n)} aggregations)"
+        assert cs["step"] == "one epoch (S=48 aggregations)" and cs["scaling"] == "strong"
         assert cw["parallelism"] == f"dp{n}"
-    assert b.bench_config(1) == b.bench_config(1, strong=True)   # N = 1: the two modes coincide
+        v = b.bench_config(n, workload="vgg16")
+        assert v["global_batch"] == 1024 and v["step"] == "one epoch (S=50 aggregations)"
+        assert "138,357,544" in v["workload"]
+    c1s, c1w = b.bench_config(1), b.bench_config(1, strong=False)
+    c1s.pop("scaling"), c1w.pop("scaling")
+    assert c1s == c1w                                              # N = 1: the two modes coincide
+
+
+def test_self_launch_command(monkeypatch):
+    """--gpus N > 1 without WORLD_SIZE re-runs bench.py under torch.distributed.run (127.0.0.1)."""
+    b = _bench()
+    seen = {}
+    monkeypatch.setattr(b.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    a = b.parse(["--gpus", "4", "--steps", "2"])
+    b.self_launch(a, ["--gpus", "4", "--steps", "2"])
+    cmd = seen["cmd"]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1" and cmd[-3:] == ["--gpus", "4", "--steps", "2"][-3:]
+
+
+def test_reference_arm_does_not_load_the_product():
+    """The oracle arm builds torchvision's ResNet-18 directly: importing bench + running its setup must not
+    load libpropring.so (VERDICT r1 "What's weak" #1)."""
+    import subprocess
+
+    code = ("import sys; sys.argv=['bench.py']; import bench; bench.cpu_reference_setup(1); "
+            "import os; maps=open('/proc/self/maps').read(); print('LOADED' if 'libpropring' in maps else 'CLEAN'); "
+            "print('MOD' if any(m.startswith('paper_2111_08272_b200') for m in sys.modules) else 'NOMOD')")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300).stdout
+    assert "CLEAN" in out and "NOMOD" in out, out
 
 
 def test_oracle_leg_allocation_matches_timed_arm():
@@ -29,8 +60,10 @@ def test_oracle_leg_allocation_matches_timed_arm():
 
     b = _bench()
     for n in (1, 2, 8):
-        a = OA.alloc_init(b.N_DATA, [1] * n, C=b.units_for(n), g=b.G_UNIT)
+        a = OA.alloc_init(b.N_DATA, [1] * n, C=b.units_for(n, strong=False), g=b.G_UNIT)
         assert a.n == [1024] * n and a.S == 50_000 // (1024 * n)
+        s = OA.alloc_init(b.N_DATA, [1] * n, C=b.units_for(n), g=b.G_UNIT)
+        assert sum(s.n) == 1024 and s.S == 48
 
 
 def test_mix_ceiling_parser(tmp_path, monkeypatch):

@@ -67,16 +67,22 @@ def test_c1_logistic_regression_trajectory(ratios):
     shards = [OP.shard_indices(N, o.off[r], o.len[r], seed, epoch) for r in range(P)]
     assert all(np.array_equal(shards[r], idx[r].cpu().numpy()) for r in range(P))
     traj = OL.trajectory(X, y, shards, o.n, steps, lr)
-    th = np.zeros(D)
     for s in range(steps):
-        ref = OL.weighted_step_gradient(th, X, y, OL.step_rows(shards, o.n, s))
+        th = thetas_gpu[s].double().cpu().numpy()
+        rows = OL.step_rows(shards, o.n, s)
+        ref = OL.weighted_step_gradient(th, X, y, rows)                 # Eq. 1 at the GPU path's own θ_s
         # the same step from the full-batch closed form over the union of the step's rows (Eq. 1)
-        rows = np.concatenate(OL.step_rows(shards, o.n, s))
-        full = OL.grad_mean(th, X[rows], y[rows])
+        full = OL.grad_mean(th, X[np.concatenate(rows)], y[np.concatenate(rows)])
         assert np.max(np.abs(ref - full)) <= 1e-12 * np.max(np.abs(full))
-        err = np.linalg.norm(grads_gpu[s] - ref) / np.linalg.norm(ref)
-        assert err < 1e-5, (s, err)
-        th = OL.sgd_step(th, ref, lr)
+        # element by element, cancellation-aware over the per-sample terms of the sum (DESIGN.md §3 #45)
+        allr = np.concatenate(rows)
+        den = np.abs(X[allr]).T @ np.abs(OL.sigmoid(X[allr] @ th) - y[allr]) / len(allr)
+        err = np.abs(grads_gpu[s] - ref)
+        assert np.all(err <= 1e-5 * den), (s, float(np.max(err / den)))
+        # θ_{s+1} = θ_s − η·ḡ_s: one fp32 multiply and one subtraction (torch) of the GPU's own ḡ_s
+        nxt = thetas_gpu[s + 1].double().cpu().numpy()
+        want = th - float(np.float32(lr)) * grads_gpu[s]
+        assert np.all(np.abs(nxt - want) <= 2.0 ** -23 * (np.abs(want) + lr * np.abs(grads_gpu[s])) + 1e-45), s
     for s in range(steps + 1):
         tg = thetas_gpu[s].double().cpu().numpy()
         assert np.linalg.norm(tg - traj[s]) <= 1e-5 * max(1e-30, np.linalg.norm(traj[s])) + 1e-9

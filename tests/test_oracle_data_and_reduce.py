@@ -164,6 +164,39 @@ def test_linmodel_weighted_shards_equal_full_batch():
     assert np.max(np.abs(ws - full)) <= 1e-12 * np.max(np.abs(full))
 
 
+def test_linmodel_trajectory_hand_derived_two_steps():
+    """Pin of O7's trajectory() (VERDICT r1 "What's weak" #2) with a case worked by hand, so a shifted step
+    (wrong rows, θ appended before the update, a dropped weight decay or weight) fails here on the CPU.
+
+    D = 1, N = 6, two ranks with n = [1, 2] (weights 1/3, 2/3), shards rank 0 = rows [0, 1], rank 1 =
+    rows [2, 3, 4, 5]; x = [1, 2, 1, -1, 3, 0.5], y = [1, 0, 0, 1, 1, 0]; η = 0.5, λ = 0.1, θ_0 = 0.
+      step 0 rows: rank 0 {0}, rank 1 {2, 3}.  σ(0) = 1/2 so residuals σ − y = [-1/2 | 1/2, -1/2]:
+        g_0 = 1/3·(1·(−1/2)) + 2/3·½·(1·½ + (−1)·(−½)) = −1/6 + 1/3 = 1/6
+        θ_1 = 0 − ½·(1/6 + 0.1·0) = −1/12
+      step 1 rows: rank 0 {1}, rank 1 {4, 5}, at θ_1 = −1/12:
+        g_1 = 1/3·2·σ(−1/6) + 2/3·½·(3·(σ(−1/4) − 1) + ½·σ(−1/24))
+        θ_2 = θ_1 − ½·(g_1 + 0.1·θ_1)
+    """
+    import math
+
+    def sig(z):
+        return 1.0 / (1.0 + math.exp(-z))
+
+    X = np.array([[1.0], [2.0], [1.0], [-1.0], [3.0], [0.5]])
+    y = np.array([1.0, 0.0, 0.0, 1.0, 1.0, 0.0])
+    shards = [np.array([0, 1]), np.array([2, 3, 4, 5])]
+    traj = LM.trajectory(X, y, shards, [1, 2], 2, 0.5, 0.1)
+    th1 = -1.0 / 12.0
+    g1 = (1 / 3) * 2 * sig(-1 / 6) + (2 / 3) * 0.5 * (3 * (sig(-1 / 4) - 1) + 0.5 * sig(-1 / 24))
+    th2 = th1 - 0.5 * (g1 + 0.1 * th1)
+    assert len(traj) == 3
+    assert traj[0][0] == 0.0
+    assert abs(traj[1][0] - th1) <= 1e-15
+    assert abs(traj[2][0] - th2) <= 1e-15
+    # the step gradient at θ_0 is the hand value 1/6
+    assert abs(LM.weighted_step_gradient(np.zeros(1), X, y, LM.step_rows(shards, [1, 2], 0))[0] - 1 / 6) <= 1e-15
+
+
 def test_linmodel_allocation_invariance():
     """[1,3] vs [2,2] over the same global rows per step give the same θ."""
     X, y, _ = synth.logistic_problem()
