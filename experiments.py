@@ -63,6 +63,66 @@ SCHEDULES = {
 }
 
 
+def step_cost(n, sigma, a, b, spin, c0):
+    """Modelled step time (s) of a rank σ× slower that processes n rows, with the σ = 1 step affine in the
+    rows, t1(n) = a + b·n (fitted to the measured t1): "t1" emulation σ·t1(n); "sample" t1(n) + (σ−1)·c0·n."""
+    if n <= 0:
+        return 0.0
+    t1 = a + b * n
+    return sigma * t1 if spin == "t1" else t1 + (sigma - 1.0) * c0 * n
+
+
+def affine_minmax(a, b, sigma, g, C, floor=1, spin="t1", c0=0.0):
+    """The best integer allocation for affine step costs: min over w (Σw = C, w_r >= floor, units of g rows)
+    of max_r step_cost(g·w_r).  Costs are increasing in w, so for a candidate T every rank takes the most
+    units that keep it <= T; the smallest candidate T (over all achievable per-rank step times) whose
+    greedy allocation reaches C is optimal.  Returns (T_step, w)."""
+    P = len(sigma)
+    cands = sorted({step_cost(g * w, sigma[r], a, b, spin, c0) for r in range(P) for w in range(floor, C + 1)})
+    for T in cands:
+        w = []
+        for r in range(P):
+            k = floor - 1
+            for u in range(floor, C + 1):
+                if step_cost(g * u, sigma[r], a, b, spin, c0) <= T:
+                    k = u
+            w.append(k)
+        if min(w) >= floor and sum(w) >= C:
+            # trim the surplus one unit at a time from the currently costliest rank (any trim keeps max <= T;
+            # this one also minimises the remaining ranks' times lexicographically)
+            for _ in range(sum(w) - C):
+                r = max((i for i in range(P) if w[i] > floor),
+                        key=lambda i: (step_cost(g * w[i], sigma[i], a, b, spin, c0), -i))
+                w[r] -= 1
+            return T, w
+    raise ValueError("no feasible allocation")
+
+
+def fit_affine(ns, ts):
+    """Least-squares t1(n) = a + b·n over the measured (n, t1) points (b = 0 if only one n)."""
+    if len(ns) == 1:
+        return ts[0], 0.0
+    mn, mt = sum(ns) / len(ns), sum(ts) / len(ts)
+    b = sum((x - mn) * (y - mt) for x, y in zip(ns, ts)) / sum((x - mn) ** 2 for x in ns)
+    return mt - b * mn, b
+
+
+METRICS_HEADER = "scenario,epoch,rank,w,n,len,t_s_ns,t_w_ns,t_c_ns,T_ns,loss\n"
+
+
+def write_metrics_rows(path, scenario, epoch, w, n, lens, t_s, t_w, t_c, T, loss):
+    """SURVEY §5 per-(epoch, rank) metrics CSV: epoch,rank,w,n,len,t_s_ns,t_w_ns,t_c_ns,T_ns,loss (times summed
+    over the epoch; t_w = barrier wait, t_c = the exchange itself, T = the epoch's wall time on the device)."""
+    new = not os.path.exists(path) or os.path.getsize(path) == 0
+    with open(path, "a") as f:
+        if new:
+            f.write(METRICS_HEADER)
+        for r in range(len(w)):
+            ln = "" if lens is None else str(int(lens[r]))
+            f.write(f"{scenario},{epoch},{r},{int(w[r])},{int(n[r])},{ln},{t_s[r] * 1e9:.0f},{t_w[r] * 1e9:.0f},"
+                    f"{t_c * 1e9:.0f},{T * 1e9:.0f},{loss:.6g}\n")
+
+
 def run_virtual(args):
     """All P ranks of a scenario on ONE GPU, one after another (--virtual).
 
@@ -90,12 +150,13 @@ def run_virtual(args):
         policy["ema_alpha"] = args.ema
     cfg = RunConfig(N=N, shape=shape, model=model, ratios=ratios, C=C, g=g, slowdown=sigma,
                     adaptive=adaptive and not args.static, micro=args.micro or (256 if model == "vgg16" else 1024),
-                    adapt_every=k, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario))
+                    adapt_every=k, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario), spin=args.spin)
     w = Worker(cfg, 0, 1, 0, None)
     comms = pr.comm_init_local(P, 0, pr.comm_config())
     bufs = [torch.zeros(w.L, dtype=torch.float32, device="cuda") for _ in range(P)]
     idx = [torch.empty(N, dtype=torch.int64, device="cuda") for _ in range(P)]
     totals = {"T": 0.0, "bound": 0.0}
+    last_T = last_bound = last_tc = None
     for e in range(args.epochs):
         S = w.alloc.view()["S"]
         seg = k if k > 0 else S
@@ -104,6 +165,8 @@ def run_virtual(args):
             v = w.alloc.view()
             n, ns = v["n"], min(seg, S - s0)
             ws.append(v["w"])
+            if s0 == 0:
+                lens0 = v["len"]
             xs, ys = [], []
             for r in range(P):                            # a2 + a3 for every rank
                 if k > 0:
@@ -153,6 +216,14 @@ def run_virtual(args):
         ts = [sum(sum(t[r]) for _, t, _ in rows) for r in range(P)]
         totals["T"] += T
         totals["bound"] += bound
+        last_T, last_bound, last_tc = T, bound, sum(sum(tc) for _, _, tc in rows) / S
+        if args.metrics_csv:
+            tw = [sum(sum(max(t[q][j] for q in range(P)) - t[r][j] for j in range(len(tc))) for _, t, tc in rows)
+                  for r in range(P)]
+            write_metrics_rows(args.metrics_csv, args.scenario, e, ws[0], [sum(nn_[r] for nn_, _, _ in rows[:1])
+                                                                         for r in range(P)],
+                               lens0, ts, tw, sum(sum(tc) for _, _, tc in rows), T,
+                               float(torch.stack(losses).mean()) if losses else float("nan"))
         rec = {"scenario": args.scenario, "mode": "virtual", "adapt_every": k, "epoch": e, "w": ws[0],
                "w_end": w.alloc.view()["w"], "frozen": w.alloc.view()["frozen"], "t_s": ts,
                "T_emulated": T, "bound": bound, "T_over_bound": T / bound,
@@ -161,9 +232,28 @@ def run_virtual(args):
             rec["w_segments"] = ws
         print(json.dumps(rec), flush=True)
         w.epoch += 1
-    print(json.dumps({"scenario": args.scenario, "mode": "virtual", "adapt_every": k, "static": args.static,
-                      "epochs": args.epochs, "T_total": totals["T"], "bound_total": totals["bound"],
-                      "T_over_bound": totals["T"] / totals["bound"]}), flush=True)
+    # the affine-cost bound: t1(n) measured at (at least) two row counts, fitted a + b·n; the best integer
+    # allocation's step time under the same emulation (what any controller could reach), vs the linear
+    # Σspeed bound above (which assumes t_s ∝ samples, and is unattainable with a fixed step cost)
+    n_eq = w.alloc.view()["B"] // P
+    for nn in (max(1, n_eq // 2), n_eq, 2 * n_eq):
+        w.t1(nn)
+    pts = sorted((nn, ent[4] / 1e9) for nn, ent in w._graphs.items())
+    a0, b0 = fit_affine([p_[0] for p_ in pts], [p_[1] for p_ in pts])
+    v = w.alloc.view()
+    t_step, w_opt = affine_minmax(a0, b0, sigma, g, C, cfg.floor, args.spin, w.c0_ns / 1e9)
+    tc_mean = last_tc if last_tc is not None else 0.0
+    S = v["S"]
+    bound_aff = S * (t_step + tc_mean)
+    print(json.dumps({"scenario": args.scenario, "mode": "virtual", "spin": args.spin, "adapt_every": k,
+                      "static": args.static, "epochs": args.epochs, "T_total": totals["T"],
+                      "bound_total": totals["bound"], "T_over_bound": totals["T"] / totals["bound"],
+                      "t1_points": pts, "affine_fit": {"a_s": a0, "b_s_per_row": b0}, "c0_s_per_row": w.c0_ns / 1e9,
+                      "affine_opt_w": w_opt, "affine_opt_step_s": t_step,
+                      "affine_bound_epoch_s": bound_aff, "last_epoch_T": last_T,
+                      "last_epoch_T_over_affine_bound": (last_T / bound_aff) if last_T else None,
+                      "last_epoch_T_over_linear_bound": (last_T / last_bound) if last_T else None,
+                      "final_w": v["w"]}), flush=True)
     for c in comms:
         c.destroy()
 
@@ -182,6 +272,9 @@ def main():
                     help="N3: controller every k aggregation steps over the step-interleaved shard (0 = per epoch)")
     ap.add_argument("--never-freeze", action="store_true", help="keep adapting after the ratio is stable")
     ap.add_argument("--ema", type=float, default=1.0, help="EMA weight on t_s (1 = raw, S:166)")
+    ap.add_argument("--metrics-csv", default="", help="append the per-(epoch, rank) metrics CSV (SURVEY §5) here")
+    ap.add_argument("--spin", default="t1", choices=["t1", "sample"],
+                    help="K4 emulation: t1 = (σ−1)·t1(n_r) per step; sample = (σ−1)·c0·n_r (SURVEY §8(a) a4)")
     args = ap.parse_args()
     if args.virtual:
         return run_virtual(args)
@@ -211,7 +304,8 @@ def main():
         policy["ema_alpha"] = args.ema
     cfg = RunConfig(N=N, shape=shape, model=model, ratios=ratios, C=C, g=g, slowdown=sigma,
                     adaptive=adaptive and not args.static, micro=args.micro or (256 if model == "vgg16" else 1024),
-                    adapt_every=args.adapt_every, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario))
+                    adapt_every=args.adapt_every, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario),
+                    spin=args.spin)
     wk = Worker(cfg, rank, world, local, comm)
     wk.calibrate()
     c0 = torch.tensor([wk.c0_ns], dtype=torch.float64, device=tdev)
@@ -246,6 +340,10 @@ def main():
                               "frozen": wk.alloc.view()["frozen"], "t_s": ts,
                               "t_w": [x - min(ars) for x in ars], "T": Tmax, "bound": bound,
                               "T_over_bound": Tmax / bound, "loss": rec["loss"]}), flush=True)
+            if args.metrics_csv:
+                lens = wk.alloc.view()["len"]                 # the shards of this epoch (updated at the next boundary)
+                write_metrics_rows(args.metrics_csv, args.scenario, e, rec["w"], [int(x) for x in n],
+                                   lens, ts, [x - min(ars) for x in ars], min(ars), Tmax, rec["loss"])
     comm.destroy()
     dist.destroy_process_group()
 

@@ -180,6 +180,12 @@ int pr_spin(int64_t ns, void *stream);
  * Errors: PR_ERR_INVALID, PR_ERR_CUDA. */
 int pr_stamp(int64_t *d_ring, int64_t cap, void *stream);
 
+/* t_s of a segment from pr_stamp pairs, on the device (row a5 without a host synchronisation, for the
+ * asynchronous controller exchange below): *d_out = Σ_{i < k/2} (ring[2 + 2i] − ring[1 + 2i]) · 1e-9 s,
+ * k = min(ring[0], cap) stamps recorded as (start, end) pairs.  d_ring: device int64[1 + cap];
+ * d_out: device double.  Stream-ordered.  Errors: PR_ERR_INVALID, PR_ERR_CUDA. */
+int pr_stamp_seconds(const int64_t *d_ring, int64_t cap, double *d_out, void *stream);
+
 /* SGD update, §8(a) row a9: Eq. 1 with weight decay, applied to the reduced
  * gradient, fused with the gradient reset for the next aggregation:
  *   θ[i] ← fma(−lr, fma(wd, θ[i], g[i]), θ[i]);   if zero_grad: g[i] ← 0
@@ -317,6 +323,15 @@ int pr_weighted_allreduce_sgd_local(pr_comm *const *comms, float *const *d_grads
 /* Algorithm 1 step 1: every rank contributes `local` and receives all P values in rank
  * order into host out[P].  Synchronous (waits for `stream`). */
 int pr_comm_allgather_f64(pr_comm *c, double local, double *out, void *stream);
+
+/* The same exchange without a host synchronisation (K6 asynchronous): the local value is read from
+ * device memory when the kernel runs (d_local: device double, e.g. written by pr_stamp_seconds) and the
+ * P values land in h_out[P] — PINNED host memory (cudaHostAlloc / torch pin_memory), written by the
+ * device — stream-ordered.  The caller records an event behind the call and reads h_out after it; the
+ * controller can then act one segment later without stalling the stream.  Errors: PR_ERR_INVALID
+ * (local group, null pointer, h_out not device-accessible), PR_ERR_CUDA; peer timeouts latch in
+ * pr_comm_status. */
+int pr_comm_allgather_f64_async(pr_comm *c, const double *d_local, double *h_out, void *stream);
 
 /* Latched device error of the last completed call (PR_OK if none). Non-blocking host read. */
 int pr_comm_status(pr_comm *c);

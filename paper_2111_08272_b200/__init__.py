@@ -221,6 +221,11 @@ def stamp(ring, stream=None):
     _check(LIB.pr_stamp(_ptr(ring), ring.numel() - 1, _stream(stream)), "pr_stamp")
 
 
+def stamp_seconds(ring, out, stream=None):
+    """out (device float64 scalar tensor) = Σ over ring's (start, end) stamp pairs, in seconds (a5 on device)."""
+    _check(LIB.pr_stamp_seconds(_ptr(ring), ring.numel() - 1, _ptr(out), _stream(stream)), "pr_stamp_seconds")
+
+
 def sgd_update(theta, grad, lr: float, wd: float = 0.0, zero_grad: bool = True, stream=None):
     """a9: θ ← θ − lr·(g + wd·θ) (two fp32 FMAs) and, if zero_grad, g ← 0 — one pass over flat fp32
     buffers (Eq. 1; wd P:235)."""
@@ -310,6 +315,12 @@ class Comm:
         out = (ctypes.c_double * P)()
         _check(LIB.pr_comm_allgather_f64(self._h, float(x), out, _stream(stream)), "pr_comm_allgather_f64")
         return list(out)
+
+    def allgather_f64_async(self, d_local, h_out, stream=None):
+        """K6 without a host synchronisation: d_local (device float64 scalar) -> h_out (pinned float64 [P]),
+        stream-ordered; read h_out after an event recorded behind this call."""
+        _check(LIB.pr_comm_allgather_f64_async(self._h, _ptr(d_local), _ptr(h_out), _stream(stream)),
+               "pr_comm_allgather_f64_async")
 
     def status(self) -> int:
         return LIB.pr_comm_status(self._h)

@@ -64,6 +64,7 @@ SIGNATURES = {
     "pr_gather_rows": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_i64, c_vp, ctypes.POINTER(GatherOp), c_vp, c_vp, c_vp]),
     "pr_spin": (ctypes.c_int, [c_i64, c_vp]),
     "pr_stamp": (ctypes.c_int, [c_vp, c_i64, c_vp]),
+    "pr_stamp_seconds": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp]),
     "pr_sgd_update": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_i32, c_vp]),
     "pr_comm_init": (ctypes.c_int, [ctypes.POINTER(c_vp), c_i32, c_i32, c_i32, EXCHANGE_FN, c_vp,
                                     ctypes.POINTER(CommConfig)]),
@@ -77,6 +78,7 @@ SIGNATURES = {
     "pr_weighted_allreduce_sgd_local": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp),
                                                        c_i64, ctypes.POINTER(c_i64), c_dbl, c_dbl, c_i32, c_vp]),
     "pr_comm_allgather_f64": (ctypes.c_int, [c_vp, c_dbl, ctypes.POINTER(c_dbl), c_vp]),
+    "pr_comm_allgather_f64_async": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "pr_comm_status": (ctypes.c_int, [c_vp]),
     "pr_comm_timestamps": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64)]),
     "pr_comm_rank": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),

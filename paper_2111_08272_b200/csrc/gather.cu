@@ -644,7 +644,23 @@ __global__ void stamp_kernel(int64_t* ring, int64_t cap) {
     const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(ring), 1ull);
     ring[1 + (int64_t)(i % (unsigned long long)cap)] = (int64_t)t;
 }
+// Σ over the recorded (start, end) pairs, in seconds; one warp (lane-strided partial sums + shuffle).
+__global__ void stamp_seconds_kernel(const int64_t* ring, int64_t cap, double* out) {
+    const int64_t k = min(ring[0], cap);
+    long long acc = 0;
+    for (int64_t i = threadIdx.x; 2 * i + 1 < k; i += 32) acc += ring[2 + 2 * i] - ring[1 + 2 * i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) *out = (double)acc * 1e-9;
+}
 }  // namespace
+
+extern "C" int pr_stamp_seconds(const int64_t* d_ring, int64_t cap, double* d_out, void* stream) {
+    if (!d_ring || !d_out || cap < 1) return PR_ERR_INVALID;
+    stamp_seconds_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_ring, cap, d_out);
+    PR_CUDA_TRY(cudaGetLastError());
+    return PR_OK;
+}
 
 extern "C" int pr_stamp(int64_t* d_ring, int64_t cap, void* stream) {
     if (!d_ring || cap < 1) return PR_ERR_INVALID;

@@ -1310,8 +1310,10 @@ __global__ void __launch_bounds__(512, 1) oneshot_ll_kernel(const __grid_constan
     if (t0 && ch == 0) tab->stamps[2] = (long long)gtimer();
 }
 
-__global__ void allgather_f64_kernel(const DevTable* tab, unsigned long long seq, double v, double* out) {
+__global__ void allgather_f64_kernel(const DevTable* tab, unsigned long long seq, double v, const double* vp,
+                                     double* out) {
     if (threadIdx.x != 0) return;
+    if (vp) v = *vp;                                   // asynchronous form: the value is on the device
     const bool sys = tab->sysscope != 0;
     const int r = tab->rank, P = tab->P;
     const int par = (int)(seq & 1ull);
@@ -1934,11 +1936,32 @@ extern "C" int pr_comm_allgather_f64(pr_comm* c, double local, double* out, void
     double* d_out = nullptr;
     PR_CUDA_TRY(cudaHostGetDevicePointer((void**)&d_out, c->h_ag, 0));
     c->ag_seq += 1;
-    allgather_f64_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->d_tab, c->ag_seq, local, d_out);
+    allgather_f64_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->d_tab, c->ag_seq, local, nullptr, d_out);
     PR_CUDA_TRY(cudaGetLastError());
     PR_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
     if (int st = *(volatile int*)c->h_status) return st;
     for (int q = 0; q < c->P; ++q) out[q] = ((volatile double*)c->h_ag)[q];
+    return PR_OK;
+}
+
+extern "C" int pr_comm_allgather_f64_async(pr_comm* c, const double* d_local, double* h_out, void* stream) {
+    if (!c || !d_local || !h_out || c->local) return PR_ERR_INVALID;
+    if (int st = *(volatile int*)c->h_status) return st;
+    PR_CUDA_TRY(cudaSetDevice(c->device));
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h_out) != cudaSuccess || at.type != cudaMemoryTypeHost || !at.devicePointer) {
+        cudaGetLastError();
+        return PR_ERR_INVALID;                         // must be pinned host memory the device can write
+    }
+    if (c->P == 1) {                                   // identity: one stream-ordered copy
+        PR_CUDA_TRY(cudaMemcpyAsync(at.devicePointer, d_local, sizeof(double), cudaMemcpyDeviceToDevice,
+                                    (cudaStream_t)stream));
+        return PR_OK;
+    }
+    c->ag_seq += 1;
+    allgather_f64_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(c->d_tab, c->ag_seq, 0.0, d_local,
+                                                            reinterpret_cast<double*>(at.devicePointer));
+    PR_CUDA_TRY(cudaGetLastError());
     return PR_OK;
 }
 

@@ -65,6 +65,11 @@ class RunConfig:
     # aggregation steps over the step-interleaved shard (pr_shard_steps) and calls the controller at every
     # segment boundary with that segment's t_s; 0 = once per epoch (Algorithm 1 as written).
     adapt_every: int = 0
+    # N3 exchange cadence: 0 = the segment's t_s is read on the host (CUDA events) and exchanged with the
+    # synchronous K6 before the next segment; 1 = t_s is summed on the device from %globaltimer stamps and
+    # exchanged with the asynchronous K6 (pinned host result, no stream synchronisation), and the
+    # controller applies segment j's times before segment j + 2 (one segment of lag, DESIGN.md §3 #47)
+    adapt_lag: int = 0
     policy: dict | None = None              # Alloc.set_policy kwargs (e.g. never_freeze, ema_alpha)
     # time-varying stragglers: [(global_step, [σ_r ...]), ...]; σ at step s = the last entry with step <= s
     slowdown_schedule: list | None = None
@@ -77,6 +82,11 @@ class RunConfig:
     # a9 through the library's fused kernel (pr_sgd_update: SGD + gradient reset in one pass over flat
     # fp32 parameter / gradient buffers) instead of torch.optim.SGD + a separate memset
     fused_sgd: bool = True
+    # K4 emulation of a rank σ_r× slower (DESIGN.md §3 #46): "t1" spins (σ_r − 1)·t1(n_r) after each step —
+    # the rank's whole step (fixed + per-sample cost) takes σ_r× its own σ = 1 time; "sample" spins
+    # (σ_r − 1)·c0·n_r — SURVEY §8(a) a4's per-sample spin, c0 = t1(n)/n at the first n_r this rank runs
+    # (only the per-sample part is slowed; every rank pays the same fixed cost).
+    spin: str = "t1"
 
 
 FEATURE_MODELS = ("logreg", "mlp")           # fp32 feature rows (gathered by K2's COPY op), no images
@@ -344,9 +354,15 @@ class Worker:
                 return float(cur[rank])
         return float(self.cfg.slowdown[rank]) if self.cfg.slowdown else 1.0
 
-    def _spin_ns(self, n_r: int) -> int:
+    def _spin_ns(self, n_r: int, t1_ns: float = 0.0) -> int:
+        """K4 spin of this rank at the current step: (σ−1)·t1(n_r) ("t1"), or (σ−1)·c0·n_r ("sample", and the
+        eager path without a captured t1)."""
         sigma = self.sigma() if self.cfg.slowdown or self.cfg.slowdown_schedule else 1.0
-        return int((sigma - 1.0) * self.c0_ns * n_r) if sigma > 1.0 and self.c0_ns > 0 else 0
+        if sigma <= 1.0:
+            return 0
+        if self.cfg.spin == "t1" and t1_ns > 0:
+            return int((sigma - 1.0) * t1_ns)
+        return int((sigma - 1.0) * self.c0_ns * n_r) if self.c0_ns > 0 else 0
 
     def prepare(self, n_r: int, calib_reps: int = 3):
         """Capture the forward/backward of n_r rows in a CUDA graph and time its replay, t1(n_r) — the
@@ -392,7 +408,10 @@ class Worker:
                 loss2 = self.compute(xs, ys, n_r, overlap=True)
             self.stream.wait_stream(side)
             self.cfg.slowdown, self.cfg.slowdown_schedule = save, save_sched
-        self._graphs[n_r] = (g, xs, ys, loss, a.elapsed_time(b) * 1e6 / calib_reps, g2, loss2)
+        t1_ns = a.elapsed_time(b) * 1e6 / calib_reps
+        if self.c0_ns == 0.0:
+            self.c0_ns = t1_ns / n_r                           # per-sample cost at the first n_r ("sample" spin)
+        self._graphs[n_r] = (g, xs, ys, loss, t1_ns, g2, loss2)
 
     def compute_graphed(self, x, y, n_r: int):
         """a4 through the captured graph; emulated slowdown σ_r (K4): a rank σ× slower takes σ× its own
@@ -401,21 +420,26 @@ class Worker:
         g, xs, ys, loss, t1_ns, g2, loss2 = self._graphs[n_r]
         xs.copy_(x[:n_r])
         ys.copy_(y[:n_r])
-        sigma = self.sigma()
+        ns = self._spin_ns(n_r, t1_ns)
         if g2 is not None:
             # N1: stamp, slowdown first (a slower GPU finishes every bucket later), then the step whose
             # backward overlaps the bucket allreduces; the graph stamps the end of compute before its join
             pr.stamp(self.stamps, stream=self.stream)
-            if sigma > 1.0:
-                pr.spin(int((sigma - 1.0) * t1_ns), stream=self.stream)
+            if ns > 0:
+                pr.spin(ns, stream=self.stream)
             g2.replay()
-            self.launches += 2 + len(self._buckets) + (sigma > 1.0)
+            self.launches += 2 + len(self._buckets) + (ns > 0)
             return loss2.clone()
         g.replay()
-        if sigma > 1.0:
-            pr.spin(int((sigma - 1.0) * t1_ns), stream=self.stream)
+        if ns > 0:
+            pr.spin(ns, stream=self.stream)
             self.launches += 1
         return loss.clone()
+
+    def t1(self, n_r: int) -> float:
+        """Measured σ = 1 step time t1(n_r) in seconds (captures the step first if needed)."""
+        self.prepare(n_r)
+        return self._graphs[n_r][4] / 1e9
 
     # ---- a6-a9: weighted ring allreduce + SGD (Algorithm 1 steps 5-6) ---------------------------------
     def allreduce_and_update(self, n_r: int, record=False):
@@ -576,6 +600,8 @@ class Worker:
         t_s (a5) is exchanged (K6) and the controller (a10) may change w before the next segment.  Step s
         always trains on the same B permuted positions whatever w is (DESIGN §3 #43)."""
         cfg = self.cfg
+        if cfg.adapt_lag:
+            return self._run_epoch_segments_async(record, loss_to_host)
         S = self.alloc.view()["S"]
         k = cfg.adapt_every
         losses, host_losses, segs = [], [], []
@@ -622,6 +648,85 @@ class Worker:
                 changed = self.alloc.update(ts)
             segs.append({"s0": s0, "steps": ns, "w": v["w"], "t_s": ts, "changed": changed})
             s0 += ns
+        self.epoch += 1
+        self.last_ts = t_epoch
+        rec = {"t_s": t_epoch, "loss": float(torch.stack(losses).mean()), "S": S,
+               "n_r": self.alloc.view()["n"][self.rank], "w": segs[0]["w"], "segments": segs}
+        self.history.append(rec)
+        return rec
+
+    def _run_epoch_segments_async(self, record=False, loss_to_host=False):
+        """N3 with the asynchronous exchange (adapt_lag = 1): per segment, t_s (a5) is summed on the device
+        from stamp pairs (data movement, then every step's compute) and all-gathered by the asynchronous K6
+        into pinned host memory; the host never waits for the segment it just enqueued — before enqueuing
+        segment j + 1 it reads segment j − 1's times (long finished) and runs the controller on them."""
+        cfg = self.cfg
+        if self._overlap:
+            raise ValueError("adapt_lag=1 with overlap is not supported (N1 owns the step stamps)")
+        S = self.alloc.view()["S"]
+        k = cfg.adapt_every
+        if not hasattr(self, "_segring"):
+            self._segring = torch.zeros(1 + 2 * (k + 1), dtype=torch.int64, device=self.dev)
+            self._d_ts = [torch.zeros((), dtype=torch.float64, device=self.dev) for _ in range(2)]
+            self._h_ts = [torch.zeros(self.P, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+            self._seg_pending, self._seg_count = [], 0
+        losses, host_losses, segs = [], [], []
+        t_epoch, s0 = 0.0, 0
+
+        def consume(block_until):
+            nonlocal t_epoch
+            while self._seg_pending and self._seg_pending[0]["seq"] <= block_until:
+                p = self._seg_pending.pop(0)
+                p["ev"].synchronize()                       # recorded a segment ago: already complete
+                ts = [float(x) for x in self._h_ts[p["slot"]]]
+                t_epoch += ts[self.rank]
+                changed = self.alloc.update(ts) if cfg.adaptive else False
+                p["seg"].update({"t_s": ts, "changed": changed})
+
+        while s0 < S:
+            consume(self._seg_count - 2)                    # segment j − 1's times decide segment j + 1
+            v = self.alloc.view()
+            n_r, ns = v["n"][self.rank], min(k, S - s0)
+            if cfg.graphs:
+                self.prepare(n_r)
+            ring = self._segring
+            ring[0].zero_()
+            pr.stamp(ring, stream=self.stream)              # a5: data movement of the segment ...
+            pr.shard_steps(self.alloc, self.rank, self.epoch, cfg.seed, s0, ns, self.idx, stream=self.stream)
+            xe, ye = self.gather(0, ns * n_r, record)
+            pr.stamp(ring, stream=self.stream)
+            self.launches += 3
+            for j in range(ns):
+                pr.stamp(ring, stream=self.stream)          # ... then each step's compute (+ K4 spin)
+                if n_r > 0:
+                    x, y = xe[j * n_r:(j + 1) * n_r], ye[j * n_r:(j + 1) * n_r]
+                    loss = self.compute_graphed(x, y, n_r) if cfg.graphs else self.compute(x, y, n_r)
+                else:
+                    loss = torch.zeros((), device=self.dev)
+                pr.stamp(ring, stream=self.stream)
+                self.launches += 2
+                self.allreduce_and_update(n_r, record)
+                self.gstep += 1
+                losses.append(loss)
+                if loss_to_host:
+                    self._loss_readback(loss, host_losses)
+            slot = self._seg_count % 2
+            pr.stamp_seconds(ring, self._d_ts[slot], stream=self.stream)
+            if self.comm is not None:
+                self.comm.allgather_f64_async(self._d_ts[slot], self._h_ts[slot], stream=self.stream)
+            else:
+                self._h_ts[slot][:1].copy_(self._d_ts[slot].reshape(1), non_blocking=True)
+            self.launches += 2
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            seg = {"s0": s0, "steps": ns, "w": v["w"]}
+            segs.append(seg)
+            self._seg_pending.append({"seq": self._seg_count, "slot": slot, "ev": ev, "seg": seg})
+            self._seg_count += 1
+            s0 += ns
+        consume(self._seg_count)                            # epoch end: apply what is left (one wait)
+        while loss_to_host and getattr(self, "_pending", None):
+            self._read_loss(host_losses)
         self.epoch += 1
         self.last_ts = t_epoch
         rec = {"t_s": t_epoch, "loss": float(torch.stack(losses).mean()), "S": S,

@@ -1,0 +1,50 @@
+"""CPU checks of experiments.py's host logic: the affine-cost min-max bound (the best integer allocation
+for step costs a + b·n under either K4 emulation) against brute force, and the affine fit."""
+
+import itertools
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import experiments as E  # noqa: E402
+
+
+def _brute(a, b, sigma, g, C, floor, spin, c0):
+    best = None
+    for w in itertools.product(range(floor, C + 1), repeat=len(sigma)):
+        if sum(w) != C:
+            continue
+        t = max(E.step_cost(g * x, s, a, b, spin, c0) for x, s in zip(w, sigma))
+        best = t if best is None else min(best, t)
+    return best
+
+
+def test_affine_minmax_is_the_integer_optimum():
+    rng = np.random.Generator(np.random.PCG64(5))
+    for _ in range(60):
+        P = int(rng.integers(2, 5))
+        C = int(rng.integers(P, 13))
+        sigma = [float(x) for x in rng.choice([1.0, 1.5, 2.0, 4.0], P)]
+        a, b = float(rng.uniform(0, 2e-3)), float(rng.uniform(1e-7, 5e-6))
+        spin = "t1" if rng.random() < 0.5 else "sample"
+        c0 = float(rng.uniform(1e-6, 2e-5))
+        T, w = E.affine_minmax(a, b, sigma, 16, C, 1, spin, c0)
+        assert sum(w) == C and min(w) >= 1
+        assert max(E.step_cost(16 * x, s, a, b, spin, c0) for x, s in zip(w, sigma)) <= T + 1e-15
+        assert abs(T - _brute(a, b, sigma, 16, C, 1, spin, c0)) <= 1e-15
+
+
+def test_affine_minmax_linear_costs_give_the_proportional_allocation():
+    # no fixed cost: the optimum is w ∝ v (Eq. 8), e.g. C4's speeds 1:1:1:1:2:2:4:4 -> [4,4,4,4,8,8,16,16]
+    T, w = E.affine_minmax(0.0, 1e-6, [4, 4, 4, 4, 2, 2, 1, 1], 16, 64)
+    assert w == [4, 4, 4, 4, 8, 8, 16, 16] and abs(T - 256e-6) < 1e-15
+
+
+def test_fit_affine():
+    a, b = E.fit_affine([64, 128, 256], [1.3e-3 + 1.5e-6 * n for n in (64, 128, 256)])
+    assert abs(a - 1.3e-3) < 1e-12 and abs(b - 1.5e-6) < 1e-15
+    assert E.fit_affine([100], [2.0]) == (2.0, 0.0)

@@ -172,7 +172,7 @@ def _n1_worker(rank, world, port, q):
         comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=4, watchdog_ns=60_000_000_000))
         cfg = RunConfig(N=4096, shape=(1024,), classes=10, model="mlp", num_classes=10, ratios=[1, 3], C=4, g=64,
                         lr=0.05, wd=1e-4, micro=96, bf16_compute=False, channels_last=False, fused_sgd=False,
-                        overlap=True, bucket_mb=0.25)
+                        overlap=True, bucket_mb=0.004)
         w = Worker(cfg, rank, world, 0, comm)
         v = w.alloc.view()
         n_r, S = v["n"][rank], 4
@@ -224,3 +224,62 @@ def test_n1_overlapped_buckets_match_oracle_elementwise():
             for lo, hi in r0["buckets"]:
                 emu = OW.ring_emulate(np.ascontiguousarray(g[:, lo:hi]), n, "f32")
                 assert np.array_equal(r0["red"][s][lo:hi], emu), (s, lo, hi)
+
+
+def _n3_async_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2111_08272_b200 as pr
+        from paper_2111_08272_b200.trainer import RunConfig, Worker
+
+        torch.cuda.set_device(0)
+        comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=2, watchdog_ns=60_000_000_000))
+        # K6 asynchronous: device value in, pinned host out, no synchronisation inside the call
+        d = torch.tensor(1.5 + rank, dtype=torch.float64, device="cuda")
+        h = torch.zeros(world, dtype=torch.float64, pin_memory=True)
+        comm.allgather_f64_async(d, h)
+        ev = torch.cuda.Event()
+        ev.record()
+        ev.synchronize()
+        ag_ok = h.tolist() == [1.5 + r for r in range(world)]
+        sync_ok = comm.allgather_f64(7.0 + rank) == [7.0 + r for r in range(world)]
+        # N3 with the asynchronous exchange: rank 0 emulated 3x slower; the replicated controller must move
+        # units to rank 1 and every rank must take the same decisions
+        cfg = RunConfig(N=4096, shape=(1024,), classes=10, model="mlp", num_classes=10, ratios=[1, 1], C=16, g=16,
+                        micro=256, bf16_compute=False, channels_last=False, adaptive=True, adapt_every=4,
+                        adapt_lag=1, slowdown=[3.0, 1.0], policy={"never_freeze": True})
+        w = Worker(cfg, rank, world, 0, comm)
+        recs = [w.run_epoch() for _ in range(2)]
+        torch.cuda.synchronize()
+        hist = [list(map(int, w.alloc.history(i))) for i in range(w.alloc.view()["hist_len"])]
+        segs = [(sg["w"], sg.get("t_s")) for r_ in recs for sg in r_["segments"]]
+        out = {"ag_ok": ag_ok, "sync_ok": sync_ok, "hist": hist, "segs": segs, "status": comm.status(),
+               "t_s": [r_["t_s"] for r_ in recs]}
+        del w
+        comm.destroy()
+        q.put((rank, out))
+    except Exception as e:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, repr(e) + traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_n3_asynchronous_exchange_two_processes():
+    """K6 without a host synchronisation (pr_stamp_seconds + pr_comm_allgather_f64_async) and N3's one-segment-
+    lag controller on it: both ranks see the same times, take the same decisions, and the slow rank sheds
+    units (VERDICT r1 "What's weak" #11)."""
+    res = _spawn(_n3_async_worker)
+    r0, r1 = res[0], res[1]
+    assert r0["ag_ok"] and r1["ag_ok"] and r0["sync_ok"] and r1["sync_ok"]
+    assert r0["status"] == 0 and r1["status"] == 0
+    assert r0["hist"] == r1["hist"] and r0["segs"] == r1["segs"]
+    assert len(r0["hist"]) > 3 and r0["hist"][0] == [8, 8]
+    last = r0["hist"][-1]
+    assert sum(last) == 16 and last[1] > last[0], r0["hist"]
+    for wv, ts in r0["segs"]:
+        assert ts is not None and len(ts) == 2 and min(ts) > 0
+    assert min(r0["t_s"]) > 0 and min(r1["t_s"]) > 0

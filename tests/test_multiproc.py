@@ -215,3 +215,65 @@ def test_overlapped_bucket_allreduce_two_processes():
     for p in ps:
         p.join(60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def _torchrun(args, env_extra, timeout=900):
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **env_extra)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", f"--master-port={_free_port()}"] + args
+    return subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=timeout)
+
+
+@pytest.mark.gpu
+def test_experiments_multiprocess_path_two_ranks(tmp_path):
+    """experiments.py's one-rank-per-process path — real barrier inside K3, measured t_w, the K6 t_s allgather,
+    the replicated controller — with 2 processes sharing the test GPU (PR_BENCH_SHARED_GPU=1: functional only,
+    the ranks time-share one GPU), plus the per-(epoch, rank) metrics CSV of SURVEY §5."""
+    import json
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    csv = tmp_path / "m.csv"
+    r = _torchrun(["experiments.py", "--scenario", "c2-5x", "--epochs", "3", "--N", "8192",
+                   "--metrics-csv", str(csv)], {"PR_BENCH_SHARED_GPU": "1"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    recs = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert [x["epoch"] for x in recs] == [0, 1, 2]
+    for x in recs:
+        assert len(x["t_s"]) == 2 and len(x["t_w"]) == 2 and min(x["t_w"]) == 0.0
+        assert x["T"] > 0 and x["bound"] > 0 and sum(x["w"]) == 12
+    rows = csv.read_text().splitlines()
+    assert rows[0] == "scenario,epoch,rank,w,n,len,t_s_ns,t_w_ns,t_c_ns,T_ns,loss" and len(rows) == 1 + 3 * 2
+    for ln in rows[1:]:
+        f = ln.split(",")
+        assert f[0] == "c2-5x" and int(f[3]) * 32 == int(f[4]) and int(f[6]) > 0
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_self_launch_shared_gpu():
+    """`PR_BENCH_SHARED_GPU=1 python bench.py --gpus 2` (no torchrun around it: bench.py re-launches itself)
+    prints one valid JSON line from rank 0 — the driver's N > 1 form, functional on a one-GPU box."""
+    import json
+    import subprocess
+    import sys
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PR_BENCH_SHARED_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-vgg",
+                        "--e2e-epochs", "1", "--data-n", "8192"], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["global_batch"] == 1024
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["allreduce"]["bound"] == "nvlink" and d["weak_scaling"]["config"]["global_batch"] == 2048
+    assert [row["bytes"] for row in d["allreduce_sweep"]][:2] == [64 << 20, 256 << 20]
