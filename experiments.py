@@ -29,6 +29,8 @@ SCENARIOS = {
     # name: (model, N, shape, P, ratios, C, g, sigma, adaptive)
     "c2": ("resnet18", 50_000, (3, 32, 32), 2, [1, 2], 3, 128, [2.0, 1.0], False),
     "c2-equal": ("resnet18", 50_000, (3, 32, 32), 2, [1, 1], 2, 192, [2.0, 1.0], False),
+    # C2's batch (B = 384) in units of g = 16, so the controller can place it (equal start, self-adaptive)
+    "c2-adapt": ("resnet18", 50_000, (3, 32, 32), 2, [1, 1], 24, 16, [2.0, 1.0], True),
     "c2-5x": ("resnet18", 50_000, (3, 32, 32), 2, [1, 1], 12, 32, [5.0, 1.0], True),
     "c3": ("vgg16", 51_200, (3, 224, 224), 4, [1, 1, 1, 1], 64, 16, [2.0, 2.0, 1.0, 1.0], True),
     "c4": ("resnet18", 50_000, (3, 32, 32), 8, [1] * 8, 64, 16, [4, 4, 4, 4, 2, 2, 1, 1], True),
@@ -63,39 +65,41 @@ SCHEDULES = {
 }
 
 
-def step_cost(n, sigma, a, b, spin, c0):
-    """Modelled step time (s) of a rank σ× slower that processes n rows, with the σ = 1 step affine in the
-    rows, t1(n) = a + b·n (fitted to the measured t1): "t1" emulation σ·t1(n); "sample" t1(n) + (σ−1)·c0·n."""
+def step_cost(t1, n, sigma, spin, c0):
+    """Step time (s) of a rank σ× slower that processes n rows, from its σ = 1 step time t1 = t1(n): "t1"
+    emulation σ·t1(n); "sample" emulation t1(n) + (σ−1)·c0·n (DESIGN.md §3 #46)."""
     if n <= 0:
         return 0.0
-    t1 = a + b * n
     return sigma * t1 if spin == "t1" else t1 + (sigma - 1.0) * c0 * n
 
 
-def affine_minmax(a, b, sigma, g, C, floor=1, spin="t1", c0=0.0):
-    """The best integer allocation for affine step costs: min over w (Σw = C, w_r >= floor, units of g rows)
-    of max_r step_cost(g·w_r).  Costs are increasing in w, so for a candidate T every rank takes the most
-    units that keep it <= T; the smallest candidate T (over all achievable per-rank step times) whose
-    greedy allocation reaches C is optimal.  Returns (T_step, w)."""
-    P = len(sigma)
-    cands = sorted({step_cost(g * w, sigma[r], a, b, spin, c0) for r in range(P) for w in range(floor, C + 1)})
-    for T in cands:
+def minmax_alloc(cost, P, C, floor=1):
+    """The best integer allocation for increasing per-rank step costs: min over w (Σw = C, w_r >= floor) of
+    max_r cost(r, w_r).  For a candidate T every rank takes the most units that keep it <= T; the smallest
+    candidate T (over all achievable per-rank step times) whose greedy allocation reaches C is optimal.
+    Returns (T_step, w)."""
+    table = [[cost(r, u) for u in range(floor, C + 1)] for r in range(P)]
+    for T in sorted({t for row in table for t in row}):
         w = []
         for r in range(P):
             k = floor - 1
-            for u in range(floor, C + 1):
-                if step_cost(g * u, sigma[r], a, b, spin, c0) <= T:
-                    k = u
+            for j, t in enumerate(table[r]):
+                if t <= T:
+                    k = floor + j
             w.append(k)
         if min(w) >= floor and sum(w) >= C:
             # trim the surplus one unit at a time from the currently costliest rank (any trim keeps max <= T;
-            # this one also minimises the remaining ranks' times lexicographically)
+            # this one also lowers the remaining ranks' times lexicographically)
             for _ in range(sum(w) - C):
-                r = max((i for i in range(P) if w[i] > floor),
-                        key=lambda i: (step_cost(g * w[i], sigma[i], a, b, spin, c0), -i))
+                r = max((i for i in range(P) if w[i] > floor), key=lambda i: (table[i][w[i] - floor], -i))
                 w[r] -= 1
             return T, w
     raise ValueError("no feasible allocation")
+
+
+def affine_minmax(a, b, sigma, g, C, floor=1, spin="t1", c0=0.0):
+    """minmax_alloc for the affine σ = 1 step cost t1(n) = a + b·n."""
+    return minmax_alloc(lambda r, u: step_cost(a + b * g * u, g * u, sigma[r], spin, c0), len(sigma), C, floor)
 
 
 def fit_affine(ns, ts):
@@ -232,28 +236,34 @@ def run_virtual(args):
             rec["w_segments"] = ws
         print(json.dumps(rec), flush=True)
         w.epoch += 1
-    # the affine-cost bound: t1(n) measured at (at least) two row counts, fitted a + b·n; the best integer
-    # allocation's step time under the same emulation (what any controller could reach), vs the linear
-    # Σspeed bound above (which assumes t_s ∝ samples, and is unattainable with a fixed step cost)
-    n_eq = w.alloc.view()["B"] // P
-    for nn in (max(1, n_eq // 2), n_eq, 2 * n_eq):
-        w.t1(nn)
-    pts = sorted((nn, ent[4] / 1e9) for nn, ent in w._graphs.items())
-    a0, b0 = fit_affine([p_[0] for p_ in pts], [p_[1] for p_ in pts])
+    # the measured-cost bound: t1(n) captured and timed at EVERY row count a rank can get (n = g·w, floor <= w
+    # <= C − (P−1)·floor); the best integer allocation under the same emulation (what any controller could
+    # reach) is the min-max of the measured per-rank step costs — vs the linear Σspeed bound above, which
+    # assumes t_s ∝ samples and is unattainable with a fixed per-step cost.  The affine fit
+    # t1(n) ≈ a + b·n of the same table is reported beside it.
     v = w.alloc.view()
-    t_step, w_opt = affine_minmax(a0, b0, sigma, g, C, cfg.floor, args.spin, w.c0_ns / 1e9)
+    wmax = C - (P - 1) * cfg.floor
+    t1tab = {u: w.t1(g * u) for u in range(cfg.floor, wmax + 1)}
+    pts = sorted((g * u, t) for u, t in t1tab.items())
+    a0, b0 = fit_affine([p_[0] for p_ in pts], [p_[1] for p_ in pts])
+    c0s = w.c0_ns / 1e9
+    t_step, w_opt = minmax_alloc(lambda r, u: step_cost(t1tab[u], g * u, sigma[r], args.spin, c0s) if u <= wmax
+                                 else float("inf"), P, C, cfg.floor)
     tc_mean = last_tc if last_tc is not None else 0.0
     S = v["S"]
     bound_aff = S * (t_step + tc_mean)
+    # the controller's own fixed point under the measured costs (the allocation it froze at), for context
+    w_fin = v["w"]
+    t_fin = max(step_cost(t1tab[u], g * u, sigma[r], args.spin, c0s) for r, u in enumerate(w_fin) if u > 0)
     print(json.dumps({"scenario": args.scenario, "mode": "virtual", "spin": args.spin, "adapt_every": k,
                       "static": args.static, "epochs": args.epochs, "T_total": totals["T"],
                       "bound_total": totals["bound"], "T_over_bound": totals["T"] / totals["bound"],
-                      "t1_points": pts, "affine_fit": {"a_s": a0, "b_s_per_row": b0}, "c0_s_per_row": w.c0_ns / 1e9,
-                      "affine_opt_w": w_opt, "affine_opt_step_s": t_step,
-                      "affine_bound_epoch_s": bound_aff, "last_epoch_T": last_T,
-                      "last_epoch_T_over_affine_bound": (last_T / bound_aff) if last_T else None,
+                      "t1_points": pts, "affine_fit": {"a_s": a0, "b_s_per_row": b0}, "c0_s_per_row": c0s,
+                      "opt_w": w_opt, "opt_step_s": t_step, "opt_bound_epoch_s": bound_aff,
+                      "final_w_model_step_s": t_fin, "last_epoch_T": last_T,
+                      "last_epoch_T_over_opt_bound": (last_T / bound_aff) if last_T else None,
                       "last_epoch_T_over_linear_bound": (last_T / last_bound) if last_T else None,
-                      "final_w": v["w"]}), flush=True)
+                      "final_w": w_fin}), flush=True)
     for c in comms:
         c.destroy()
 

@@ -283,6 +283,20 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 }
 // generic-proxy writes (peer stores observed through an acquire) -> visible to the async proxy (TMA)
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// this thread's st.shared writes -> visible to a later bulk store's (async proxy) reads of shared memory
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// TMA bulk store shared -> global (local or NVLink peer memory), bulk-group completion (SASS: UBLKCP)
+__device__ __forceinline__ void tma_store(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// all but the newest N bulk groups have finished READING shared memory (the source tiles may be reused)
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// all but the newest N bulk groups are COMPLETE (their global writes performed)
+template <int N> __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
 
 struct Shared {
     int err;
@@ -457,19 +471,32 @@ template <> __device__ __forceinline__ uint4 sgd_v4<__nv_bfloat16>(uint4, uint4 
 // inside the loop compiled to a branch + reconvergence per element (≈ 50 instructions per 16-byte vector
 // in the ncu source view of a CTA-bound run); with MODE constant it is ≈ 15 (2 LDS, 4 FFMA, 1-3 STG).
 // out1/out2/zg/thp are already offset to the tile's first element; out2, zg, thp may be null (uniform).
-template <typename T, int MODE, bool FUSE>
-__device__ __forceinline__ void tile_vectors(const uint4* __restrict__ gs, const uint4* __restrict__ is, int nv, int cid,
+// BULK: y goes back into the received tile in shared memory (`is`, same thread, same slot: read then
+// write) and the signal thread pushes the whole tile with one TMA bulk store per destination; a COPY
+// hop then has no per-vector work at all (the loaded tile IS the output).
+template <typename T, int MODE, bool FUSE, bool BULK>
+__device__ __forceinline__ void tile_vectors(const uint4* __restrict__ gs, uint4* is, int nv, int cid,
                                              int nc, float s, T* out1, T* out2, T* zg, const T* thp, float nlr,
                                              float wd) {
     constexpr int V = Vec<T>::V;
+    if constexpr (BULK && MODE == M_COPY && !FUSE) {
+        return;
+    } else {
+    if (BULK && MODE == M_COPY && !thp && !zg) return;
     for (int v = cid; v < nv; v += nc) {
         const uint4 a = (MODE == M_SCALE || MODE == M_FMA) ? gs[v] : make_uint4(0, 0, 0, 0);
         const uint4 b = (MODE == M_FMA || MODE == M_COPY) ? is[v] : make_uint4(0, 0, 0, 0);
         uint4 y = Vec<T>::op(MODE, s, a, b);
         if (FUSE && thp) y = sgd_v4<T>(*reinterpret_cast<const uint4*>(thp + (int64_t)v * V), y, nlr, wd);
         if (FUSE && zg) st_v4(zg + (int64_t)v * V, make_uint4(0, 0, 0, 0));
-        st_v4(out1 + (int64_t)v * V, y);
-        if (out2) st_v4(out2 + (int64_t)v * V, y);
+        if (BULK) {
+            is[v] = y;
+        } else {
+            st_v4(out1 + (int64_t)v * V, y);
+            if (out2) st_v4(out2 + (int64_t)v * V, y);
+        }
+    }
+    if (BULK) fence_proxy_async_smem();                   // the bulk store reads these smem writes
     }
 }
 
@@ -489,7 +516,7 @@ struct SliceArgs {
 // TMA bytes, compute + store the full 16-byte vectors (tile_vectors), the ragged tail (only at the end of
 // the buffer), then one arrive per warp on `stored`.  Pointers advance by a tile; no per-tile branching on
 // the mode, no 64-bit multiplies (these dominated a CTA-bound run once the element loop was tight).
-template <typename T, int MODE, bool FUSE>
+template <typename T, int MODE, bool FUSE, bool BULK>
 __device__ __forceinline__ void consume_slice(Shared& sh, uint8_t* smem, int kTileBytes, int kStages, int& stg, uint32_t& ph,
                                               int cid, int nc, int lane, const SliceArgs<T>& a) {
     constexpr int V = Vec<T>::V;
@@ -504,9 +531,9 @@ __device__ __forceinline__ void consume_slice(Shared& sh, uint8_t* smem, int kTi
         const bool ok = sh.tile_ok[stg] != 0;
         const int nv = (ne * (int)sizeof(T)) / 16;
         const uint4* gs = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes);
-        const uint4* is = reinterpret_cast<const uint4*>(smem + (size_t)stg * 2 * kTileBytes + kTileBytes);
+        uint4* is = reinterpret_cast<uint4*>(smem + (size_t)stg * 2 * kTileBytes + kTileBytes);
         if (ok) {
-            tile_vectors<T, MODE, FUSE>(gs, is, nv, cid, nc, a.s, o1, o2, zp, tp, a.nlr, a.wd);
+            tile_vectors<T, MODE, FUSE, BULK>(gs, is, nv, cid, nc, a.s, o1, o2, zp, tp, a.nlr, a.wd);
             if (nv * V < ne) {                                      // ragged tail: end of the buffer only
                 const int64_t e0 = a.len - left;
                 for (int e = nv * V + cid; e < ne; e += nc) {
@@ -542,7 +569,10 @@ __device__ __forceinline__ void consume_slice(Shared& sh, uint8_t* smem, int kTi
 }
 
 // FUSE (compile time): the K7-fused variant; the plain ring is compiled without any of its code.
-template <typename T, bool FUSE>
+// BULK (compile time, PR_COMM_FLAG_BULK_STORE): consumers write each tile's result back into shared memory
+// and the signal thread pushes it with TMA bulk stores (cp.async.bulk.global.shared::cta) instead of 16-byte
+// STGs from every consumer lane; a slice's ready flag is released once its bulk groups have completed.
+template <typename T, bool FUSE, bool BULK>
 __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ LaunchArgs A) {
     extern __shared__ __align__(128) uint8_t smem[];   // [stages][2][tile_bytes]: g tile, recv tile
     __shared__ Shared sh;
@@ -657,6 +687,15 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
         if (k == K_MID || k == K_LAST) return act ? M_FMA : M_COPY;
         return M_COPY;
     };
+    // where a hop's result goes: the next rank's staging slot, own buffer, and/or the next rank's buffer
+    auto dests = [&](int kind, int64_t lo, unsigned long long prodJ, T*& out1, T*& out2) {
+        T* nslot = reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ));
+        out2 = nullptr;
+        if (kind == K_FIRST || kind == K_MID) out1 = nslot;
+        else if (kind == K_LAST) { out1 = th + lo; out2 = direct ? nth + lo : nslot; }
+        else if (kind == K_AGMID) { if (direct) out1 = nth + lo; else { out1 = buf + lo; out2 = nslot; } }
+        else out1 = buf + lo;                                   // K_AGLAST (staged)
+    };
 
     if (threadIdx.x < 32) {
         // ================= producer: flags -> TMA bulk loads into the smem ring =======================
@@ -721,9 +760,67 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
         // ================= signal warp: per-slice release of ready flags, off the data path ===========
         // Waits until the consumers' stores of a slice's tiles are issued (stored barrier, release.cta by
         // every consumer warp), then one sys-scope release makes the whole slice visible to the peer.
-        if (threadIdx.x == 32) {
+        if (threadIdx.x == 32 && BULK) {
+            // BULK: the signal thread also moves the data.  Per tile: wait `stored` (the consumers' results
+            // are in the tile's smem, fenced for the async proxy), issue one bulk store per destination,
+            // commit; the stage is handed back to the producer once its bulk group has finished reading
+            // smem (one group of slack).  A slice's flag is released after all its groups COMPLETED.
             unsigned long long prodJ = st->slot_base, agP = st->ag_base, consJ = st->slot_base;
-            int stg = 0;
+            int stg = 0, prev_stg = -1;
+            uint32_t ph = 0;
+            for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
+                int64_t lo, len;
+                range(c, i, lo, len);
+                const int64_t nt = ntiles(kind, len);
+                const bool sends = sends_ag(kind) || writes_slot(kind);
+                T* out1;
+                T* out2;
+                dests(kind, lo, prodJ, out1, out2);
+                bool ok = true;
+                for (int64_t t = 0; t < nt; ++t) {
+                    mbar_wait(&sh.stored[stg], ph);
+                    ok = ok && sh.tile_ok[stg] != 0;
+                    const int64_t e0 = t * te;
+                    const int64_t ne = min(te, len - e0);
+                    const uint32_t vb = (uint32_t)((ne * (int64_t)sizeof(T)) & ~15ll);
+                    const uint8_t* src = smem + (size_t)stg * 2 * kTileBytes + kTileBytes;
+                    if (ok && vb) {
+                        tma_store(out1 + e0, src, vb);
+                        if (out2) tma_store(out2 + e0, src, vb);
+                    }
+                    bulk_commit();
+                    bulk_wait_read<1>();                    // the previous tile's stores have read their smem
+                    if (prev_stg >= 0) mbar_arrive(&sh.empty[prev_stg]);
+                    prev_stg = stg;
+                    if (++stg == kStages) {
+                        stg = 0;
+                        ph ^= 1u;
+                    }
+                    if (t == nt - 1) {
+                        bulk_wait<0>();                     // the slice's writes are performed ...
+                        fence_proxy_async_global();         // ... and ordered before the generic release
+                        if (sends && ok) {
+                            if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
+                            else st_release(&nxf->rs_ready, prodJ + 1, sys);
+                        }
+                        if (reads_slot(kind) && ok) st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);
+                    }
+                }
+                if (nt == 0 && !*(volatile int*)&sh.err) {   // empty slice: nothing to wait for
+                    if (sends) {
+                        if (sends_ag(kind)) st_release(&nxf->ag_ready, agP + 1, sys);
+                        else st_release(&nxf->rs_ready, prodJ + 1, sys);
+                    }
+                    if (reads_slot(kind)) st_relaxed_u64(&pvf->rs_credit, consJ + 1, sys);
+                }
+                if (sends_ag(kind)) ++agP;
+                else if (writes_slot(kind)) ++prodJ;
+                if (reads_slot(kind)) ++consJ;
+            });
+            bulk_wait<0>();
+            if (prev_stg >= 0) mbar_arrive(&sh.empty[prev_stg]);
+        } else if (threadIdx.x == 32) {
+            unsigned long long prodJ = st->slot_base, agP = st->ag_base, consJ = st->slot_base;            int stg = 0;
             uint32_t ph = 0;
             for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
                 int64_t lo, len;
@@ -776,12 +873,8 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
             const int64_t nt = ntiles(kind, len);
             const int mode = mode_of(kind);
             T* out1;
-            T* out2 = nullptr;
-            T* nslot = reinterpret_cast<T*>(slot_of(tab->win[next], tab, ch, prodJ));
-            if (kind == K_FIRST || kind == K_MID) out1 = nslot;
-            else if (kind == K_LAST) { out1 = th + lo; out2 = direct ? nth + lo : nslot; }
-            else if (kind == K_AGMID) { if (direct) out1 = nth + lo; else { out1 = buf + lo; out2 = nslot; } }
-            else out1 = buf + lo;                                   // K_AGLAST (staged)
+            T* out2;
+            dests(kind, lo, prodJ, out1, out2);
             const T* gsrc = buf + lo;
             const T* isrc = (kind == K_AGMID && direct) ? th + lo
                                                         : reinterpret_cast<const T*>(slot_of(my, tab, ch, consJ));
@@ -791,10 +884,10 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
                             A.nlr, A.wd};   // (slot credits are returned by the signal warp)
             // the hop's arithmetic is fixed per instantiation: one switch per slice, none per tile / element
             switch (mode) {
-                case M_SCALE: consume_slice<T, M_SCALE, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
-                case M_FMA: consume_slice<T, M_FMA, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
-                case M_COPY: consume_slice<T, M_COPY, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
-                default: consume_slice<T, M_ZERO, FUSE>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
+                case M_SCALE: consume_slice<T, M_SCALE, FUSE, BULK>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
+                case M_FMA: consume_slice<T, M_FMA, FUSE, BULK>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
+                case M_COPY: consume_slice<T, M_COPY, FUSE, BULK>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
+                default: consume_slice<T, M_ZERO, FUSE, BULK>(sh, smem, kTileBytes, kStages, stg, ph, cid, nc, lane, sa); break;
             }
             if (reads_slot(kind)) ++consJ;
             if (writes_slot(kind)) ++prodJ;
@@ -1416,7 +1509,7 @@ void resolve_config(pr_comm_config& c, bool cross_gpu) {
 }
 
 int check_config(const pr_comm_config& c) {
-    if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
+    if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE | PR_COMM_FLAG_BULK_STORE)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
         (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_ONESHOT ||
@@ -1582,13 +1675,16 @@ int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_conf
                              channels, threads, 0, s, coop);
         default: break;
     }
-    void* fn = a.fuse ? (void*)ring_kernel<float, true>
-                      : f32 ? (void*)ring_kernel<float, false> : (void*)ring_kernel<__nv_bfloat16, false>;
+    const bool bulk = (cfg.flags & PR_COMM_FLAG_BULK_STORE) != 0;
+    void* fn = bulk ? (a.fuse ? (void*)ring_kernel<float, true, true>
+                              : f32 ? (void*)ring_kernel<float, false, true> : (void*)ring_kernel<__nv_bfloat16, false, true>)
+                    : (a.fuse ? (void*)ring_kernel<float, true, false>
+                              : f32 ? (void*)ring_kernel<float, false, false> : (void*)ring_kernel<__nv_bfloat16, false, false>);
     const size_t smem = (size_t)cfg.stages * 2 * cfg.tile_bytes;
     // the dynamic-smem opt-in is a per-device function attribute: cached per (device, instantiation)
     static std::mutex mu;
-    static size_t attr_set[PR_MAX_DEVICES][3];
-    const int di = a.fuse ? 2 : (f32 ? 0 : 1);
+    static size_t attr_set[PR_MAX_DEVICES][6];
+    const int di = (a.fuse ? 2 : (f32 ? 0 : 1)) + (bulk ? 3 : 0);
     if (device < 0 || device >= PR_MAX_DEVICES) return PR_ERR_INVALID;
     {
         std::lock_guard<std::mutex> lk(mu);

@@ -13,12 +13,16 @@ sys.path.insert(0, ROOT)
 import experiments as E  # noqa: E402
 
 
+def _cost(a, b, g, x, s, spin, c0):
+    return E.step_cost(a + b * g * x, g * x, s, spin, c0)
+
+
 def _brute(a, b, sigma, g, C, floor, spin, c0):
     best = None
     for w in itertools.product(range(floor, C + 1), repeat=len(sigma)):
         if sum(w) != C:
             continue
-        t = max(E.step_cost(g * x, s, a, b, spin, c0) for x, s in zip(w, sigma))
+        t = max(_cost(a, b, g, x, s, spin, c0) for x, s in zip(w, sigma))
         best = t if best is None else min(best, t)
     return best
 
@@ -34,7 +38,7 @@ def test_affine_minmax_is_the_integer_optimum():
         c0 = float(rng.uniform(1e-6, 2e-5))
         T, w = E.affine_minmax(a, b, sigma, 16, C, 1, spin, c0)
         assert sum(w) == C and min(w) >= 1
-        assert max(E.step_cost(16 * x, s, a, b, spin, c0) for x, s in zip(w, sigma)) <= T + 1e-15
+        assert max(_cost(a, b, 16, x, s, spin, c0) for x, s in zip(w, sigma)) <= T + 1e-15
         assert abs(T - _brute(a, b, sigma, 16, C, 1, spin, c0)) <= 1e-15
 
 
@@ -42,6 +46,16 @@ def test_affine_minmax_linear_costs_give_the_proportional_allocation():
     # no fixed cost: the optimum is w ∝ v (Eq. 8), e.g. C4's speeds 1:1:1:1:2:2:4:4 -> [4,4,4,4,8,8,16,16]
     T, w = E.affine_minmax(0.0, 1e-6, [4, 4, 4, 4, 2, 2, 1, 1], 16, 64)
     assert w == [4, 4, 4, 4, 8, 8, 16, 16] and abs(T - 256e-6) < 1e-15
+
+
+def test_minmax_alloc_on_a_measured_table():
+    """A non-affine cost table (a step at a microbatch boundary): the greedy min-max is still the optimum."""
+    tab = {u: 1e-3 + 2e-6 * 16 * u + (0.8e-3 if u > 8 else 0.0) for u in range(1, 17)}
+    sigma = [3.0, 1.0, 1.0]
+    T, w = E.minmax_alloc(lambda r, u: sigma[r] * tab[u], 3, 16)
+    best = min(max(sigma[r] * tab[x] for r, x in enumerate(ws))
+               for ws in itertools.product(range(1, 15), repeat=3) if sum(ws) == 16)
+    assert sum(w) == 16 and abs(T - best) < 1e-15
 
 
 def test_fit_affine():

@@ -620,3 +620,74 @@ def test_auto_with_unregistered_or_staged_buffers_skips_two_shot():
     for L in (300_001, 1 << 20):
         _check(P, L, "f32", [1, 2, 3, 4], comms, seed=L)
     assert all(c.status() == 0 for c in comms)
+
+
+# ---- the TMA bulk-store data path (PR_COMM_FLAG_BULK_STORE) ------------------------------------------------
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_bulk_store_ring_bit_identical_to_ring_replay(P, dtype):
+    """Results written back to shared memory and pushed by one thread with cp.async.bulk stores: the same
+    bits as the ring replay (direct and staged all-gather, .gpu and .sys scope, ragged tails)."""
+    for cfg in (dict(bulk_store=True), dict(bulk_store=True, force_staged=True),
+                dict(bulk_store=True, sys_scope=True, channels=4, slot_bytes=4096, tile_bytes=1024, stages=3)):
+        comms = group(P, **cfg)
+        rng = np.random.Generator(np.random.PCG64(77 + P))
+        for L in (1, 7, P + 1, 1000, 4099, 65_537, 2 ** 20 + 3):
+            n = [int(x) * 16 for x in rng.integers(0, 5, P)]
+            if sum(n) == 0:
+                n[0] = 16
+            _check(P, L, dtype, n, comms, kind="mixed" if L % 2 else "gaussian", seed=L + P)
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_bulk_store_fused_and_full_sizes(P):
+    comms = group(P, bulk_store=True)
+    for L in (7, 4099, 300_001):
+        _fused_case(P, L, [1 + (r % 3) for r in range(P)], comms, seed=L + 31)
+    _check(P, 11_689_512, "f32", SKEW[-P:], comms, seed=5)
+    comms = group(P, **(dict(CROSS8) if P == 8 else dict(CROSS)), bulk_store=True)
+    _check_sampled(P, 11_689_512, SKEW[-P:], comms, seed=P + 11)
+    _fused_case(P, 11_689_512, SKEW[-P:], comms, seed=P + 13)
+
+
+def test_bulk_store_randomized_configs_and_graph_replay():
+    rng = np.random.Generator(np.random.PCG64(4242))
+    for case in range(30):
+        P = int(rng.choice([2, 3, 4, 5, 8]))
+        cfg = dict(channels=int(rng.integers(1, 9)), slots=int(rng.choice([2, 4, 8])),
+                   slot_bytes=int(rng.choice([256, 4096, 65536, 262144])), stages=int(rng.integers(2, 7)),
+                   tile_bytes=int(rng.choice([256, 1024, 4096, 16384])), threads=int(rng.choice([64, 256, 512])),
+                   sys_scope=bool(rng.integers(0, 2)), force_staged=bool(rng.integers(0, 2)), bulk_store=True)
+        comms = pr.comm_init_local(P, 0, pr.comm_config(watchdog_ns=5_000_000_000, **cfg))
+        try:
+            for _ in range(2):
+                L = int(rng.choice([1, 3, 17, 1000, 4097, 65_537, 300_001]))
+                n = [int(x) for x in rng.integers(0, 5, P)]
+                if sum(n) == 0:
+                    n[0] = 1
+                _check(P, L, "f32" if rng.integers(0, 2) else "bf16", n, comms, seed=case * 11 + L)
+            if not cfg["force_staged"]:
+                _fused_case(P, int(rng.choice([7, 5000, 200_003])), [1 + (r % 3) for r in range(P)], comms,
+                            seed=case + 700)
+        finally:
+            for c in comms:
+                c.destroy()
+    # graph replay: counters carried on the device across replays
+    P, L = 4, 100_003
+    comms = group(P, bulk_store=True)
+    host, dev = _inputs(P, L, "f32", seed=3)
+    n = [3, 1, 2, 5]
+    emu = W.ring_emulate(host, n, "f32")
+    s = torch.cuda.Stream()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        pr.weighted_allreduce_local(comms, dev, n, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gr, stream=s):
+            pr.weighted_allreduce_local(comms, dev, n, stream=s)
+    for _ in range(3):
+        for r in range(P):
+            dev[r].copy_(torch.from_numpy(host[r]))
+        gr.replay()
+        torch.cuda.synchronize()
+        assert all(np.array_equal(d.cpu().numpy(), emu) for d in dev)

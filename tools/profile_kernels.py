@@ -114,6 +114,10 @@ if __name__ == "__main__":
         gather(49152, 3072, 50000, reps, 1024, impls=(1,), layout=1, seq=True)
     if what in ("gather_imagenet", "all"):
         gather(336, 150528, 2000, reps, 50176)
+    if what == "gather_imagenet_hwc":                  # the C3 step launch, channels-last, LSU vs TMA
+        gather(336, 150528, 2000, reps, 50176, impls=(1, 2), layout=1)
+    if what == "gather_imagenet_epoch_hwc":            # a VGG-16 epoch-size launch (16,384 distinct rows, 7.4 GB)
+        gather(16384, 150528, 16384, reps, 50176, impls=(1, 2), layout=1)
     if what in ("shard", "all"):
         shard(reps)
     if what in ("sgd", "all"):

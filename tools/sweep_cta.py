@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--channels", type=int, default=16)
     ap.add_argument("--P", type=int, default=2)
     ap.add_argument("--quick", action="store_true", help="four reference configurations only")
+    ap.add_argument("--bulk", action="store_true", help="TMA bulk-store data path (PR_COMM_FLAG_BULK_STORE)")
+    ap.add_argument("--cfg", default="", help="one configuration as JSON (overrides the grid)")
     a = ap.parse_args()
     P, L = a.P, (a.mib << 20) // 4
     store = [torch.randn(L, device="cuda") for _ in range(P)]
@@ -38,11 +40,14 @@ def main():
                 dict(stages=3, tile_bytes=32768, slot_bytes=1048576, threads=512, slots=8),
                 dict(stages=6, tile_bytes=16384, slot_bytes=1048576, threads=512, slots=8),
                 dict(stages=12, tile_bytes=8192, slot_bytes=1048576, threads=512, slots=8)]
+    if a.cfg:
+        cfgs = [json.loads(a.cfg)]
     for cfg in cfgs:
         if cfg["stages"] * 2 * cfg["tile_bytes"] > 200 * 1024 or cfg["stages"] * cfg["tile_bytes"] < 32768:
             continue
         try:
-            comms = pr.comm_init_local(P, 0, pr.comm_config(channels=a.channels, sys_scope=a.sys, **cfg))
+            comms = pr.comm_init_local(P, 0, pr.comm_config(channels=a.channels, sys_scope=a.sys, bulk_store=a.bulk,
+                                                            **cfg))
         except pr.PropringError as e:
             print(json.dumps({**cfg, "err": str(e)[:80]}), flush=True)
             continue
@@ -57,7 +62,8 @@ def main():
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) / 3 * 1e3
         bus = L * 4 * 2 * (P - 1) / P / (us * 1e-6) / 1e9
-        print(json.dumps({**cfg, "channels": a.channels, "sys": a.sys, "us": round(us, 1), "busbw_equiv_GBs": round(bus),
+        print(json.dumps({**cfg, "channels": a.channels, "sys": a.sys, "bulk": a.bulk, "us": round(us, 1),
+                          "busbw_equiv_GBs": round(bus),
                           "per_channel_GBs": round(bus / a.channels, 1)}), flush=True)
         for c in comms:
             c.destroy()
