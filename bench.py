@@ -496,6 +496,24 @@ def allreduce_sweep(ctx, reps=20):
         if not ctx["shared"]:
             row.update(_nccl_pair(buf, s, world, tdev, reps))
         res.append(row)
+    # N2's NVLS variant (in-switch reduction through an NVSwitch multicast object) where the platform has one
+    nv_comm = pr.comm_init(rank, world, ctx["local"], config=pr.comm_config(algo=pr.ALGO_NVLS))
+    try:
+        nv = nv_comm.nvls_alloc(zmax)
+        for row in res:
+            if row["dtype"] != "float32":
+                continue
+            Z = row["bytes"]
+            buf = nv[:Z].view(torch.float32)
+            g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+            buf.copy_(torch.randn(buf.numel(), device="cuda", generator=g))
+            row["propring_NVLS"] = _timed_collective(lambda: pr.weighted_allreduce(nv_comm, buf, n[rank]), buf, world,
+                                                     tdev, reps)
+    except pr.PropringError as e:
+        for row in res:
+            row["propring_NVLS"] = {"unavailable": str(e)[:160]}
+    finally:
+        nv_comm.destroy()
     return res
 
 

@@ -44,6 +44,7 @@ extern "C" {
 #define PR_ERR_PEER_TIMEOUT      -10   /* watchdog expired waiting for a peer (TransportClosed) */
 #define PR_ERR_CAPACITY          -11   /* output capacity too small                                  */
 #define PR_ERR_INTERNAL          -12   /* invariant violated inside the library (a bug)              */
+#define PR_ERR_UNSUPPORTED       -13   /* the platform lacks a capability (NVSwitch multicast for NVLS) */
 
 const char *pr_strerror(int code);
 int pr_version(void);
@@ -254,6 +255,11 @@ typedef struct {
  * per-hop rounding (same bits).  (P−1)·2·Z bytes sent per rank: for buffers <= os_max_bytes (larger
  * buffers given PR_ALGO_ONESHOT take the ring).  Works with unregistered buffers. */
 #define PR_ALGO_ONESHOT  4
+#define PR_ALGO_NVLS     5   /* NVSwitch in-switch reduction: fp32 buffers inside the NVLS
+                              * region (pr_comm_nvls_alloc); each rank weights its buffer in place, then
+                              * reduces its chunk with multimem.ld_reduce and multicasts it with multimem.st.
+                              * The switch's summation order is unspecified: within tolerance of the fp64
+                              * mean, NOT the ring's bits.  Buffers outside the region take the ring. */
 
 /* Byte allgather supplied by the caller (e.g. over a torch process group): every rank passes `len`
  * bytes in `send` and receives the P·len bytes of all ranks, rank-ordered, in `recv`.  Returns 0 on
@@ -334,6 +340,16 @@ int pr_comm_allgather_f64(pr_comm *c, double local, double *out, void *stream);
  * (local group, null pointer, h_out not device-accessible), PR_ERR_CUDA; peer timeouts latch in
  * pr_comm_status. */
 int pr_comm_allgather_f64_async(pr_comm *c, const double *d_local, double *h_out, void *stream);
+
+/* NVLS region (collective, every rank with the same bytes): allocates `bytes` (rounded up
+ * to the multicast granularity) on every rank's device, binds all of them to ONE NVSwitch multicast
+ * object and maps both aliases; *d_ptr = this rank's unicast address (zeroed).  A weighted allreduce with
+ * config.algo = PR_ALGO_NVLS on an fp32 buffer inside it reduces in the switch.  At most one region per
+ * communicator; freed by pr_comm_destroy.  The multicast handle travels as a fabric handle when the
+ * platform has one, else as a file descriptor duplicated with pidfd_getfd.
+ * Errors (on every rank together): PR_ERR_UNSUPPORTED (no multicast: a single-GPU or non-NVSwitch
+ * system, a container without the fabric), PR_ERR_INVALID (local group, P < 2, a region exists). */
+int pr_comm_nvls_alloc(pr_comm *c, size_t bytes, void **d_ptr);
 
 /* Latched device error of the last completed call (PR_OK if none). Non-blocking host read. */
 int pr_comm_status(pr_comm *c);

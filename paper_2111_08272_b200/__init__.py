@@ -34,6 +34,7 @@ PR_ERR_ZERO_SAMPLES = -9
 PR_ERR_PEER_TIMEOUT = -10
 PR_ERR_CAPACITY = -11
 PR_ERR_INTERNAL = -12
+PR_ERR_UNSUPPORTED = -13
 
 GATHER_COPY = 0
 GATHER_U8_TO_F32_AFFINE = 1
@@ -254,6 +255,7 @@ ALGO_TWO_SHOT = 1
 ALGO_AUTO = 2
 ALGO_LL = 3
 ALGO_ONESHOT = 4
+ALGO_NVLS = 5
 
 
 def comm_config(channels=0, slots=8, threads=512, slot_bytes=0, watchdog_ns=10_000_000_000,
@@ -307,6 +309,18 @@ class Comm:
         import torch
         p = ctypes.c_void_p()
         _check(LIB.pr_comm_alloc(self._h, nbytes, ctypes.byref(p)), "pr_comm_alloc")
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        t = torch.as_tensor(_DeviceBuffer(p.value, nbytes, dev), device=dev)
+        self._owned.append(t)
+        return t.view(dtype) if dtype is not None else t
+
+    def nvls_alloc(self, nbytes: int, dtype=None, device=None):
+        """NVLS region (collective): this rank's unicast view of memory bound to one NVSwitch multicast object
+        across all ranks, as a torch tensor.  Raises PropringError(PR_ERR_UNSUPPORTED) where the platform has
+        no multicast (every rank together)."""
+        import torch
+        p = ctypes.c_void_p()
+        _check(LIB.pr_comm_nvls_alloc(self._h, nbytes, ctypes.byref(p)), "pr_comm_nvls_alloc")
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         t = torch.as_tensor(_DeviceBuffer(p.value, nbytes, dev), device=dev)
         self._owned.append(t)

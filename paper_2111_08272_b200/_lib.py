@@ -79,6 +79,7 @@ SIGNATURES = {
                                                        c_i64, ctypes.POINTER(c_i64), c_dbl, c_dbl, c_i32, c_vp]),
     "pr_comm_allgather_f64": (ctypes.c_int, [c_vp, c_dbl, ctypes.POINTER(c_dbl), c_vp]),
     "pr_comm_allgather_f64_async": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "pr_comm_nvls_alloc": (ctypes.c_int, [c_vp, ctypes.c_size_t, ctypes.POINTER(c_vp)]),
     "pr_comm_status": (ctypes.c_int, [c_vp]),
     "pr_comm_timestamps": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i64)]),
     "pr_comm_rank": (ctypes.c_int, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),

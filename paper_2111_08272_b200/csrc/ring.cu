@@ -26,7 +26,10 @@
 // oneshot_ll_kernel (one hop, tiny buffers), twoshot_kernel (2 phases), and ring_kernel<float, true>
 // (K7's SGD fused into the last reduce-scatter hop; the all-gather carries θ').  Channel count, tile and
 // slot sizes default from the topology (resolve_config): CTAs per rank are the bound across GPUs.
+#include <cuda.h>            // driver-API types only: entry points are fetched with cudaGetDriverEntryPoint
 #include <cuda_bf16.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstring>
@@ -67,6 +70,10 @@ struct AgEntry {
     unsigned long long seq;
     double v;
 };
+struct NvFlags {            // NVLS: by q, the call sequence whose phase A (scale) / B (reduce + multicast) it finished
+    unsigned long long a[PR_MAX_RANKS];
+    unsigned long long b[PR_MAX_RANKS];
+};
 static_assert(sizeof(ChanFlags) == 384, "flags");
 static_assert(sizeof(HsEntry) == 128, "hs");
 static_assert(sizeof(ChanState) == 128, "state");
@@ -86,6 +93,10 @@ struct DevTable {
     int64_t min_slice_bytes;        // > 0: cut each chunk share into up to slots/2 slices of >= this (ring)
     uint64_t off_os;                // one-shot LL: [channels][P sources][os_region_bytes]
     int64_t os_region_bytes;        // LL lines for one channel's share of the whole buffer
+    uint64_t off_nv;                // NVLS barrier counters: [channels] NvFlags
+    uint8_t* nv_uc;                 // NVLS region: this rank's unicast mapping (null: none) ...
+    uint8_t* nv_mc;                 // ... and the multicast mapping of the same offsets (all ranks' memory)
+    int64_t nv_bytes;
     volatile int* status;           // host-mapped
     volatile long long* stamps;     // host-mapped [3]
     uint8_t* win[PR_MAX_RANKS];
@@ -135,6 +146,8 @@ void layout(DevTable& t) {
     o += (uint64_t)t.channels * (uint64_t)(t.P > 1 ? 2 * t.P - 2 : 0) * (uint64_t)t.ll_region_bytes;
     t.off_os = o = align_up(o, 4096);
     o += (uint64_t)t.channels * (uint64_t)t.P * (uint64_t)t.os_region_bytes;
+    t.off_nv = o = align_up(o, 4096);
+    o += (uint64_t)t.channels * sizeof(NvFlags);
     t.window_bytes = align_up(o, 4096);
 }
 
@@ -1403,6 +1416,147 @@ __global__ void __launch_bounds__(512, 1) oneshot_ll_kernel(const __grid_constan
     if (t0 && ch == 0) tab->stamps[2] = (long long)gtimer();
 }
 
+// =====================================================================================================
+// NVLS: the reduction done inside the NVSwitch.  The gradient buffer lives in an NVLS
+// region (pr_comm_nvls_alloc: every rank's memory bound to one multicast object), so one
+// multimem.ld_reduce through the multicast address returns Σ_q x_q[j] summed by the switch, and one
+// multimem.st writes the result into every rank's memory.  The switch adds raw values, so the weights are
+// applied first (phase A: x_r ← s_r·g_r in place, or 0 when n_r = 0 — a zero rank contributes exactly
+// zero, never 0·g, DESIGN.md §3 #33); then (phase B) rank r reduces chunk r's channel share and
+// multicasts it.  Per-channel barriers between the phases go through the windows' NvFlags (release /
+// acquire at .sys scope), with fence.proxy.alias around them: phase A writes through the unicast alias,
+// phase B reads and writes the same bytes through the multicast alias.  Reduction order inside the switch
+// is unspecified: the result is checked against the fp64 weighted mean within tolerance, not bit for bit
+// (DESIGN.md §3 #48).  fp32 only.
+// =====================================================================================================
+__device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+__device__ __forceinline__ float4 mm_ld_reduce_v4(const float* mc) {
+    float4 r;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(mc)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ void mm_st_v4(float* mc, float4 v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ float mm_ld_reduce_f32(const float* mc) {
+    float r;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r) : "l"(mc) : "memory");
+    return r;
+}
+__device__ __forceinline__ void mm_st_f32(float* mc, float v) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
+}
+__device__ __forceinline__ NvFlags* nv_of(uint8_t* w, const DevTable* t, int ch) {
+    return reinterpret_cast<NvFlags*>(w + t->off_nv) + ch;
+}
+
+__global__ void __launch_bounds__(512, 1) nvls_kernel(const __grid_constant__ LaunchArgs A) {
+    __shared__ int s_err;
+    __shared__ long long s_sumn;
+    __shared__ unsigned long long s_seq;
+    const RankCall& rc = A.calls[blockIdx.y];
+    const DevTable* tab = rc.tab;
+    const int ch = blockIdx.x;
+    const int r = tab->rank, P = tab->P;
+    uint8_t* my = tab->win[r];
+    ChanState* st = state_of(my, tab, ch);
+    const bool t0 = threadIdx.x == 0;
+    unsigned long long deadline = ~0ull;
+    if (threadIdx.x < 32) {                           // warp 0: the handshake = the barrier
+        const unsigned long long start = gtimer();
+        if (t0 && ch == 0) tab->stamps[0] = (long long)start;
+        if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
+        const HsOut hs = handshake(A, rc, tab, st, ch, tab->sysscope != 0, deadline, nullptr, nullptr);
+        if (t0) {
+            s_err = hs.err;
+            s_sumn = hs.sumn;
+            s_seq = st->seq;
+            if (ch == 0) tab->stamps[1] = (long long)gtimer();
+        }
+    }
+    __syncthreads();
+    if (s_err) {
+        if (t0) latch(tab, s_err);
+        return;
+    }
+    if (tab->watchdog_ns > 0) deadline = gtimer() + (unsigned long long)tab->watchdog_ns;
+    const unsigned long long seq = s_seq;
+    const int64_t count = A.count;
+    const int64_t per = (count + P - 1) / P;
+    const int64_t cs = (per + 3) / 4 * 4;                             // chunk (as the ring, 16 bytes)
+    const int64_t subp = (cs + tab->channels - 1) / tab->channels;
+    const int64_t sub = (subp + 3) / 4 * 4;
+    const float s = (float)((double)rc.n_local / (double)s_sumn);    // n_r/Σn: fp64 division, fp32 weight
+    const bool act = rc.n_local > 0;
+    float* buf = reinterpret_cast<float*>(rc.buf);
+    float* mcb = reinterpret_cast<float*>(tab->nv_mc + (reinterpret_cast<uint8_t*>(rc.buf) - tab->nv_uc));
+    auto range = [&](int c, int64_t& lo, int64_t& len) {
+        const int64_t clo = (int64_t)c * cs;
+        const int64_t chi = min(clo + cs, count);
+        lo = clo + (int64_t)ch * sub;
+        const int64_t hi = min(clo + min((int64_t)(ch + 1) * sub, cs), chi);
+        len = hi > lo ? hi - lo : 0;
+    };
+    auto barrier = [&](bool phase_b) -> bool {       // channel ch of every rank reached this point of call seq
+        fence_proxy_alias();
+        __threadfence_system();
+        __syncthreads();
+        bool ok = true;
+        if (threadIdx.x < 32) {
+            for (int q = (int)threadIdx.x; q < P; q += 32) {
+                NvFlags* f = nv_of(tab->win[q], tab, ch);
+                st_release(phase_b ? &f->b[r] : &f->a[r], seq, true);
+            }
+            NvFlags* mf = nv_of(my, tab, ch);
+            for (int q = (int)threadIdx.x; q < P; q += 32)
+                ok = ok && wait_ge(phase_b ? &mf->b[q] : &mf->a[q], seq, deadline, true);
+            ok = __all_sync(0xffffffffu, ok);
+            if (!ok && t0) latch(tab, PR_ERR_PEER_TIMEOUT);
+            if (t0) s_err = ok ? 0 : PR_ERR_PEER_TIMEOUT;
+        }
+        __syncthreads();
+        fence_proxy_alias();
+        return s_err == 0;
+    };
+    // phase A: this channel's share of every chunk of the own buffer, weighted in place (unicast alias)
+    for (int c = 0; c < P; ++c) {
+        int64_t lo, len;
+        range(c, lo, len);
+        const int64_t nv = len / 4;
+        float4* v4 = reinterpret_cast<float4*>(buf + lo);
+        for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+            float4 x = v4[v];
+            x = act ? make_float4(__fmul_rn(s, x.x), __fmul_rn(s, x.y), __fmul_rn(s, x.z), __fmul_rn(s, x.w))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+            v4[v] = x;
+        }
+        for (int64_t e = nv * 4 + threadIdx.x; e < len; e += blockDim.x) buf[lo + e] = act ? __fmul_rn(s, buf[lo + e]) : 0.f;
+    }
+    if (!barrier(false)) return;
+    // phase B: chunk r's share: switch-reduced sum -> multicast into every rank's buffer
+    {
+        int64_t lo, len;
+        range(r, lo, len);
+        const int64_t nv = len / 4;
+        for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+            float* p = mcb + lo + 4 * v;
+            mm_st_v4(p, mm_ld_reduce_v4(p));
+        }
+        for (int64_t e = nv * 4 + threadIdx.x; e < len; e += blockDim.x) {
+            float* p = mcb + lo + e;
+            mm_st_f32(p, mm_ld_reduce_f32(p));
+        }
+    }
+    barrier(true);                                    // every rank's multicast stores into my memory landed
+    __syncthreads();
+    if (t0 && ch == 0) tab->stamps[2] = (long long)gtimer();
+}
+
 __global__ void allgather_f64_kernel(const DevTable* tab, unsigned long long seq, double v, const double* vp,
                                      double* out) {
     if (threadIdx.x != 0) return;
@@ -1470,6 +1624,10 @@ struct pr_comm {
     pr_exchange_fn fn = nullptr;
     void* ctx = nullptr;
     unsigned long long ag_seq = 0;
+    // NVLS region (pr_comm_nvls_alloc): multicast object, this rank's physical memory, the two mappings
+    unsigned long long nv_mc_handle = 0, nv_mem_handle = 0;
+    uintptr_t nv_uc = 0, nv_mc = 0;
+    size_t nv_size = 0;
 };
 
 namespace {
@@ -1512,7 +1670,7 @@ int check_config(const pr_comm_config& c) {
     if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE | PR_COMM_FLAG_BULK_STORE)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
-        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_ONESHOT ||
+        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_NVLS ||
         c.ll_max_bytes < 0 || c.ll_max_bytes > (64ll << 20) || c.os_max_bytes < 0 || c.os_max_bytes > (16ll << 20) ||
         c.min_slice_bytes < 0 || c.min_slice_bytes % 16 ||
         c.ts_slots < 2 || c.ts_slots > 16 || c.ts_slot_bytes < 256 || c.ts_slot_bytes % 256 ||
@@ -1580,9 +1738,12 @@ int exchange(pr_comm* c, const void* send, size_t len, void* recv) {
     return c->fn(c->ctx, send, len, recv) == 0 ? PR_OK : PR_ERR_INVALID;
 }
 
+void nvls_release(pr_comm* c);
+
 void free_comm(pr_comm* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    nvls_release(c);
     for (auto& rg : c->regs) {
         for (int q = 0; q < (int)rg.peer.size(); ++q)
             if (!c->local && q != c->rank && rg.peer[q]) cudaIpcCloseMemHandle(rg.peer[q]);
@@ -1630,8 +1791,10 @@ size_t dtype_size(int32_t dt) { return dt == PR_DTYPE_F32 ? 4 : (dt == PR_DTYPE_
 // under FORCE_STAGED); an explicit PR_ALGO_TWO_SHOT on an unregistered buffer latches PR_ERR_INVALID.
 // `registered` is per rank: a job whose ranks differ there picks different kernels, and the handshake
 // (which carries the algorithm) turns that into PR_ERR_LENGTH_MISMATCH on every rank.
-int pick_algo(const pr_comm_config& cfg, int64_t count, int32_t dtype, int P, bool registered) {
+int pick_algo(const pr_comm_config& cfg, int64_t count, int32_t dtype, int P, bool registered, bool in_nvls = false) {
     const int64_t bytes = count * (dtype == PR_DTYPE_F32 ? 4 : 2);
+    // NVLS only when asked for, on an fp32 buffer inside the communicator's NVLS region; otherwise the ring
+    if (cfg.algo == PR_ALGO_NVLS) return (in_nvls && dtype == PR_DTYPE_F32 && P > 1) ? PR_ALGO_NVLS : PR_ALGO_RING;
     const int64_t ts_max = cfg.ts_max_bytes * (P >= 8 ? 4 : (P >= 4 ? 2 : 1));
     const bool direct_ok = registered && !(cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
     if ((cfg.algo == PR_ALGO_ONESHOT || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.os_max_bytes) return PR_ALGO_ONESHOT;
@@ -1655,15 +1818,18 @@ int launch_k3(void* fn, const LaunchArgs& a, int nranks, int channels, int block
     return PR_OK;
 }
 
-int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_config& cfg, cudaStream_t s, bool coop) {
+int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_config& cfg, cudaStream_t s, bool coop,
+                bool in_nvls = false) {
     const int32_t threads = cfg.threads, channels = cfg.channels;
     const bool f32 = a.dtype == PR_DTYPE_F32;
     bool registered = true;
     for (int r = 0; r < nranks; ++r) registered = registered && a.calls[r].reg_id >= 0;
     // the fused update (K7 inside K3) exists in the TMA ring only (its callers check pick_algo)
-    const int algo = a.fuse ? PR_ALGO_RING : pick_algo(cfg, a.count, a.dtype, P, registered);
+    const int algo = a.fuse ? PR_ALGO_RING : pick_algo(cfg, a.count, a.dtype, P, registered, in_nvls);
     a.algo = algo;
     switch (algo) {
+        case PR_ALGO_NVLS:
+            return launch_k3((void*)nvls_kernel, a, nranks, channels, threads, 0, s, coop);
         case PR_ALGO_ONESHOT:
             return launch_k3(f32 ? (void*)oneshot_ll_kernel<float> : (void*)oneshot_ll_kernel<__nv_bfloat16>, a, nranks,
                              channels, threads, 0, s, coop);
@@ -1697,7 +1863,205 @@ int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_conf
     return launch_k3(fn, a, nranks, channels, threads + 64, smem, s, coop);
 }
 
+// ---- NVLS region: driver entry points fetched at run time (no link-time libcuda dependency: the library
+// must load on a GPU-less host) ---------------------------------------------------------------------------
+struct DrvApi {
+    bool ok = false;
+    CUresult (*devGet)(CUdevice*, int);
+    CUresult (*devAttr)(int*, CUdevice_attribute, CUdevice);
+    CUresult (*mcGran)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags);
+    CUresult (*mcCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*);
+    CUresult (*mcAdd)(CUmemGenericAllocationHandle, CUdevice);
+    CUresult (*mcBind)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                       unsigned long long);
+    CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t);
+    CUresult (*memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+    CUresult (*memRelease)(CUmemGenericAllocationHandle);
+    CUresult (*addrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+    CUresult (*addrFree)(CUdeviceptr, size_t);
+    CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+    CUresult (*memUnmap)(CUdeviceptr, size_t);
+    CUresult (*setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+    CUresult (*exportH)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long);
+    CUresult (*importH)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType);
+};
+
+const DrvApi& drv() {
+    static DrvApi d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        auto get = [](const char* name, void** fp) {
+            cudaDriverEntryPointQueryResult q;
+            return cudaGetDriverEntryPoint(name, fp, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess && *fp;
+        };
+        bool ok = true;
+        ok = ok && get("cuDeviceGet", (void**)&d.devGet);
+        ok = ok && get("cuDeviceGetAttribute", (void**)&d.devAttr);
+        ok = ok && get("cuMulticastGetGranularity", (void**)&d.mcGran);
+        ok = ok && get("cuMulticastCreate", (void**)&d.mcCreate);
+        ok = ok && get("cuMulticastAddDevice", (void**)&d.mcAdd);
+        ok = ok && get("cuMulticastBindMem", (void**)&d.mcBind);
+        ok = ok && get("cuMulticastUnbind", (void**)&d.mcUnbind);
+        ok = ok && get("cuMemCreate", (void**)&d.memCreate);
+        ok = ok && get("cuMemRelease", (void**)&d.memRelease);
+        ok = ok && get("cuMemAddressReserve", (void**)&d.addrReserve);
+        ok = ok && get("cuMemAddressFree", (void**)&d.addrFree);
+        ok = ok && get("cuMemMap", (void**)&d.memMap);
+        ok = ok && get("cuMemUnmap", (void**)&d.memUnmap);
+        ok = ok && get("cuMemSetAccess", (void**)&d.setAccess);
+        ok = ok && get("cuMemExportToShareableHandle", (void**)&d.exportH);
+        ok = ok && get("cuMemImportFromShareableHandle", (void**)&d.importH);
+        d.ok = ok;
+        cudaGetLastError();
+    });
+    return d;
+}
+
+void nvls_release(pr_comm* c) {
+    if (!c->nv_size) return;
+    const DrvApi& d = drv();
+    CUdevice dev = 0;
+    d.devGet(&dev, c->device);
+    if (c->nv_mc) { d.memUnmap((CUdeviceptr)c->nv_mc, c->nv_size); d.addrFree((CUdeviceptr)c->nv_mc, c->nv_size); }
+    if (c->nv_uc) { d.memUnmap((CUdeviceptr)c->nv_uc, c->nv_size); d.addrFree((CUdeviceptr)c->nv_uc, c->nv_size); }
+    if (c->nv_mc_handle && c->nv_mem_handle) d.mcUnbind((CUmemGenericAllocationHandle)c->nv_mc_handle, dev, 0, c->nv_size);
+    if (c->nv_mem_handle) d.memRelease((CUmemGenericAllocationHandle)c->nv_mem_handle);
+    if (c->nv_mc_handle) d.memRelease((CUmemGenericAllocationHandle)c->nv_mc_handle);
+    c->nv_uc = c->nv_mc = 0;
+    c->nv_mc_handle = c->nv_mem_handle = 0;
+    c->nv_size = 0;
+    c->tab.nv_uc = c->tab.nv_mc = nullptr;
+    c->tab.nv_bytes = 0;
+}
+
+struct NvHello {
+    int32_t err;        // this rank failed a step so far (every rank fails together)
+    int32_t kind;       // rank 0's export: 1 fabric handle, 2 POSIX file descriptor (pid + fd)
+    int32_t pid, fd;
+    unsigned char fabric[64];
+};
+
+// One collective step of the setup: every rank contributes its error flag (and rank 0 its handle);
+// returns the first error of any rank.
+int nv_sync(pr_comm* c, NvHello& me, std::vector<NvHello>& all) {
+    all.assign(c->P, NvHello{});
+    if (exchange(c, &me, sizeof(NvHello), all.data())) return PR_ERR_INVALID;
+    for (const NvHello& h : all)
+        if (h.err) return h.err;
+    return PR_OK;
+}
+
 }  // namespace
+
+// NVLS region: see include/propring.h.  Collective.
+extern "C" int pr_comm_nvls_alloc(pr_comm* c, size_t bytes, void** d_ptr) {
+    if (!c || !d_ptr || bytes == 0 || c->local || c->P < 2 || c->nv_size) return PR_ERR_INVALID;
+    PR_CUDA_TRY(cudaSetDevice(c->device));
+    const DrvApi& d = drv();
+    NvHello me{};
+    std::vector<NvHello> all;
+    CUdevice dev = 0;
+    int mc_ok = 0;
+    if (!d.ok || d.devGet(&dev, c->device) != CUDA_SUCCESS ||
+        d.devAttr(&mc_ok, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev) != CUDA_SUCCESS || !mc_ok)
+        me.err = PR_ERR_UNSUPPORTED;
+    CUmulticastObjectProp mp;
+    std::memset(&mp, 0, sizeof(mp));
+    mp.numDevices = (unsigned)c->P;
+    mp.size = bytes;
+    size_t gran = 0;
+    if (!me.err) {
+        mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+        if (d.mcGran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !gran) me.err = PR_ERR_UNSUPPORTED;
+    }
+    const size_t size = gran ? (bytes + gran - 1) / gran * gran : 0;
+    mp.size = size;
+    CUmemGenericAllocationHandle mc = 0, mem = 0;
+    CUmemAllocationHandleType htype = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    // step 1: rank 0 creates the multicast object and exports it (fabric handle as bytes if the platform
+    // has one, else a file descriptor the peers duplicate with pidfd_getfd)
+    if (c->rank == 0 && !me.err) {
+        mp.handleTypes = (CUmemAllocationHandleType)(CU_MEM_HANDLE_TYPE_FABRIC | CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+        if (d.mcCreate(&mc, &mp) == CUDA_SUCCESS &&
+            d.exportH(me.fabric, mc, CU_MEM_HANDLE_TYPE_FABRIC, 0) == CUDA_SUCCESS) {
+            me.kind = 1;
+        } else {
+            if (mc) d.memRelease(mc);
+            mc = 0;
+            mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+            int fd = -1;
+            if (d.mcCreate(&mc, &mp) == CUDA_SUCCESS &&
+                d.exportH(&fd, mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) == CUDA_SUCCESS) {
+                me.kind = 2;
+                me.pid = (int32_t)getpid();
+                me.fd = fd;
+            } else {
+                me.err = PR_ERR_UNSUPPORTED;
+            }
+        }
+    }
+    int rc = nv_sync(c, me, all);
+    // step 2: the peers import it
+    if (!rc && c->rank != 0) {
+        const NvHello& h0 = all[0];
+        if (h0.kind == 1) {
+            htype = CU_MEM_HANDLE_TYPE_FABRIC;
+            if (d.importH(&mc, (void*)h0.fabric, CU_MEM_HANDLE_TYPE_FABRIC) != CUDA_SUCCESS) me.err = PR_ERR_UNSUPPORTED;
+        } else {
+            const int pfd = (int)syscall(SYS_pidfd_open, h0.pid, 0);
+            const int fd = pfd >= 0 ? (int)syscall(SYS_pidfd_getfd, pfd, h0.fd, 0) : -1;
+            if (fd < 0 || d.importH(&mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) != CUDA_SUCCESS)
+                me.err = PR_ERR_UNSUPPORTED;
+            if (fd >= 0) close(fd);
+            if (pfd >= 0) close(pfd);
+        }
+    } else if (!rc && c->rank == 0) {
+        htype = all[0].kind == 1 ? CU_MEM_HANDLE_TYPE_FABRIC : CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    }
+    if (!rc) rc = nv_sync(c, me, all);
+    if (c->rank == 0 && me.kind == 2 && me.fd >= 0) close(me.fd);   // every peer has duplicated it
+    // step 3: every rank adds its device, allocates and binds its memory, maps both aliases
+    CUdeviceptr uc = 0, mcp = 0;
+    if (!rc) {
+        CUmemAllocationProp ap;
+        std::memset(&ap, 0, sizeof(ap));
+        ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        ap.location.id = c->device;
+        ap.requestedHandleTypes = htype;
+        CUmemAccessDesc acc;
+        acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc.location.id = c->device;
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        if (d.mcAdd(mc, dev) != CUDA_SUCCESS || d.memCreate(&mem, size, &ap, 0) != CUDA_SUCCESS ||
+            d.mcBind(mc, 0, mem, 0, size, 0) != CUDA_SUCCESS || d.addrReserve(&uc, size, gran, 0, 0) != CUDA_SUCCESS ||
+            d.memMap(uc, size, 0, mem, 0) != CUDA_SUCCESS || d.setAccess(uc, size, &acc, 1) != CUDA_SUCCESS ||
+            d.addrReserve(&mcp, size, gran, 0, 0) != CUDA_SUCCESS || d.memMap(mcp, size, 0, mc, 0) != CUDA_SUCCESS ||
+            d.setAccess(mcp, size, &acc, 1) != CUDA_SUCCESS || cudaMemset((void*)uc, 0, size) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess)
+            me.err = PR_ERR_UNSUPPORTED;
+        cudaGetLastError();
+        rc = nv_sync(c, me, all);
+    }
+    c->nv_mc_handle = mc;
+    c->nv_mem_handle = mem;
+    c->nv_uc = (uintptr_t)uc;
+    c->nv_mc = (uintptr_t)mcp;
+    c->nv_size = size;
+    if (!rc) {
+        c->tab.nv_uc = (uint8_t*)uc;
+        c->tab.nv_mc = (uint8_t*)mcp;
+        c->tab.nv_bytes = (int64_t)size;
+        rc = push_table(c);
+    }
+    if (rc) {
+        nvls_release(c);
+        return rc;
+    }
+    *d_ptr = (void*)uc;
+    return PR_OK;
+}
 
 extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t device, pr_exchange_fn fn, void* ctx,
                             const pr_comm_config* cfg) {
@@ -1900,8 +2264,10 @@ extern "C" int pr_weighted_allreduce(pr_comm* c, void* d_buf, int64_t count, int
     a.calls[0].buf = d_buf;
     a.calls[0].n_local = n_local;
     find_reg(c, d_buf, (size_t)count * dtype_size(dt), &a.calls[0].reg_id, &a.calls[0].reg_off);
+    const uintptr_t b = (uintptr_t)d_buf;
+    const bool in_nvls = c->nv_uc && b >= c->nv_uc && b + (size_t)count * dtype_size(dt) <= c->nv_uc + c->nv_size;
     PR_CUDA_TRY(cudaSetDevice(c->device));
-    return launch_ring(a, 1, c->P, c->device, c->cfg, (cudaStream_t)stream, false);
+    return launch_ring(a, 1, c->P, c->device, c->cfg, (cudaStream_t)stream, false, in_nvls);
 }
 
 extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d_bufs, int64_t count, int32_t dt,
@@ -2107,6 +2473,7 @@ extern "C" const char* pr_strerror(int code) {
         case PR_ERR_PEER_TIMEOUT: return "peer timeout (watchdog)";
         case PR_ERR_CAPACITY: return "capacity too small";
         case PR_ERR_INTERNAL: return "internal error";
+        case PR_ERR_UNSUPPORTED: return "not supported on this platform (NVLS multicast)";
         default: return "unknown error";
     }
 }

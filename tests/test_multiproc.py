@@ -131,6 +131,44 @@ def _gpu_worker(rank, world, port, q):
                     bad.append(f"fused status={comm.status()}")
             dist.barrier()
             comm.destroy()
+        # a registration that fails on any rank leaves nothing behind (the next one gets region 0
+        # and the direct all-gather works); NVLS (N2) is set up or refused on every rank together
+        comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=2, watchdog_ns=30_000_000_000,
+                                                                  algo=pr.ALGO_NVLS))
+        try:
+            comm.register(torch.zeros(1024, pin_memory=True))       # host memory: no CUDA-IPC handle
+            bad.append("registering host memory succeeded")
+        except pr.PropringError as e:
+            if e.code != pr.PR_ERR_CUDA:
+                bad.append(f"register error {e.code}")
+        L = 4099
+        g = synth.gradients(world, L, seed_base=21)
+        n = [3, 5]
+        buf = comm.alloc(L * 4, dtype=torch.float32)
+        buf.copy_(torch.from_numpy(g[rank]))
+        pr.weighted_allreduce(comm, buf, n[rank])                  # outside any NVLS region: the ring
+        torch.cuda.synchronize()
+        if not (comm.status() == 0 and np.array_equal(buf.cpu().numpy(), W.ring_emulate(g, n, "f32"))):
+            bad.append(f"ring after failed register: status={comm.status()}")
+        try:
+            nv = comm.nvls_alloc(L * 4, dtype=torch.float32)
+            nv_code = 0
+        except pr.PropringError as e:
+            nv, nv_code = None, e.code
+        codes = [None] * world
+        dist.all_gather_object(codes, nv_code)
+        if len(set(codes)) != 1 or nv_code not in (0, pr.PR_ERR_UNSUPPORTED):
+            bad.append(f"nvls codes {codes}")
+        if nv is not None:                                         # a box with NVSwitch multicast
+            nv.copy_(torch.from_numpy(g[rank]))
+            pr.weighted_allreduce(comm, nv, n[rank])
+            torch.cuda.synchronize()
+            ref, den = W.weighted_average(W.as_f64(g, "f32"), n)
+            err, zb = W.error_metric(nv.double().cpu().numpy(), ref, den)
+            if not (comm.status() == 0 and zb == 0 and err <= 1e-5):
+                bad.append(f"nvls err={err} status={comm.status()}")
+        dist.barrier()
+        comm.destroy()
         q.put((rank, "ok" if not bad else "; ".join(bad)))
     except Exception as e:
         q.put((rank, repr(e)))
