@@ -354,6 +354,7 @@ def run_workload(name, args, ctx, strong=True, steps=None, warmup=None, e2e_epoc
         del wk                                             # the device-resident leg is done: free its memory
         torch.cuda.empty_cache()
         wk_h = Worker(cfg_h, rank, world, local, comm, data=xh, labels=yh)
+        del xh, yh                                         # the pinned copy inside wk_h is the one used
         for _ in range(3):                                 # warm-up: the allocation freezes, after
             epoch(w=wk_h)                                  # which every epoch prefetches the next one's rows
         torch.cuda.synchronize()

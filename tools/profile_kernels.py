@@ -122,6 +122,10 @@ if __name__ == "__main__":
         shard(reps)
     if what in ("sgd", "all"):
         sgd(reps)
+    if what == "sgd_vgg16":                            # the VGG-16 leg's update (138,357,544 fp32)
+        sgd(reps, L=138_357_544)
+    if what == "gather_imagenet_epoch_hwc_lsu":        # the VGG-16 leg's launch kind (LSU, channels-last)
+        gather(16384, 150528, 16384, reps, 50176, impls=(1,), layout=1)
     if what in ("ring_fused", "all"):
         ring_fused(reps)
     if what == "ring_fused_only":

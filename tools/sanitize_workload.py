@@ -54,7 +54,8 @@ def main():
     # K3: local groups, both scopes, direct and staged, ragged counts
     for flags in (dict(), dict(sys_scope=True), dict(force_staged=True), dict(algo=pr.ALGO_TWO_SHOT),
                   dict(algo=pr.ALGO_LL), dict(algo=pr.ALGO_LL, sys_scope=True), dict(algo=pr.ALGO_ONESHOT),
-                  dict(min_slice_bytes=512)):
+                  dict(min_slice_bytes=512), dict(bulk_store=True), dict(bulk_store=True, force_staged=True),
+                  dict(bulk_store=True, sys_scope=True), dict(algo=pr.ALGO_AUTO, force_staged=True)):
         comms = pr.comm_init_local(3, 0, pr.comm_config(channels=2, slots=4, slot_bytes=4096, stages=2,
                                                         tile_bytes=2048, threads=64, **flags))
         for L in (5, 3001):
@@ -73,27 +74,35 @@ def main():
                                   OW.ring_emulate(hb, [2, 5, 0], "bf16"))
         for c in comms:
             c.destroy()
-    # K3 with K7 fused (rows a6-a9): [grad | theta] per rank, against ring + K7 composed
-    comms = pr.comm_init_local(3, 0, pr.comm_config(channels=2, slots=4, slot_bytes=4096, stages=2, tile_bytes=2048,
-                                                    threads=64))
-    for L in (5, 3001):
-        Lp = (L + 3) // 4 * 4
-        g = synth.gradients(3, L, seed_base=L + 1)
-        th0 = torch.from_numpy(synth.gradients(1, L, seed_base=L + 2)[0]).cuda()
-        store = [torch.zeros(2 * Lp, device="cuda") for _ in range(3)]
-        gr, th = [s_[:L] for s_ in store], [s_[Lp:Lp + L] for s_ in store]
-        for r in range(3):
-            gr[r].copy_(torch.from_numpy(g[r]))
-            th[r].copy_(th0)
-        pr.weighted_allreduce_sgd_local(comms, gr, th, [2, 0, 1], 0.1, 1e-4)
-        ref = th0.clone()
-        pr.sgd_update(ref, torch.from_numpy(OW.ring_emulate(g, [2, 0, 1], "f32")).cuda(), 0.1, 1e-4)
-        torch.cuda.synchronize()
-        assert all(c.status() == 0 for c in comms)
-        assert all(torch.equal(t, ref) for t in th) and all(torch.count_nonzero(x) == 0 for x in gr)
-    for c in comms:
-        c.destroy()
+    # K3 with K7 fused (rows a6-a9): [grad | theta] per rank, against ring + K7 composed (STG and bulk paths)
+    for bulk in (False, True):
+        comms = pr.comm_init_local(3, 0, pr.comm_config(channels=2, slots=4, slot_bytes=4096, stages=2, tile_bytes=2048,
+                                                        threads=64, bulk_store=bulk))
+        for L in (5, 3001):
+            Lp = (L + 3) // 4 * 4
+            g = synth.gradients(3, L, seed_base=L + 1)
+            th0 = torch.from_numpy(synth.gradients(1, L, seed_base=L + 2)[0]).cuda()
+            store = [torch.zeros(2 * Lp, device="cuda") for _ in range(3)]
+            gr, th = [s_[:L] for s_ in store], [s_[Lp:Lp + L] for s_ in store]
+            for r in range(3):
+                gr[r].copy_(torch.from_numpy(g[r]))
+                th[r].copy_(th0)
+            pr.weighted_allreduce_sgd_local(comms, gr, th, [2, 0, 1], 0.1, 1e-4)
+            ref = th0.clone()
+            pr.sgd_update(ref, torch.from_numpy(OW.ring_emulate(g, [2, 0, 1], "f32")).cuda(), 0.1, 1e-4)
+            torch.cuda.synchronize()
+            assert all(c.status() == 0 for c in comms)
+            assert all(torch.equal(t, ref) for t in th) and all(torch.count_nonzero(x) == 0 for x in gr)
+        for c in comms:
+            c.destroy()
+    # a6 timestamps on the device + K6's device-side value path (pr_stamp / pr_stamp_seconds)
+    ring = torch.zeros(9, dtype=torch.int64, device="cuda")
+    for _ in range(4):
+        pr.stamp(ring)
+    d = torch.zeros((), dtype=torch.float64, device="cuda")
+    pr.stamp_seconds(ring, d)
     torch.cuda.synchronize()
+    assert float(d) >= 0.0
     print("sanitize workload: ok")
 
 

@@ -63,7 +63,7 @@ def main():
     reps = [a for a in sys.argv[2:] if a.endswith(".ncu-rep")]
     launches = sys.argv[sys.argv.index("--launches") + 1] if "--launches" in sys.argv else None
     lines = [f"# ncu summary — {tag}", "", "Captured with `ncu --set full --clock-control none --import-source on` "
-             "(kernel replay, cold caches, serialised) by `tools/ncu_round.sh` on one B200; "
+             "(kernel replay, cold caches, serialised) by `tools/ncu_round.sh` / `tools/ncu_round2.sh` on one B200; "
              "raw reports stay in gpurun_out/ (scratch).", ""]
     traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
@@ -87,8 +87,11 @@ def main():
             if st:
                 lines.append("| top stall reasons (cycles/instr) | " + ", ".join(f"{n} {x:.1f}" for x, n in st) + " |")
             lines.append("")
-            kind = ("gather" if "gather" in kname else "sgd" if "sgd_kernel" in kname else
-                    "ring_ll" if "ring_ll" in kname else "ring_fused" if "ring_kernel<float, 1>" in kname else
+            kind = ("gather_imagenet" if "gather" in kname and "imagenet" in name else
+                    "sgd_vgg16" if "sgd_kernel" in kname and "vgg" in name else
+                    "gather" if "gather" in kname else "sgd" if "sgd_kernel" in kname else
+                    "ring_ll" if "ring_ll" in kname else
+                    "ring_fused" if ("ring_kernel<float, 1" in kname or "ring_kernel<float, true" in kname) else
                     "twoshot" if "twoshot" in kname else "ring_colocated" if "ring" in kname else
                     "permute" if "permute" in kname else name)
             if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d:
@@ -115,7 +118,8 @@ def main():
             per[k][1] += t
             total += t
         mine = ("gather_tma_kernel", "gather_kernel", "permute_kernel", "ring_kernel", "ring_ll_kernel", "twoshot_kernel",
-                "sgd_kernel", "spin_kernel", "stamp_kernel", "allgather_f64")
+                "sgd_kernel", "spin_kernel", "stamp_kernel", "allgather_f64", "oneshot_ll_kernel", "nvls_kernel",
+                "stamp_seconds_kernel")
         lines += ["## Launch list of the bench command (`ncu --metrics gpu__time_duration.sum`)", "",
                   f"Total kernel time {total / 1e3:.2f} ms over {sum(v[0] for v in per.values())} launches "
                   "(cold-cache, serialised: compare shares, not absolutes).", "",
