@@ -1451,14 +1451,25 @@ __device__ __forceinline__ float mm_ld_reduce_f32(const float* mc) {
 __device__ __forceinline__ void mm_st_f32(float* mc, float v) {
     asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "f"(v) : "memory");
 }
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+    float v;
+    asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
 __device__ __forceinline__ NvFlags* nv_of(uint8_t* w, const DevTable* t, int ch) {
     return reinterpret_cast<NvFlags*>(w + t->off_nv) + ch;
 }
 
+// EMU (local groups only, for tests): the switch operations are replaced by their definition over the
+// ranks' unicast buffers — ld_reduce = Σ_q x_q[j] in rank order, st = a store into every rank's buffer —
+// so the kernel's phases, geometry, barriers, tails and zero ranks are exercised on one GPU, where no
+// multicast object can be created.
+template <bool EMU>
 __global__ void __launch_bounds__(512, 1) nvls_kernel(const __grid_constant__ LaunchArgs A) {
     __shared__ int s_err;
     __shared__ long long s_sumn;
     __shared__ unsigned long long s_seq;
+    __shared__ uint8_t* s_bufs[PR_MAX_RANKS];
     const RankCall& rc = A.calls[blockIdx.y];
     const DevTable* tab = rc.tab;
     const int ch = blockIdx.x;
@@ -1471,9 +1482,9 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const __grid_constant__ La
         const unsigned long long start = gtimer();
         if (t0 && ch == 0) tab->stamps[0] = (long long)start;
         if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
-        const HsOut hs = handshake(A, rc, tab, st, ch, tab->sysscope != 0, deadline, nullptr, nullptr);
+        const HsOut hs = handshake(A, rc, tab, st, ch, tab->sysscope != 0, deadline, nullptr, EMU ? s_bufs : nullptr);
         if (t0) {
-            s_err = hs.err;
+            s_err = hs.err ? hs.err : ((EMU && !hs.direct) ? PR_ERR_INVALID : 0);
             s_sumn = hs.sumn;
             s_seq = st->seq;
             if (ch == 0) tab->stamps[1] = (long long)gtimer();
@@ -1494,7 +1505,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const __grid_constant__ La
     const float s = (float)((double)rc.n_local / (double)s_sumn);    // n_r/Σn: fp64 division, fp32 weight
     const bool act = rc.n_local > 0;
     float* buf = reinterpret_cast<float*>(rc.buf);
-    float* mcb = reinterpret_cast<float*>(tab->nv_mc + (reinterpret_cast<uint8_t*>(rc.buf) - tab->nv_uc));
+    float* mcb = EMU ? nullptr : reinterpret_cast<float*>(tab->nv_mc + (reinterpret_cast<uint8_t*>(rc.buf) - tab->nv_uc));
     auto range = [&](int c, int64_t& lo, int64_t& len) {
         const int64_t clo = (int64_t)c * cs;
         const int64_t chi = min(clo + cs, count);
@@ -1543,13 +1554,21 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const __grid_constant__ La
         int64_t lo, len;
         range(r, lo, len);
         const int64_t nv = len / 4;
-        for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
-            float* p = mcb + lo + 4 * v;
-            mm_st_v4(p, mm_ld_reduce_v4(p));
-        }
-        for (int64_t e = nv * 4 + threadIdx.x; e < len; e += blockDim.x) {
-            float* p = mcb + lo + e;
-            mm_st_f32(p, mm_ld_reduce_f32(p));
+        if constexpr (EMU) {
+            for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
+                float acc = 0.0f;
+                for (int q = 0; q < P; ++q) acc = __fadd_rn(acc, ld_cg_f32(reinterpret_cast<const float*>(s_bufs[q]) + lo + e));
+                for (int q = 0; q < P; ++q) reinterpret_cast<float*>(s_bufs[q])[lo + e] = acc;
+            }
+        } else {
+            for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+                float* p = mcb + lo + 4 * v;
+                mm_st_v4(p, mm_ld_reduce_v4(p));
+            }
+            for (int64_t e = nv * 4 + threadIdx.x; e < len; e += blockDim.x) {
+                float* p = mcb + lo + e;
+                mm_st_f32(p, mm_ld_reduce_f32(p));
+            }
         }
     }
     barrier(true);                                    // every rank's multicast stores into my memory landed
@@ -1828,8 +1847,9 @@ int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_conf
     const int algo = a.fuse ? PR_ALGO_RING : pick_algo(cfg, a.count, a.dtype, P, registered, in_nvls);
     a.algo = algo;
     switch (algo) {
-        case PR_ALGO_NVLS:
-            return launch_k3((void*)nvls_kernel, a, nranks, channels, threads, 0, s, coop);
+        case PR_ALGO_NVLS:   // a local group (coop) runs the emulation: no multicast object on one device
+            return launch_k3(coop ? (void*)nvls_kernel<true> : (void*)nvls_kernel<false>, a, nranks, channels, threads,
+                             0, s, coop);
         case PR_ALGO_ONESHOT:
             return launch_k3(f32 ? (void*)oneshot_ll_kernel<float> : (void*)oneshot_ll_kernel<__nv_bfloat16>, a, nranks,
                              channels, threads, 0, s, coop);
@@ -2299,7 +2319,8 @@ extern "C" int pr_weighted_allreduce_local(pr_comm* const* comms, void* const* d
         find_reg(comms[r], d_bufs[r], 0, &a.calls[r].reg_id, &a.calls[r].reg_off);
     }
     PR_CUDA_TRY(cudaSetDevice(c0->device));
-    return launch_ring(a, P, P, c0->device, c0->cfg, (cudaStream_t)stream, true);
+    // PR_ALGO_NVLS in a local group: the software emulation of the multicast kernel (nvls_kernel<true>)
+    return launch_ring(a, P, P, c0->device, c0->cfg, (cudaStream_t)stream, true, /*in_nvls=*/true);
 }
 
 // ---- K7 fused into K3: weighted allreduce + SGD update (+ gradient reset) ---------------------------

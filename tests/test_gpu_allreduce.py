@@ -691,3 +691,35 @@ def test_bulk_store_randomized_configs_and_graph_replay():
         gr.replay()
         torch.cuda.synchronize()
         assert all(np.array_equal(d.cpu().numpy(), emu) for d in dev)
+
+
+# ---- NVLS (N2): the multicast kernel's logic through its software emulation on one GPU ---------------------
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_nvls_kernel_emulated_within_tolerance(P):
+    """PR_ALGO_NVLS in a local group runs nvls_kernel<EMU>: the same phases (weights applied in place, a
+    per-channel cross-rank barrier, chunk-owner reduce + store to every rank, a second barrier), with the
+    switch's ld_reduce / multicast store replaced by their definition over the ranks' buffers — one GPU has
+    no multicast object.  Switch order is unspecified (DESIGN.md §3 #48): tolerance vs the fp64 mean, all
+    ranks identical, a zero-sample rank holding NaN contributes nothing, back-to-back calls and bf16 (which
+    takes the ring) included."""
+    comms = group(P, algo=pr.ALGO_NVLS, channels=4)
+    rng = np.random.Generator(np.random.PCG64(500 + P))
+    for L in (1, 7, P + 1, 1000, 4099, 2 ** 20 + 3):
+        n = [int(x) * 16 for x in rng.integers(1, 6, P)]
+        if L % 2:
+            n[int(rng.integers(0, P))] = 0
+        host, dev = _inputs(P, L, "f32", kind="mixed" if L % 2 else "gaussian", seed=L + P)
+        for r in range(P):
+            if n[r] == 0:
+                dev[r].fill_(float("nan"))
+        pr.weighted_allreduce_local(comms, dev, n)
+        pr.weighted_allreduce_local(comms, [d.clone() for d in dev], n)      # back to back (seq advances)
+        torch.cuda.synchronize()
+        assert all(c.status() == 0 for c in comms)
+        outs = [d.cpu().numpy() for d in dev]
+        assert all(np.array_equal(outs[0], o) for o in outs[1:])
+        h64 = W.as_f64(host, "f32")
+        ref, den = W.weighted_average(h64, n)
+        err, zb = W.error_metric(outs[0].astype(np.float64), ref, den)
+        assert zb == 0 and err <= TOL["f32"], (L, err)
+    _check(P, 4099, "bf16", [1 + r for r in range(P)], comms, seed=9)         # bf16: the ring's bits

@@ -89,7 +89,7 @@ def run_colocated(P, max_mib, reps, algo=0):
         c.destroy()
 
 
-def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0):
+def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0, bulk=False):
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -102,11 +102,13 @@ def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0):
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, P = dist.get_rank(), dist.get_world_size()
-    comm = pr.comm_init(rank, P, local, config=pr.comm_config(algo=algo, channels=channels, min_slice_bytes=min_slice))
+    comm = pr.comm_init(rank, P, local, config=pr.comm_config(algo=algo, channels=channels, min_slice_bytes=min_slice,
+                                                              bulk_store=bulk))
     n = weights(P)
     s = n[rank] / sum(n)
     Zmax = max_mib << 20
-    raw = comm.alloc(Zmax)
+    # NVLS (algo 5): the buffers must live in the communicator's NVLS region (multicast-bound memory)
+    raw = comm.nvls_alloc(Zmax) if algo == pr.ALGO_NVLS else comm.alloc(Zmax)
     for dtype, es in ((torch.float32, 4), (torch.bfloat16, 2)):
         for Z in sizes(max_mib):
             L = Z // es
@@ -162,11 +164,12 @@ if __name__ == "__main__":
     ap.add_argument("--colocated", type=int, default=0)
     ap.add_argument("--max-mib", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--algo", type=int, default=0, help="0 ring, 1 two-shot, 2 auto, 3 LL ring, 4 one-shot LL")
+    ap.add_argument("--algo", type=int, default=0, help="0 ring, 1 two-shot, 2 auto, 3 LL ring, 4 one-shot LL, 5 NVLS")
     ap.add_argument("--channels", type=int, default=0, help="CTAs per rank (multi-GPU mode; 0 = topology default)")
     ap.add_argument("--min-slice", type=int, default=0, help="ring min_slice_bytes (0 = slot-sized slices)")
+    ap.add_argument("--bulk", action="store_true", help="ring data path with TMA bulk stores")
     a = ap.parse_args()
     if a.colocated:
         run_colocated(a.colocated, a.max_mib, a.reps, a.algo)
     else:
-        run_multi(a.max_mib, a.reps, a.algo, a.channels, a.min_slice)
+        run_multi(a.max_mib, a.reps, a.algo, a.channels, a.min_slice, a.bulk)

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Everything this round could not measure on a one-GPU box, for the first call that gets > 1 GPU.
+# Everything that cannot be measured on a one-GPU box, for the first call that gets > 1 GPU.
 # Output -> gpurun_out/mg_*.  Usage: bash tools/multigpu_first_run.sh [max GPUs, default 8]
 G=${1:-8}
 mkdir -p gpurun_out
@@ -15,8 +15,14 @@ for P in 2 4 8; do
       > gpurun_out/mg_bench_p$P.json 2> gpurun_out/mg_bench_p$P.err
   timeout 1200 $TR --nproc-per-node $P --master-port $((29620 + P)) bench.py --gpus $P --steps 5 --warmup 3 --overlap \
       --no-cpu-baseline > gpurun_out/mg_bench_overlap_p$P.json 2> gpurun_out/mg_bench_overlap_p$P.err
-  timeout 1200 $TR --nproc-per-node $P --master-port $((29660 + P)) bench.py --gpus $P --steps 5 --warmup 3 --strong \
-      --no-cpu-baseline > gpurun_out/mg_bench_strong_p$P.json 2> gpurun_out/mg_bench_strong_p$P.err
+  timeout 1200 $TR --nproc-per-node $P --master-port $((29660 + P)) bench.py --gpus $P --steps 5 --warmup 3 --weak \
+      --no-cpu-baseline --no-vgg > gpurun_out/mg_bench_weak_p$P.json 2> gpurun_out/mg_bench_weak_p$P.err
+  # TMA bulk-store data path vs 16-byte STG over real NVLink (co-located proxy: 5-8 % slower)
+  timeout 900 $TR --nproc-per-node $P --master-port $((29670 + P)) tools/ar_sweep.py --max-mib 256 --bulk \
+      > gpurun_out/mg_ar_sweep_bulk_p$P.jsonl 2> gpurun_out/mg_ar_sweep_bulk_p$P.err
+  # NVLS (in-switch reduction), where the box can create a multicast object
+  timeout 900 $TR --nproc-per-node $P --master-port $((29680 + P)) tools/ar_sweep.py --max-mib 1024 --algo 5 \
+      > gpurun_out/mg_ar_sweep_nvls_p$P.jsonl 2> gpurun_out/mg_ar_sweep_nvls_p$P.err
 done
 # ring channel count (CTAs per rank) at the largest P: 16 is the co-located optimum, NVLink may want more
 for ch in 16 24 32 48 64; do
