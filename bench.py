@@ -203,11 +203,16 @@ def mix_ceiling():
         return None
 
 
-def traffic_from_profiles(kind):
-    """dram bytes per launch from the committed ncu --set full capture (profiles/ncu_traffic.json)."""
+def traffic_from_profiles(kind, algorithmic_bytes=None):
+    """dram bytes per launch from the committed ncu --set full capture (profiles/ncu_traffic.json); when the
+    capture's launch was a different size (its algorithmic bytes are recorded), scaled to this launch."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f).get(kind, {}).get("dram_bytes_per_launch")
+            e = json.load(f).get(kind, {})
+        t = e.get("dram_bytes_per_launch")
+        if t is not None and algorithmic_bytes and e.get("algorithmic_bytes"):
+            t = t * algorithmic_bytes / e["algorithmic_bytes"]
+        return t
     except Exception:
         return None
 
@@ -297,7 +302,7 @@ def run_workload(name, args, ctx, strong=True, steps=None, warmup=None, e2e_epoc
               "bound": "hbm", "achieved": g_bytes / (g_avg * 1e-3) / 1e9 if g_ms else None, "peak": hbm,
               "unit": "GB/s", "peak_kind": peak_kind, "launches": len(g_ms), "avg_us": g_avg * 1e3,
               "bytes_per_launch": g_bytes, "total_ms": sum(g_ms),
-              "traffic": traffic_from_profiles("gather" if name == "resnet18" else "gather_imagenet")}
+              "traffic": traffic_from_profiles("gather" if name == "resnet18" else "gather_imagenet", g_bytes)}
     gather["frac"] = gather["achieved"] / hbm if gather["achieved"] else None
     mix = mix_ceiling()
     if mix and gather["achieved"]:
@@ -314,7 +319,7 @@ def run_workload(name, args, ctx, strong=True, steps=None, warmup=None, e2e_epoc
                "bound": "hbm", "achieved": u_bytes / (u_avg * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                "peak_kind": peak_kind, "launches": len(u_ms), "avg_us": u_avg * 1e3,
                "bytes_per_launch": u_bytes, "total_ms": sum(u_ms),
-               "traffic": traffic_from_profiles("sgd" if name == "resnet18" else "sgd_vgg16")}
+               "traffic": traffic_from_profiles("sgd" if name == "resnet18" else "sgd_vgg16", u_bytes)}
         sgd["frac"] = sgd["achieved"] / hbm
         if sgd["total_ms"] > roof["total_ms"]:
             roof = sgd

@@ -74,27 +74,41 @@ def step_cost(t1, n, sigma, spin, c0):
 
 
 def minmax_alloc(cost, P, C, floor=1):
-    """The best integer allocation for increasing per-rank step costs: min over w (Σw = C, w_r >= floor) of
-    max_r cost(r, w_r).  For a candidate T every rank takes the most units that keep it <= T; the smallest
-    candidate T (over all achievable per-rank step times) whose greedy allocation reaches C is optimal.
-    Returns (T_step, w)."""
+    """The best integer allocation for measured per-rank step costs: min over w (Σw = C, w_r >= floor) of
+    max_r cost(r, w_r).  Costs need not be monotone in w (cuDNN picks a different algorithm per batch size,
+    so a measured t1(n) table has dips): for a candidate T, rank r may take any u with cost(r, u) <= T, and
+    a subset-sum DP over the ranks decides whether the units can total exactly C; a binary search over the
+    sorted achievable step times finds the smallest feasible T.  Among the allocations meeting it, the DP
+    keeps the one whose costs sum lowest.  Returns (T_step, w)."""
     table = [[cost(r, u) for u in range(floor, C + 1)] for r in range(P)]
-    for T in sorted({t for row in table for t in row}):
-        w = []
+    cands = sorted({t for row in table for t in row})
+
+    def solve(T):
+        # best[k] = (sum of costs, choice list) reaching k units with the ranks so far
+        best = {0: (0.0, [])}
         for r in range(P):
-            k = floor - 1
-            for j, t in enumerate(table[r]):
-                if t <= T:
-                    k = floor + j
-            w.append(k)
-        if min(w) >= floor and sum(w) >= C:
-            # trim the surplus one unit at a time from the currently costliest rank (any trim keeps max <= T;
-            # this one also lowers the remaining ranks' times lexicographically)
-            for _ in range(sum(w) - C):
-                r = max((i for i in range(P) if w[i] > floor), key=lambda i: (table[i][w[i] - floor], -i))
-                w[r] -= 1
-            return T, w
-    raise ValueError("no feasible allocation")
+            nxt = {}
+            for k, (sc, ch) in best.items():
+                for j, t in enumerate(table[r]):
+                    u = floor + j
+                    if t > T or k + u > C:
+                        continue
+                    cand = (sc + t, ch + [u])
+                    if k + u not in nxt or cand[0] < nxt[k + u][0]:
+                        nxt[k + u] = cand
+            best = nxt
+        return best.get(C)
+
+    lo, hi = 0, len(cands) - 1
+    if solve(cands[hi]) is None:
+        raise ValueError("no feasible allocation")
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if solve(cands[mid]) is not None:
+            hi = mid
+        else:
+            lo = mid + 1
+    return cands[lo], solve(cands[lo])[1]
 
 
 def affine_minmax(a, b, sigma, g, C, floor=1, spin="t1", c0=0.0):
@@ -243,8 +257,19 @@ def run_virtual(args):
     # t1(n) ≈ a + b·n of the same table is reported beside it.
     v = w.alloc.view()
     wmax = C - (P - 1) * cfg.floor
-    t1tab = {u: w.t1(g * u) for u in range(cfg.floor, wmax + 1)}
-    pts = sorted((g * u, t) for u, t in t1tab.items())
+    # --opt-stride k: time every k-th unit count (plus the ends and the final allocation's) and interpolate
+    # linearly between them (VGG-16 captures cost seconds each); 1 = every unit count
+    meas = sorted(set(range(cfg.floor, wmax + 1, max(1, args.opt_stride))) | {wmax} | set(v["w"]) - {0})
+    t1m = {u: w.t1(g * u) for u in meas}
+    t1tab = {}
+    for u in range(cfg.floor, wmax + 1):
+        if u in t1m:
+            t1tab[u] = t1m[u]
+        else:
+            a_ = max(x for x in meas if x < u)
+            b_ = min(x for x in meas if x > u)
+            t1tab[u] = t1m[a_] + (t1m[b_] - t1m[a_]) * (u - a_) / (b_ - a_)
+    pts = sorted((g * u, t) for u, t in t1m.items())
     a0, b0 = fit_affine([p_[0] for p_ in pts], [p_[1] for p_ in pts])
     c0s = w.c0_ns / 1e9
     t_step, w_opt = minmax_alloc(lambda r, u: step_cost(t1tab[u], g * u, sigma[r], args.spin, c0s) if u <= wmax
@@ -283,6 +308,8 @@ def main():
     ap.add_argument("--never-freeze", action="store_true", help="keep adapting after the ratio is stable")
     ap.add_argument("--ema", type=float, default=1.0, help="EMA weight on t_s (1 = raw, S:166)")
     ap.add_argument("--metrics-csv", default="", help="append the per-(epoch, rank) metrics CSV (SURVEY §5) here")
+    ap.add_argument("--opt-stride", type=int, default=1,
+                    help="measured-cost bound: time t1 at every k-th unit count and interpolate (1 = all)")
     ap.add_argument("--spin", default="t1", choices=["t1", "sample"],
                     help="K4 emulation: t1 = (σ−1)·t1(n_r) per step; sample = (σ−1)·c0·n_r (SURVEY §8(a) a4)")
     args = ap.parse_args()

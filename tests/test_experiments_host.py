@@ -58,6 +58,20 @@ def test_minmax_alloc_on_a_measured_table():
     assert sum(w) == 16 and abs(T - best) < 1e-15
 
 
+def test_minmax_alloc_non_monotone_costs():
+    """A measured table is not monotone (cuDNN picks a different algorithm per batch size): a feasible
+    allocation may skip over a costly unit count; the DP still finds the exact optimum."""
+    rng = np.random.Generator(np.random.PCG64(9))
+    for _ in range(40):
+        P, C = 3, int(rng.integers(3, 13))
+        tab = [[float(x) for x in rng.uniform(1.0, 2.0, C + 1)] for _ in range(P)]
+        T, w = E.minmax_alloc(lambda r, u: tab[r][u], P, C)
+        best = min(max(tab[r][x] for r, x in enumerate(ws))
+                   for ws in itertools.product(range(1, C + 1), repeat=P) if sum(ws) == C)
+        assert sum(w) == C and min(w) >= 1 and abs(T - best) < 1e-15
+        assert max(tab[r][x] for r, x in enumerate(w)) <= T
+
+
 def test_fit_affine():
     a, b = E.fit_affine([64, 128, 256], [1.3e-3 + 1.5e-6 * n for n in (64, 128, 256)])
     assert abs(a - 1.3e-3) < 1e-12 and abs(b - 1.5e-6) < 1e-15

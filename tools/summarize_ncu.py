@@ -28,7 +28,8 @@ KEYS = [
     ("launch__block_size", "block"),
     ("lts__t_bytes.sum", "L2 bytes"),
 ]
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+         "ns": 1e-3, "us": 1, "ms": 1e3}
 
 
 def raw(rep):
@@ -81,6 +82,9 @@ def main():
                 if isinstance(v, float) and u in SCALE and key.startswith(("dram__bytes", "lts__t_bytes")):
                     v = v * SCALE[u]
                     u = "byte"
+                if isinstance(v, float) and u in ("nsecond", "usecond", "msecond", "ns", "us", "ms") and key == "gpu__time_duration.sum":
+                    v = v * SCALE[u]
+                    u = "usecond"
                 d[key] = v
                 lines.append(f"| {label} (`{key}`) | {v:,.3f} {u} |" if isinstance(v, float) else f"| {label} | {v} |")
             st = stalls(hdr, row)
