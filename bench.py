@@ -193,11 +193,13 @@ def bench_config(world, overlap=False, strong=True, workload="resnet18", data_n=
 
 
 def mix_ceiling():
-    """Best GB/s of the sequential 1:2 read:write streaming probe (context for K2's roofline)."""
+    """Best GB/s of the sequential 1:2 read:write streaming probe at the ImageNet epoch size (context for
+    K2's roofline): 2.47 GB u8 read, 4.93 GB written, 16-byte STGs or smem tiles + bulk stores, L2 evicted
+    clean or dirty before each rep (tools/probes/mix_probe.cu, profiles/round2_k2_mix_probe_imagenet.txt)."""
     try:
         import re
-        with open(os.path.join(ROOT, "profiles", "round1_k2_mix_ceiling.txt")) as f:
-            v = [float(m.group(1)) for m in re.finditer(r"widen .*?([0-9.]+) GB/s", f.read())]
+        with open(os.path.join(ROOT, "profiles", "round2_k2_mix_probe_imagenet.txt")) as f:
+            v = [float(m.group(1)) for m in re.finditer(r"widen .*?([0-9.]+) GB/s best", f.read())]
         return max(v) if v else None
     except OSError:
         return None
@@ -298,7 +300,8 @@ def run_workload(name, args, ctx, strong=True, steps=None, warmup=None, e2e_epoc
     g_rows = [n for _, _, n in wk.gather_events]
     g_avg = statistics.mean(g_ms) if g_ms else float("nan")
     g_bytes = statistics.mean(g_rows) * (row_bytes + 2 * row_bytes + 8 + 8 + 8) if g_rows else 0.0
-    gather = {"kernel": "gather_kernel<U8_TO_BF16_AFFINE> channels-last (K2, LSU, one launch per epoch)",
+    gather = {"kernel": "gather_hwc_bulk_kernel<U8_TO_BF16_AFFINE, 3> channels-last (K2: coalesced loads -> smem "
+                        "tile -> cp.async.bulk store; one launch per epoch)",
               "bound": "hbm", "achieved": g_bytes / (g_avg * 1e-3) / 1e9 if g_ms else None, "peak": hbm,
               "unit": "GB/s", "peak_kind": peak_kind, "launches": len(g_ms), "avg_us": g_avg * 1e3,
               "bytes_per_launch": g_bytes, "total_ms": sum(g_ms),
@@ -307,8 +310,9 @@ def run_workload(name, args, ctx, strong=True, steps=None, warmup=None, e2e_epoc
     mix = mix_ceiling()
     if mix and gather["achieved"]:
         gather["mix_ceiling"] = {"gbs": mix, "frac": gather["achieved"] / mix,
-                                 "source": "tools/probes/widen_probe.cu: sequential stream with K2's 1:2 "
-                                           "read:write byte mix (profiles/round1_k2_mix_ceiling.txt)"}
+                                 "source": "tools/probes/mix_probe.cu: sequential stream with K2's 1:2 read:write "
+                                           "byte mix at the ImageNet epoch size, best store flavour "
+                                           "(profiles/round2_k2_mix_probe_imagenet.txt)"}
     roof = gather
     sgd = None
     if wk.sgd_events:

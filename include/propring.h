@@ -141,9 +141,12 @@ int pr_permute(int64_t N, uint64_t seed, int64_t epoch, int64_t begin, int64_t c
 #define PR_GATHER_U8_TO_F32_AFFINE  1  /* (float(x) − shift_c)·scale_c, two fp32 roundings, no FMA   */
 #define PR_GATHER_U8_TO_BF16_AFFINE 2  /* the same value rounded to bfloat16 (RNE)                   */
 #define PR_GATHER_MAX_CHANNELS 16
-#define PR_GATHER_IMPL_AUTO 0   /* TMA staging when the launch moves >= 8 MiB of input, else LSU        */
+#define PR_GATHER_IMPL_AUTO 0   /* device source, >= 1 MiB: channels-last -> BULK; CHW >= 8 MiB -> TMA; else LSU */
 #define PR_GATHER_IMPL_LSU  1   /* warp per 2 KiB segment, ld.global.nc 16-byte vectors                 */
 #define PR_GATHER_IMPL_TMA  2   /* cp.async.bulk rows / segments into a 4-stage smem ring (mbarrier)    */
+#define PR_GATHER_IMPL_BULK 3   /* channels-last output only: coalesced loads -> smem tile in output
+                                   order -> one cp.async.bulk store per 4096 output pixels (device
+                                   sources; a host source runs the LSU kernel); PR_ERR_INVALID for CHW */
 #define PR_GATHER_LAYOUT_CHW 0  /* output row in the input's channel-major order                        */
 #define PR_GATHER_LAYOUT_HWC 1  /* channels-last output: element (c, p) at p·channels + c; needs
                                    channels <= 4 and plane % 16 == 0 (both kernels)                     */

@@ -180,6 +180,7 @@ def permute(N: int, seed: int, epoch: int, begin: int, count: int, out, stream=N
 GATHER_IMPL_AUTO = 0
 GATHER_IMPL_LSU = 1
 GATHER_IMPL_TMA = 2
+GATHER_IMPL_BULK = 3
 GATHER_LAYOUT_CHW = 0
 GATHER_LAYOUT_HWC = 1
 

@@ -6,8 +6,11 @@
 // build-defined (DESIGN.md §3 #38, #41): dst[t,:] = op(src[idx[t],:]), lab_dst[t] = lab_src[idx[t]];
 // with PR_GATHER_LAYOUT_HWC the output element (c, p) of a CHW row is stored at p·C + c.
 //
-// HBM-bound: per row, row_bytes read + out_bytes written (+8 B index, +16 B label).  Two kernels with
+// HBM-bound: per row, row_bytes read + out_bytes written (+8 B index, +16 B label).  Three kernels with
 // identical results:
+//   gather_hwc_bulk_kernel  channels-last output: coalesced loads, conversion into a smem tile in output
+//                      order, one cp.async.bulk store per 4096 output pixels (below; the AUTO choice for
+//                      channels-last launches of >= 1 MiB from device memory);
 //   gather_tma_kernel  persistent CTAs; a producer warp prefetches row indices and issues cp.async.bulk
 //                      copies (whole rows, 24 KiB segments, or per-channel pixel blocks) into a 4-stage
 //                      mbarrier ring; 8 consumer warps convert from smem and store 16-byte vectors.
@@ -479,6 +482,151 @@ __global__ void __launch_bounds__(32 * (kTmaConsumerWarps + 1)) gather_tma_kerne
     }
 }
 
+// ---- Bulk-store variant (channels-last output) ----------------------------------------------------------
+// The output of a channels-last gather is one contiguous stream: dst pixel q (row t = q / plane, pixel
+// p = q mod plane) sits at q·C·es.  A unit is kBulkPx consecutive output pixels (several short rows or a
+// block of a long row): every thread loads kBulkGroups 8-pixel groups (C 8-byte loads each, coalesced per
+// plane across the warp, all issued before any conversion), converts them into the unit's smem tile in
+// output order (16-byte smem stores, conflict-free at the 48-byte lane stride), and one thread pushes the
+// whole tile with a single cp.async.bulk store.  Two tiles per CTA: a tile is rewritten only after its
+// previous bulk store has read it.  Why: a 1:2 read:write stream with 16-byte STGs tops out at 5.97 TB/s
+// on B200, with smem tiles + bulk stores at 6.28 TB/s (tools/probes/mix_probe.cu, ImageNet-sized) —
+// full-line writes in large bursts.  t = q / plane by a 64-bit multiply-high with m = ceil(2^64 / plane),
+// exact while q·plane < 2^64 (checked on the host).
+constexpr int kBulkThreads = 256;
+constexpr int kBulkGroupsDefault = 2;                            // 8-pixel groups per thread per unit
+constexpr int64_t kBulkAutoBytes = 1 << 20;                      // AUTO: input bytes from which the bulk kernel runs
+
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int OP, int C, int kBulkGroups>
+__global__ void __launch_bounds__(kBulkThreads) gather_hwc_bulk_kernel(const __grid_constant__ GatherParams p,
+                                                                       uint64_t magic) {
+    extern __shared__ __align__(128) uint8_t tiles[];             // [2][kBulkPx · C · es]
+    constexpr int64_t kBulkPx = 8 * kBulkThreads * kBulkGroups;      // output pixels per unit
+    constexpr int es = OP == PR_GATHER_U8_TO_BF16_AFFINE ? 2 : 4;
+    constexpr int NV = C * 8 * es / 16;                              // 16-byte vectors per 8-pixel group
+    constexpr int64_t kTile = kBulkPx * C * es;
+    if (p.lab_dst) {                                                 // labels: one thread per row
+        const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < p.n; t += nthreads)
+            p.lab_dst[t] = p.lab_src[p.idx[t]];
+    }
+    const uint64_t plane = (uint64_t)p.plane;
+    const uint64_t total = (uint64_t)p.n * plane;
+    const uint64_t units = (total + kBulkPx - 1) / kBulkPx;
+    int buf = 0;
+    for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        uint8_t* tile = tiles + buf * kTile;
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();                                             // the tile's previous store has read it
+        const uint64_t q0 = u * kBulkPx;
+        const uint64_t npx = min((uint64_t)kBulkPx, total - q0);
+        uint32_t ww[kBulkGroups][C * 2];
+#pragma unroll
+        for (int g = 0; g < kBulkGroups; ++g) {
+            const uint64_t px = 8ull * (threadIdx.x + (uint64_t)g * kBulkThreads);
+            if (px < npx) {
+                const uint64_t q = q0 + px;
+                const uint64_t t = __umul64hi(q, magic);
+                const uint8_t* s = p.src + __ldg(p.idx + t) * p.row_bytes + (q - t * plane);
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const uint2 w = *reinterpret_cast<const uint2*>(s + c * p.plane);
+                    ww[g][2 * c] = w.x;
+                    ww[g][2 * c + 1] = w.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < kBulkGroups; ++g) {
+            const uint64_t px = 8ull * (threadIdx.x + (uint64_t)g * kBulkThreads);
+            if (px < npx) {
+                uint4 o[NV];
+                hwc_convert_words<OP, C, 8>(p, ww[g], o);
+                uint4* d = reinterpret_cast<uint4*>(tile + px * C * es);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) d[v] = o[v];
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> bulk copy
+        __syncthreads();
+        if (threadIdx.x == 0) bulk_store(p.dst + q0 * C * es, tile, (uint32_t)(npx * C * es));
+        buf ^= 1;
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int OP, int G>
+const void* bulk_fn_g(int C) {
+    switch (C) {
+        case 1: return (const void*)gather_hwc_bulk_kernel<OP, 1, G>;
+        case 2: return (const void*)gather_hwc_bulk_kernel<OP, 2, G>;
+        case 3: return (const void*)gather_hwc_bulk_kernel<OP, 3, G>;
+        default: return (const void*)gather_hwc_bulk_kernel<OP, 4, G>;
+    }
+}
+template <int OP>
+const void* bulk_fn(int C, int G) {
+    return G == 1 ? bulk_fn_g<OP, 1>(C) : bulk_fn_g<OP, 2>(C);
+}
+
+// Launch of the bulk-store kernel; false when the geometry is outside its exactness range (caller falls back).
+int launch_hwc_bulk(const GatherParams& p, cudaStream_t s, bool* launched) {
+    *launched = false;
+    const unsigned __int128 pl = (unsigned __int128)(uint64_t)p.plane;
+    if ((unsigned __int128)(uint64_t)p.n * pl * pl >= ((unsigned __int128)1 << 64)) return PR_OK;
+    const uint64_t magic = (uint64_t)((((unsigned __int128)1 << 64) + pl - 1) / pl);
+    // A/B knob: groups per thread, 1 or 2 (measured, 4 bench launch sizes: 2 = 1 within noise; 4 is 5-20 %
+    // slower and its f32 4-channel tiles would not fit in shared memory)
+    static const int G = [] {
+        const char* e = getenv("PR_GATHER_BULK_GROUPS");
+        const int v = e ? atoi(e) : kBulkGroupsDefault;
+        return v == 1 ? 1 : 2;
+    }();
+    const int64_t upx = 8 * kBulkThreads * G;
+    const int es = p.op == PR_GATHER_U8_TO_BF16_AFFINE ? 2 : 4;
+    const int C = p.channels;
+    const size_t smem = 2 * (size_t)upx * C * es;
+    const void* fn = p.op == PR_GATHER_U8_TO_BF16_AFFINE ? bulk_fn<PR_GATHER_U8_TO_BF16_AFFINE>(C, G)
+                                                         : bulk_fn<PR_GATHER_U8_TO_F32_AFFINE>(C, G);
+    // per device, per (op, C): dynamic-smem opt-in and the resident grid
+    static std::mutex mu;
+    static int grid_of[PR_MAX_DEVICES][2][kMaxHwcChannels + 1];
+    int dev = 0;
+    PR_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= PR_MAX_DEVICES) return PR_ERR_INVALID;
+    const int oi = p.op == PR_GATHER_U8_TO_BF16_AFFINE ? 1 : 0;
+    int grid = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!grid_of[dev][oi][C]) {
+            PR_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int sms = 0, per = 0;
+            PR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            PR_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kBulkThreads, smem));
+            static const int cap = [] {
+                const char* e = getenv("PR_GATHER_BULK_CTAS");      // A/B knob: CTAs per SM (default 8)
+                const int v = e ? atoi(e) : 8;
+                return v < 1 ? 8 : v;
+            }();
+            grid_of[dev][oi][C] = sms * (per < 1 ? 1 : (per < cap ? per : cap));
+        }
+        grid = grid_of[dev][oi][C];
+    }
+    const int64_t units = ((int64_t)p.n * p.plane + upx - 1) / upx;
+    const int blocks = (int)(units < grid ? (units > 0 ? units : 1) : grid);
+    void* args[] = {(void*)&p, (void*)&magic};
+    PR_CUDA_TRY(cudaLaunchKernel(fn, dim3(blocks), dim3(kBulkThreads), args, smem, s));
+    *launched = true;
+    return PR_OK;
+}
+
 }  // namespace
 
 extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_bytes, const int64_t* d_idx, int64_t n,
@@ -529,6 +677,14 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
     }
     // Measured on B200: CHW output, >= 8 MiB: TMA 5.26 vs LSU 4.89 TB/s; HWC output: LSU
     // 5.61 vs TMA 4.90 TB/s (each lane's per-plane 8-byte loads coalesce; no extra smem pass).
+    if (impl == PR_GATHER_IMPL_BULK && !p.hwc) return PR_ERR_INVALID;   // channels-last output only
+    if (p.hwc && !host_src &&
+        (impl == PR_GATHER_IMPL_BULK || (impl == PR_GATHER_IMPL_AUTO && n * row_bytes >= kBulkAutoBytes))) {
+        bool launched = false;
+        const int rc = launch_hwc_bulk(p, s, &launched);
+        if (rc != PR_OK || launched) return rc;
+        if (impl == PR_GATHER_IMPL_BULK) return PR_ERR_INVALID;      // outside the kernel's index range
+    }
     const bool tma = impl == PR_GATHER_IMPL_TMA ||
                      (impl == PR_GATHER_IMPL_AUTO && !host_src && !p.hwc && n * row_bytes >= (8ll << 20));
     if (tma) {

@@ -146,16 +146,17 @@ class Worker:
                 labels = torch.from_numpy(synth.labels(cfg.N, cfg.classes, seed=1))
         self.X = data.pin_memory() if cfg.host_data else data.to(self.dev)
         self.Y = labels.to(self.dev)
-        # K2 kernel chosen here, as the library's AUTO rule would (HWC or host data -> LSU, CHW -> TMA),
-        # so the launch does no host-side pointer query
-        lsu = cfg.host_data or cfg.channels_last
+        # K2 kernel chosen here, as the library's AUTO rule would (host data -> LSU, channels-last -> the
+        # bulk-store kernel, CHW -> TMA), so the launch does no host-side pointer query
+        lsu = cfg.host_data
         if self.features:                             # fp32 rows: a byte-exact copy (O5 COPY)
             self.gop = pr.make_gather_op(pr.GATHER_COPY, impl=pr.GATHER_IMPL_LSU)
         else:
             C, H, W = cfg.shape
             self.gop = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE if cfg.bf16_compute else pr.GATHER_U8_TO_F32_AFFINE,
                                          [1.0 / s for s in CIFAR_STD[:C]], CIFAR_MEAN[:C], H * W,
-                                         impl=pr.GATHER_IMPL_LSU if lsu else pr.GATHER_IMPL_TMA,
+                                         impl=pr.GATHER_IMPL_LSU if lsu else
+                                         pr.GATHER_IMPL_BULK if cfg.channels_last else pr.GATHER_IMPL_TMA,
                                          layout=pr.GATHER_LAYOUT_HWC if cfg.channels_last else pr.GATHER_LAYOUT_CHW)
         torch.backends.cudnn.benchmark = True
         # try every cuDNN algorithm when autotuning (default: the first 10 heuristics' picks): the

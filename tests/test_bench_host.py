@@ -67,13 +67,16 @@ def test_oracle_leg_allocation_matches_timed_arm():
 
 
 def test_mix_ceiling_parser(tmp_path, monkeypatch):
+    """The K2 ceiling is the best 1:2 widen line of the ImageNet-size mix probe (the plain copy lines and
+    the mean columns are not it)."""
     b = _bench()
     prof = tmp_path / "profiles"
     prof.mkdir()
-    (prof / "round1_k2_mix_ceiling.txt").write_text(
-        "widen u1 grid 4xSM                 best   81.92 us mean   82.34 us   5529.6 GB/s (best)\n"
-        "copy 151MB->151MB grid 4xSM        best   63.49 us mean   64.33 us   4756.6 GB/s (best)\n")
+    (prof / "round2_k2_mix_probe_imagenet.txt").write_text(
+        "clean  widen stg grid 4xSM            best   1239.0 us mean   1241.3 us   5971.4 GB/s best   5960.7 GB/s mean\n"
+        "clean  copy 1:1 grid 8xSM             best    792.6 us mean    805.5 us   6223.4 GB/s best   6123.3 GB/s mean\n"
+        "dirty  widen tma-store grid 3xSM      best   1183.7 us mean   1186.1 us   6250.3 GB/s best   6237.7 GB/s mean\n")
     monkeypatch.setattr(b, "ROOT", str(tmp_path))
-    assert b.mix_ceiling() == 5529.6
-    (prof / "round1_k2_mix_ceiling.txt").unlink()
+    assert b.mix_ceiling() == 6250.3
+    (prof / "round2_k2_mix_probe_imagenet.txt").unlink()
     assert b.mix_ceiling() is None

@@ -185,13 +185,52 @@ def test_gather_hwc_bit_exact(channels, plane, n):
     scale = np.array([1.0 / STD[c % 3] for c in range(channels)], dtype=np.float32)
     shift = np.array([MEAN[c % 3] for c in range(channels)], dtype=np.float32)
     dX, didx = _dev(X), _dev(idx)
+    Y = rng.integers(0, 1000, nsrc, dtype=np.int64)
+    dY = _dev(Y)
     for op, width, impl in [(o, w, i) for o, w in ((pr.GATHER_U8_TO_BF16_AFFINE, 2), (pr.GATHER_U8_TO_F32_AFFINE, 4))
-                            for i in (pr.GATHER_IMPL_LSU, pr.GATHER_IMPL_TMA)]:
-        out = torch.full((n * row_bytes * width,), 0x5A, dtype=torch.uint8, device="cuda")
+                            for i in (pr.GATHER_IMPL_LSU, pr.GATHER_IMPL_TMA, pr.GATHER_IMPL_BULK)]:
+        out = torch.full((n * row_bytes * width + 64,), 0x5A, dtype=torch.uint8, device="cuda")
+        lab = torch.full((n,), -7, dtype=torch.int64, device="cuda")
         gop = pr.make_gather_op(op, scale, shift, plane, impl=impl, layout=pr.GATHER_LAYOUT_HWC)
+        pr.gather_rows(dX, nsrc, row_bytes, didx, n, out, gop, dY, lab)
+        ref, rlab = OG.gather_rows(X, idx, op, scale, shift, plane, layout="hwc", Y=Y)
+        got = out.cpu().numpy()
+        assert np.array_equal(got[:n * row_bytes * width], np.ascontiguousarray(ref).view(np.uint8).reshape(-1))
+        assert (got[n * row_bytes * width:] == 0x5A).all()          # nothing written past the output
+        assert np.array_equal(lab.cpu().numpy(), rlab)
+
+
+@pytest.mark.parametrize("channels,plane,n", [(3, 1024, 4097), (3, 1360, 333), (1, 4096, 3), (4, 16, 1),
+                                              (3, 50176, 7), (2, 8192, 5)])
+def test_gather_hwc_bulk_unit_boundaries(channels, plane, n):
+    """The bulk-store kernel's units are 4096 consecutive OUTPUT pixels: units that span several rows, start
+    mid-row, end mid-row, a ragged last unit, and rows longer than a unit — bit-exact against the oracle, with
+    the bytes past the output untouched."""
+    row_bytes = channels * plane
+    nsrc = max(16, n)
+    rng = np.random.Generator(np.random.PCG64(7 * plane + n))
+    X = rng.integers(0, 256, (nsrc, row_bytes), dtype=np.uint8)
+    idx = rng.integers(0, nsrc, n, dtype=np.int64)
+    scale = np.array([1.0 / STD[c % 3] for c in range(channels)], dtype=np.float32)
+    shift = np.array([MEAN[c % 3] for c in range(channels)], dtype=np.float32)
+    dX, didx = _dev(X), _dev(idx)
+    for op, width in ((pr.GATHER_U8_TO_BF16_AFFINE, 2), (pr.GATHER_U8_TO_F32_AFFINE, 4)):
+        out = torch.full((n * row_bytes * width + 4096,), 0x5A, dtype=torch.uint8, device="cuda")
+        gop = pr.make_gather_op(op, scale, shift, plane, impl=pr.GATHER_IMPL_BULK, layout=pr.GATHER_LAYOUT_HWC)
         pr.gather_rows(dX, nsrc, row_bytes, didx, n, out, gop)
         ref, _ = OG.gather_rows(X, idx, op, scale, shift, plane, layout="hwc")
-        assert np.array_equal(out.cpu().numpy(), np.ascontiguousarray(ref).view(np.uint8).reshape(-1))
+        got = out.cpu().numpy()
+        assert np.array_equal(got[:n * row_bytes * width], np.ascontiguousarray(ref).view(np.uint8).reshape(-1))
+        assert (got[n * row_bytes * width:] == 0x5A).all()
+
+
+def test_gather_bulk_rejects_chw():
+    X = torch.zeros((4, 3 * 16), dtype=torch.uint8, device="cuda")
+    idx = torch.zeros(2, dtype=torch.int64, device="cuda")
+    out = torch.empty((2, 48), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(pr.PropringError):
+        pr.gather_rows(X, 4, 48, idx, 2, out, pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE, [1.0] * 3, [0.0] * 3,
+                                                                16, impl=pr.GATHER_IMPL_BULK))
 
 
 def test_gather_hwc_rejects_unsupported():

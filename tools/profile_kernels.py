@@ -44,7 +44,7 @@ def gather(rows, row_bytes, nsrc, reps, plane, impls=(1, 2), layout=0, seq=False
                                impl=impl, layout=layout)
         us = timed(lambda: pr.gather_rows(X, nsrc, row_bytes, idx, rows, out, op, Y, lab), reps)
         byts = rows * (3 * row_bytes + 24)
-        print(f"gather[{'LSU' if impl == 1 else 'TMA'}{',HWC' if layout else ''}] rows={rows} row_bytes={row_bytes}: {us:.2f} us, "
+        print(f"gather[{ {1: 'LSU', 2: 'TMA', 3: 'BULK'}[impl]}{',HWC' if layout else ''}] rows={rows} row_bytes={row_bytes}: {us:.2f} us, "
               f"{byts / us / 1e3:.1f} GB/s algorithmic")
 
 
@@ -118,6 +118,14 @@ if __name__ == "__main__":
         gather(336, 150528, 2000, reps, 50176, impls=(1, 2), layout=1)
     if what == "gather_imagenet_epoch_hwc":            # a VGG-16 epoch-size launch (16,384 distinct rows, 7.4 GB)
         gather(16384, 150528, 16384, reps, 50176, impls=(1, 2), layout=1)
+    if what == "gather_bulk_ab":                       # channels-last: LSU vs bulk-store kernel at the bench's sizes
+        for rows, rb, nsrc, plane in ((1024, 3072, 50000, 1024), (49152, 3072, 50000, 1024),
+                                      (336, 150528, 2000, 50176), (16384, 150528, 16384, 50176)):
+            gather(rows, rb, nsrc, reps, plane, impls=(1, 3), layout=1)
+    if what == "gather_imagenet_epoch_hwc_bulk":       # the VGG-16 leg's launch with the bulk-store kernel
+        gather(16384, 150528, 16384, reps, 50176, impls=(3,), layout=1)
+    if what == "gather_epoch_hwc_bulk":
+        gather(49152, 3072, 50000, reps, 1024, impls=(3,), layout=1)
     if what in ("shard", "all"):
         shard(reps)
     if what in ("sgd", "all"):
