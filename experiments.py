@@ -65,6 +65,20 @@ SCHEDULES = {
 }
 
 
+def make_policy(args):
+    """Alloc.set_policy kwargs from the command line (None = the library defaults: Eq. 10, stop rule on)."""
+    policy = {}
+    if args.never_freeze or args.scenario in SCHEDULES:
+        policy["never_freeze"] = True
+    if args.ema < 1.0:
+        policy["ema_alpha"] = args.ema
+    if args.model == "affine":
+        import paper_2111_08272_b200 as pr
+
+        policy["model"] = pr.ALLOC_MODEL_AFFINE
+    return policy or None
+
+
 def step_cost(t1, n, sigma, spin, c0):
     """Step time (s) of a rank σ× slower that processes n rows, from its σ = 1 step time t1 = t1(n): "t1"
     emulation σ·t1(n); "sample" emulation t1(n) + (σ−1)·c0·n (DESIGN.md §3 #46)."""
@@ -163,9 +177,7 @@ def run_virtual(args):
     if args.N:
         N = args.N
     k = args.adapt_every
-    policy = {"never_freeze": True} if (args.never_freeze or args.scenario in SCHEDULES) else None
-    if policy is not None and args.ema < 1.0:
-        policy["ema_alpha"] = args.ema
+    policy = make_policy(args)
     cfg = RunConfig(N=N, shape=shape, model=model, ratios=ratios, C=C, g=g, slowdown=sigma,
                     adaptive=adaptive and not args.static, micro=args.micro or (256 if model == "vgg16" else 1024),
                     adapt_every=k, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario), spin=args.spin)
@@ -307,6 +319,8 @@ def main():
                     help="N3: controller every k aggregation steps over the step-interleaved shard (0 = per epoch)")
     ap.add_argument("--never-freeze", action="store_true", help="keep adapting after the ratio is stable")
     ap.add_argument("--ema", type=float, default=1.0, help="EMA weight on t_s (1 = raw, S:166)")
+    ap.add_argument("--model", default="proportional", choices=["proportional", "affine"],
+                    help="controller step-cost model: the paper's Eq. 10, or the affine extension (DESIGN §3 #49)")
     ap.add_argument("--metrics-csv", default="", help="append the per-(epoch, rank) metrics CSV (SURVEY §5) here")
     ap.add_argument("--opt-stride", type=int, default=1,
                     help="measured-cost bound: time t1 at every k-th unit count and interpolate (1 = all)")
@@ -336,9 +350,7 @@ def main():
     dist.init_process_group("gloo" if shared else "nccl", **({} if shared else {"device_id": torch.device("cuda", local)}))
     tdev = "cpu" if shared else "cuda"
     comm = pr.comm_init(rank, world, local, config=pr.comm_config(algo=pr.ALGO_AUTO))
-    policy = {"never_freeze": True} if (args.never_freeze or args.scenario in SCHEDULES) else None
-    if policy is not None and args.ema < 1.0:
-        policy["ema_alpha"] = args.ema
+    policy = make_policy(args)
     cfg = RunConfig(N=N, shape=shape, model=model, ratios=ratios, C=C, g=g, slowdown=sigma,
                     adaptive=adaptive and not args.static, micro=args.micro or (256 if model == "vgg16" else 1024),
                     adapt_every=args.adapt_every, policy=policy, slowdown_schedule=SCHEDULES.get(args.scenario),

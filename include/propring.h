@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PR_VERSION 10000       /* 1.0.0 */
+#define PR_VERSION 10100       /* 1.1.0 */
 #define PR_MAX_RANKS 64
 
 /* ---- error codes (SPEC error names in parentheses) ------------------------------------------- */
@@ -73,12 +73,25 @@ typedef struct {
     int64_t off[PR_MAX_RANKS]; /* shard offsets: exclusive prefix sum of len in rank order             */
 } pr_alloc_view;
 
+/* Step-time model of the controller.  PROPORTIONAL is the paper's: t_i ∝ w_i (Eq. 6-8), the
+ * update is Eq. 10 + Hamilton.  AFFINE is an opt-in extension (DESIGN.md §3 #49) for steps with a fixed
+ * per-step cost, where Eq. 10's fixed point (all t_i equal) is not the balanced optimum: each rank's
+ * t_i(w) = a_i + b_i·w is fitted by least squares over its last fit_window (w, t) observations (fewer than
+ * two distinct w: a_i = 0, b_i = t_i/w_i; a fit with b <= 0 or a < 0: the same proportional fallback), and
+ * w' = the integer min-max allocation: min over Σw = C, w >= floor of max_i a_i + b_i·w_i (greedy, ties to
+ * the lowest rank).  While no rank has two distinct w (the first update from a uniform start), the update
+ * is Eq. 10 exactly.  Requires floor >= 1. */
+#define PR_ALLOC_MODEL_PROPORTIONAL 0
+#define PR_ALLOC_MODEL_AFFINE       1
+
 /* Stop-rule / smoothing policy of the self-adaptive controller. */
 typedef struct {
     int32_t window;        /* stable when the last `window` vectors differ by <= tol (default 2)     */
     int32_t never_freeze;  /* 1: keep re-allocating every epoch (default 0)                          */
     int64_t tol;           /* per-component tolerance in units (default 1)                           */
     double  ema_alpha;     /* t_eff = a·t + (1−a)·t_eff_prev; 1.0 = raw last-epoch times (default)   */
+    int32_t model;         /* PR_ALLOC_MODEL_* (default PROPORTIONAL)                               */
+    int32_t fit_window;    /* AFFINE: observations per rank in the fit, 2..64 (default 8)             */
 } pr_alloc_policy;
 
 /* Static allocation (§3.1; a1).  w = Hamilton(C·r_i/Σr, floor) with ties to the lowest rank
@@ -104,7 +117,7 @@ int pr_alloc_update(pr_alloc *a, const double *step_times, int32_t *changed);
 int pr_alloc_query(const pr_alloc *a, pr_alloc_view *out);
 /* k-th allocation vector of the history (0 = initial); w_out: host int64[P]. */
 int pr_alloc_history(const pr_alloc *a, int64_t k, int64_t *w_out);
-/* Checkpoint (POD bytes: w, history, frozen flag, policy, EMA state).  *size receives the byte count;
+/* Checkpoint (POD bytes: w, history, frozen flag, policy, EMA state, the t of every update).  *size receives the byte count;
  * with buf == NULL only the size is returned.  PR_ERR_CAPACITY if cap is too small. */
 int pr_alloc_save(const pr_alloc *a, void *buf, size_t cap, size_t *size);
 int pr_alloc_load(pr_alloc **out, const void *buf, size_t size);

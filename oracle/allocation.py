@@ -16,6 +16,14 @@ Follows the paper's algorithm step by step:
 * Eq. 9 = Appendix Eq. 22 closed-form increment u, and the Appendix linear
   system A·u = b (Eqs. 15-21) solved by Gaussian elimination as an oracle cross-check.
 
+* Affine step-cost model (opt-in extension, DESIGN.md §3 #49 — NOT in the paper): the paper's model is
+  t_s ∝ samples (Eq. 6-8); with a fixed per-step cost each rank's epoch time is fitted as
+  t_i(w) = a_i + b_i·w by least squares over its last `fit_window` (w, t) observations, and the next
+  allocation is the integer min-max allocation min_{Σw=C, w>=floor} max_i a_i + b_i·w_i, built by handing
+  out units one at a time to the rank with the smallest cost after taking it (ties to the lowest rank).
+  Fewer than two distinct w for a rank: a_i = 0, b_i = t_i/w_i; a fit with b <= 0 or a < 0: the same
+  proportional model through the latest observation.  No rank with two distinct w: Eq. 10 exactly.
+
 The fp64 operation order of `controller_quotas` is part of the definition (bit-exact with the host
 library; DESIGN.md §3 #35):  v_i = w_i / t_i;  S_v = ((v_0 + v_1) + ...) left to right;
 q_i = (C·v_i) / S_v.
@@ -62,6 +70,9 @@ class Allocation:
     never_freeze: bool = False
     ema_alpha: float = 1.0
     t_prev: list | None = None
+    model: str = "proportional"       # or "affine" (§3 #49)
+    fit_window: int = 8
+    t_hist: list = field(default_factory=list)   # t used by update k (history[k] was in effect)
 
 
 def shard_sizes(N: int, w, C: int):
@@ -129,6 +140,47 @@ def is_stable(history, window: int, tol: int) -> bool:
     return True
 
 
+def affine_fit(ws, ts):
+    """Least-squares t = a + b·w over one rank's observations (chronological), fixed fp64 order:
+    means by left-to-right sums, then Σ(w−mw)², Σ(w−mw)(t−mt) left to right; b = sxy/sxx, a = mt − b·mw.
+    None when fewer than two distinct w; (0, t/w of the latest) when b <= 0 or a < 0."""
+    if all(x == ws[0] for x in ws):
+        return None
+    n = len(ws)
+    sw = 0.0
+    st = 0.0
+    for x, y in zip(ws, ts):
+        sw = sw + float(x)
+        st = st + y
+    mw = sw / float(n)
+    mt = st / float(n)
+    sxx = 0.0
+    sxy = 0.0
+    for x, y in zip(ws, ts):
+        d = float(x) - mw
+        sxx = sxx + d * d
+        sxy = sxy + d * (y - mt)
+    b = sxy / sxx
+    a = mt - b * mw
+    if b > 0.0 and a >= 0.0 and math.isfinite(a) and math.isfinite(b):
+        return a, b
+    return 0.0, ts[-1] / float(ws[-1])
+
+
+def minmax_greedy(models, C: int, floor: int):
+    """Integer min-max allocation for increasing affine costs: every rank at the floor, then each remaining
+    unit to the rank whose cost a + b·(w+1) is smallest (ties to the lowest rank)."""
+    w = [floor] * len(models)
+    for _ in range(C - len(models) * floor):
+        best, bc = 0, None
+        for i, (a, b) in enumerate(models):
+            c = a + b * float(w[i] + 1)
+            if bc is None or c < bc:
+                best, bc = i, c
+        w[best] += 1
+    return w
+
+
 def alloc_update(a: Allocation, t_s) -> bool:
     """O8, Algorithm 1 steps 1-3.  Returns `changed`.  Mutates `a` only on success."""
     if a.frozen:
@@ -140,10 +192,22 @@ def alloc_update(a: Allocation, t_s) -> bool:
         raise ZeroTiming()
     if a.ema_alpha != 1.0 and a.t_prev is not None:
         t = [a.ema_alpha * x + (1.0 - a.ema_alpha) * y for x, y in zip(t, a.t_prev)]
-    q = controller_quotas(a.w, t, a.C)
-    w_new = hamilton(q, a.C, a.floor)
+    w_new = None
+    if a.model == "affine":
+        obs = list(zip(a.history[:len(a.t_hist)], a.t_hist))[-(a.fit_window - 1):] + [(list(a.w), t)]
+        models = []
+        for i in range(a.P):
+            f = affine_fit([o[0][i] for o in obs], [o[1][i] for o in obs])
+            models.append(f)
+        if any(f is not None for f in models):
+            models = [f if f is not None else (0.0, t[i] / float(a.w[i])) for i, f in enumerate(models)]
+            w_new = minmax_greedy(models, a.C, a.floor)
+    if w_new is None:
+        q = controller_quotas(a.w, t, a.C)
+        w_new = hamilton(q, a.C, a.floor)
     changed = w_new != a.w
     a.t_prev = t
+    a.t_hist.append(list(t))
     a.w = w_new
     a.history.append(list(w_new))
     a.epoch += 1

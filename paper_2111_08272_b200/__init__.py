@@ -43,6 +43,10 @@ DTYPE_F32 = 0
 DTYPE_BF16 = 1
 
 
+# pr_alloc_policy.model (include/propring.h): the paper's Eq. 10, or the affine step-cost extension
+ALLOC_MODEL_PROPORTIONAL = 0
+ALLOC_MODEL_AFFINE = 1
+
 class PropringError(RuntimeError):
     def __init__(self, code: int, where: str):
         self.code = code
@@ -107,8 +111,10 @@ class Alloc:
         _check(LIB.pr_alloc_update(self._h, arr, ctypes.byref(ch)), "pr_alloc_update")
         return bool(ch.value)
 
-    def set_policy(self, window=2, tol=1, never_freeze=False, ema_alpha=1.0):
-        pol = AllocPolicy(window=window, never_freeze=1 if never_freeze else 0, tol=tol, ema_alpha=ema_alpha)
+    def set_policy(self, window=2, tol=1, never_freeze=False, ema_alpha=1.0, model=ALLOC_MODEL_PROPORTIONAL,
+                   fit_window=8):
+        pol = AllocPolicy(window=window, never_freeze=1 if never_freeze else 0, tol=tol, ema_alpha=ema_alpha,
+                          model=model, fit_window=fit_window)
         _check(LIB.pr_alloc_set_policy(self._h, ctypes.byref(pol)), "pr_alloc_set_policy")
 
     def view(self) -> dict:

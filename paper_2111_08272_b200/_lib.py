@@ -28,7 +28,8 @@ class AllocView(ctypes.Structure):
 
 
 class AllocPolicy(ctypes.Structure):
-    _fields_ = [("window", c_i32), ("never_freeze", c_i32), ("tol", c_i64), ("ema_alpha", c_dbl)]
+    _fields_ = [("window", c_i32), ("never_freeze", c_i32), ("tol", c_i64), ("ema_alpha", c_dbl),
+                ("model", c_i32), ("fit_window", c_i32)]
 
 
 class GatherOp(ctypes.Structure):

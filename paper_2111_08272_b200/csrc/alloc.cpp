@@ -4,7 +4,8 @@
 // Algorithm 1, Eq. 10, integer rounding, stop rule.
 // Readings: #1 unit of w, #3 Hamilton rounding with ties to the lowest rank, #6 first
 // epoch, #7 stop rule, #9 exact-integer shard sizes, #10 epoch remainder, #34 floor clamping,
-// #35 fixed fp64 operation order (compiled with -ffp-contract=off).
+// #35 fixed fp64 operation order (compiled with -ffp-contract=off); #49 the affine step-cost model
+// (PR_ALLOC_MODEL_AFFINE, an opt-in extension of Eq. 8-10 for steps with a fixed per-step cost).
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -20,10 +21,11 @@ struct pr_alloc {
     int64_t C = 0, g = 1, floor = 1;
     int64_t epoch = 0;
     int32_t frozen = 0;
-    pr_alloc_policy policy{2, 0, 1, 1.0};
+    pr_alloc_policy policy{2, 0, 1, 1.0, PR_ALLOC_MODEL_PROPORTIONAL, 8};
     std::vector<int64_t> w;                  // current allocation, units
     std::vector<std::vector<int64_t>> hist;  // allocation history (initial vector first)
     std::vector<double> t_prev;              // EMA state (empty until the first successful update)
+    std::vector<std::vector<double>> t_hist; // t used by update k (hist[k] was in effect): hist.size() − 1 rows
 };
 
 namespace {
@@ -134,6 +136,58 @@ bool is_stable(const pr_alloc* a) {
     return true;
 }
 
+// ---- affine step-cost model (DESIGN.md §3 #49) ------------------------------------------------------
+// Rank i's epoch time as a function of its units: t_i(w) = a_i + b_i·w, fitted by least squares over its
+// last `fit_window` observations (w in effect, t measured), fixed fp64 order.  Returns false when the
+// observations hold fewer than two distinct w (no slope can be estimated).  A fit with b <= 0 or a < 0 (noise)
+// falls back to the proportional model of Eq. 8 through the latest observation: a = 0, b = t/w.
+bool affine_fit(const std::vector<const std::vector<int64_t>*>& ow, const std::vector<const std::vector<double>*>& ot,
+                int32_t i, double& a_out, double& b_out) {
+    const size_t n = ow.size();
+    bool distinct = false;
+    for (size_t k = 1; k < n; ++k)
+        if ((*ow[k])[i] != (*ow[0])[i]) distinct = true;
+    if (!distinct) return false;
+    double sw = 0.0, st = 0.0;
+    for (size_t k = 0; k < n; ++k) { sw = sw + (double)(*ow[k])[i]; st = st + (*ot[k])[i]; }
+    const double mw = sw / (double)n, mt = st / (double)n;
+    double sxx = 0.0, sxy = 0.0;
+    for (size_t k = 0; k < n; ++k) {
+        const double d = (double)(*ow[k])[i] - mw;
+        sxx = sxx + d * d;
+        sxy = sxy + d * ((*ot[k])[i] - mt);
+    }
+    const double b = sxy / sxx;
+    const double a = mt - b * mw;
+    if (b > 0.0 && a >= 0.0 && std::isfinite(a) && std::isfinite(b)) {
+        a_out = a;
+        b_out = b;
+    } else {
+        a_out = 0.0;
+        b_out = (*ot[n - 1])[i] / (double)(*ow[n - 1])[i];
+    }
+    return true;
+}
+
+// min over integer w (Σw = C, w_i >= floor) of max_i (a_i + b_i·w_i), b_i > 0: start every rank at the
+// floor and hand out the remaining units one at a time to the rank whose cost after taking it is the
+// smallest (ties -> lowest rank).  With increasing costs the k-th unit handed out is the k-th smallest
+// marginal cost, so the final maximum is the minimum possible (greedy is exact for min-max).
+void minmax_greedy(const std::vector<double>& a, const std::vector<double>& b, int64_t C, int64_t floor,
+                   std::vector<int64_t>& w) {
+    const size_t P = a.size();
+    w.assign(P, floor);
+    for (int64_t left = C - (int64_t)P * floor; left > 0; --left) {
+        size_t best = 0;
+        double bc = 0.0;
+        for (size_t i = 0; i < P; ++i) {
+            const double c = a[i] + b[i] * (double)(w[i] + 1);
+            if (i == 0 || c < bc) { best = i; bc = c; }
+        }
+        w[best] += 1;
+    }
+}
+
 }  // namespace
 
 extern "C" int pr_alloc_init(pr_alloc** out, int64_t N, int32_t P, const double* ratios, int64_t C, int64_t g,
@@ -169,9 +223,16 @@ extern "C" int pr_alloc_init(pr_alloc** out, int64_t N, int32_t P, const double*
     return PR_OK;
 }
 
+namespace {
+bool policy_ok(const pr_alloc_policy& p, int64_t floor) {
+    return p.window >= 2 && p.tol >= 0 && p.ema_alpha > 0.0 && p.ema_alpha <= 1.0 &&
+           (p.model == PR_ALLOC_MODEL_PROPORTIONAL || (p.model == PR_ALLOC_MODEL_AFFINE && floor >= 1)) &&
+           p.fit_window >= 2 && p.fit_window <= 64 && (p.never_freeze == 0 || p.never_freeze == 1);
+}
+}  // namespace
+
 extern "C" int pr_alloc_set_policy(pr_alloc* a, const pr_alloc_policy* p) {
-    if (!a || !p || p->window < 2 || p->tol < 0 || !(p->ema_alpha > 0.0) || !(p->ema_alpha <= 1.0))
-        return PR_ERR_INVALID;
+    if (!a || !p || !policy_ok(*p, a->floor)) return PR_ERR_INVALID;
     a->policy = *p;
     return PR_OK;
 }
@@ -190,17 +251,45 @@ extern "C" int pr_alloc_update(pr_alloc* a, const double* t_s, int32_t* changed)
         const double al = a->policy.ema_alpha;
         for (int32_t i = 0; i < P; ++i) t[i] = al * t[i] + (1.0 - al) * a->t_prev[i];
     }
-    // Eq. 10: v_i = w_i/t_i; S_v left to right; q_i = (C·v_i)/S_v.
-    std::vector<double> v(P), q(P);
-    for (int32_t i = 0; i < P; ++i) v[i] = (double)a->w[i] / t[i];
-    double sv = 0.0;
-    for (int32_t i = 0; i < P; ++i) sv = sv + v[i];
-    for (int32_t i = 0; i < P; ++i) q[i] = ((double)a->C * v[i]) / sv;
     std::vector<int64_t> w2;
-    int rc = hamilton(q, a->C, a->floor, w2);
-    if (rc) return rc;
+    bool done = false;
+    if (a->policy.model == PR_ALLOC_MODEL_AFFINE) {
+        // observations (w in effect, t measured): the last fit_window of the history plus this epoch's
+        std::vector<const std::vector<int64_t>*> ow;
+        std::vector<const std::vector<double>*> ot;
+        const size_t nh = a->t_hist.size();
+        const size_t keep = (size_t)a->policy.fit_window - 1;
+        for (size_t k = nh > keep ? nh - keep : 0; k < nh; ++k) { ow.push_back(&a->hist[k]); ot.push_back(&a->t_hist[k]); }
+        ow.push_back(&a->w);
+        ot.push_back(&t);
+        std::vector<double> ca(P), cb(P);
+        bool any = false;
+        for (int32_t i = 0; i < P; ++i) {
+            if (affine_fit(ow, ot, i, ca[i], cb[i])) {
+                any = true;
+            } else {
+                ca[i] = 0.0;                                   // one w seen: Eq. 8's proportional model
+                cb[i] = t[i] / (double)a->w[i];
+            }
+        }
+        if (any) {                                             // else: no slope anywhere -> Eq. 10 below
+            minmax_greedy(ca, cb, a->C, a->floor, w2);
+            done = true;
+        }
+    }
+    if (!done) {
+        // Eq. 10: v_i = w_i/t_i; S_v left to right; q_i = (C·v_i)/S_v.
+        std::vector<double> v(P), q(P);
+        for (int32_t i = 0; i < P; ++i) v[i] = (double)a->w[i] / t[i];
+        double sv = 0.0;
+        for (int32_t i = 0; i < P; ++i) sv = sv + v[i];
+        for (int32_t i = 0; i < P; ++i) q[i] = ((double)a->C * v[i]) / sv;
+        int rc = hamilton(q, a->C, a->floor, w2);
+        if (rc) return rc;
+    }
     const int32_t ch = (w2 != a->w) ? 1 : 0;
     a->t_prev = t;
+    a->t_hist.push_back(t);
     a->w = w2;
     a->hist.push_back(w2);
     a->epoch += 1;
@@ -246,7 +335,7 @@ struct SaveHeader {
 extern "C" int pr_alloc_save(const pr_alloc* a, void* buf, size_t cap, size_t* size) {
     if (!a || !size) return PR_ERR_INVALID;
     const size_t need = sizeof(SaveHeader) + sizeof(int64_t) * a->P * (1 + a->hist.size()) +
-                        sizeof(double) * a->P;
+                        sizeof(double) * a->P * a->hist.size();   // t_prev + t_hist (hist_len − 1 rows)
     if (!buf) { *size = need; return PR_OK; }
     if (cap < need) return PR_ERR_CAPACITY;
     SaveHeader h;
@@ -261,7 +350,8 @@ extern "C" int pr_alloc_save(const pr_alloc* a, void* buf, size_t cap, size_t* s
     for (auto& v : a->hist) { std::memcpy(p, v.data(), sizeof(int64_t) * a->P); p += sizeof(int64_t) * a->P; }
     std::vector<double> tp(a->P, 0.0);
     if (!a->t_prev.empty()) tp = a->t_prev;
-    std::memcpy(p, tp.data(), sizeof(double) * a->P);
+    std::memcpy(p, tp.data(), sizeof(double) * a->P); p += sizeof(double) * a->P;
+    for (auto& v : a->t_hist) { std::memcpy(p, v.data(), sizeof(double) * a->P); p += sizeof(double) * a->P; }
     *size = need;
     return PR_OK;
 }
@@ -278,15 +368,16 @@ extern "C" int pr_alloc_load(pr_alloc** out, const void* buf, size_t size) {
     // same bounds as pr_alloc_init
     if (h.N < 1 || h.N > ((int64_t)1 << 40) || h.C < 1 || h.C > ((int64_t)1 << 20) || h.g < 1 ||
         h.g > ((int64_t)1 << 30) || h.floor < 0 || h.C < (int64_t)h.P * h.floor || h.N < h.g * h.C || h.epoch < 0 ||
-        (h.frozen != 0 && h.frozen != 1) || (h.has_tprev != 0 && h.has_tprev != 1))
+        (h.frozen != 0 && h.frozen != 1) || h.has_tprev != (h.hist_len > 1 ? 1 : 0))
         return PR_ERR_INVALID;
     // same bounds as pr_alloc_set_policy
-    if (h.policy.window < 2 || h.policy.tol < 0 || !(h.policy.ema_alpha > 0.0) || !(h.policy.ema_alpha <= 1.0))
-        return PR_ERR_INVALID;
-    // size check without overflow: the vectors are (1 + hist_len)·P int64 + P doubles
+    if (!policy_ok(h.policy, h.floor)) return PR_ERR_INVALID;
+    // size check without overflow: (1 + hist_len)·P int64 (w, history) + hist_len·P doubles (t_prev, t_hist)
     const size_t row = sizeof(int64_t) * h.P;
-    const size_t fixed = sizeof(SaveHeader) + row + sizeof(double) * h.P;
-    if (size < fixed || (uint64_t)h.hist_len > (size - fixed) / row || size != fixed + row * (size_t)h.hist_len)
+    const size_t drow = sizeof(double) * h.P;
+    const size_t fixed = sizeof(SaveHeader) + row;
+    if (size < fixed || (uint64_t)h.hist_len > (size - fixed) / (row + drow) ||
+        size != fixed + (row + drow) * (size_t)h.hist_len)
         return PR_ERR_INVALID;
     const char* p = (const char*)buf + sizeof(h);
     // every allocation vector (current and history) must be one pr_alloc could have produced: Σw = C, w >= floor
@@ -307,6 +398,13 @@ extern "C" int pr_alloc_load(pr_alloc** out, const void* buf, size_t size) {
     if (h.has_tprev)
         for (double t : tp)
             if (!std::isfinite(t) || !(t > 0.0)) return PR_ERR_INVALID;
+    const char* th = p + row * (size_t)(1 + h.hist_len) + drow;      // t_hist rows
+    for (int64_t k = 0; k + 1 < h.hist_len; ++k)
+        for (uint32_t i = 0; i < h.P; ++i) {
+            double t;
+            std::memcpy(&t, th + drow * (size_t)k + sizeof(double) * i, sizeof(t));
+            if (!std::isfinite(t) || !(t > 0.0)) return PR_ERR_INVALID;
+        }
     pr_alloc* a = new (std::nothrow) pr_alloc();
     if (!a) return PR_ERR_INTERNAL;
     try {
@@ -317,6 +415,8 @@ extern "C" int pr_alloc_load(pr_alloc** out, const void* buf, size_t size) {
         a->hist.resize((size_t)h.hist_len, std::vector<int64_t>(h.P));
         for (auto& v : a->hist) { std::memcpy(v.data(), p, row); p += row; }
         if (h.has_tprev) a->t_prev = tp;
+        a->t_hist.resize((size_t)(h.hist_len - 1), std::vector<double>(h.P));
+        for (auto& v : a->t_hist) { std::memcpy(v.data(), th, drow); th += drow; }
     } catch (...) {   // std::bad_alloc must not cross the C ABI
         delete a;
         return PR_ERR_INTERNAL;

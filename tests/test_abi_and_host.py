@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(_lib.LIB, s), s
         assert s in _lib.SIGNATURES, f"binding lacks {s}"
-    assert pr.version() == 10000
+    assert pr.version() == 10100
 
 
 def test_library_is_built_for_sm100a():
@@ -179,7 +179,8 @@ def test_load_rejects_corrupt_checkpoints():
     good = bytearray(a.save())
     assert pr.Alloc.load(bytes(good)).view() == a.view()
     # SaveHeader: magic@0 version@8 P@12 N@16 C@24 g@32 floor@40 epoch@48 frozen@56 has_tprev@60
-    #             policy{window@64 never_freeze@68 tol@72 ema@80} hist_len@88; w[P] @96, hist, t_prev
+    #             policy{window@64 never_freeze@68 tol@72 ema@80 model@88 fit_window@92} hist_len@96;
+    #             w[P] @104, hist[hist_len][P], t_prev[P], t_hist[hist_len-1][P]
     def patched(off, fmt, val):
         b = bytearray(good)
         struct.pack_into(fmt, b, off, val)
@@ -188,10 +189,12 @@ def test_load_rejects_corrupt_checkpoints():
     bad = [patched(24, "<q", 0), patched(32, "<q", 0), patched(16, "<q", 1 << 41), patched(16, "<q", 100),
            patched(40, "<q", 17), patched(48, "<q", -1), patched(56, "<i", 7), patched(64, "<i", 1),
            patched(72, "<q", -1), patched(80, "<d", 0.0), patched(80, "<d", float("nan")),
-           patched(88, "<q", 1 << 60), patched(88, "<q", 0), patched(88, "<q", 3),
-           patched(96, "<q", 17),                      # current w no longer sums to C
-           patched(96 + 8 * 4, "<q", -1),              # a history vector with a negative entry
-           patched(len(good) - 8, "<d", -1.0),         # a non-positive EMA time
+           patched(88, "<i", 7), patched(92, "<i", 1), patched(92, "<i", 65), patched(60, "<i", 0),
+           patched(96, "<q", 1 << 60), patched(96, "<q", 0), patched(96, "<q", 3),
+           patched(104, "<q", 17),                     # current w no longer sums to C
+           patched(104 + 8 * 4, "<q", -1),             # a history vector with a negative entry
+           patched(len(good) - 40, "<d", -1.0),        # a non-positive EMA time (t_prev)
+           patched(len(good) - 8, "<d", float("nan")), # a non-finite recorded t (t_hist)
            bytes(good[:-1]), bytes(good) + b"\0"]
     for b in bad:
         with pytest.raises(pr.PropringError):
@@ -222,3 +225,56 @@ def test_header_is_plain_c():
     hdr = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "propring.h")
     r = subprocess.run([cc, "-fsyntax-only", "-std=c99", "-Wall", "-Werror", "-x", "c", hdr], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_affine_model_trajectories_bit_exact():
+    """PR_ALLOC_MODEL_AFFINE (DESIGN.md §3 #49): 2,000 random controller trajectories — affine, linear and
+    noisy step costs, ties, zero-timing rejections, checkpoint/restore mid-run — give the same integers,
+    history and frozen flag as the oracle's definition."""
+    rng = np.random.Generator(np.random.PCG64(4949))
+    for case in range(2000):
+        P = int(rng.integers(1, 9))
+        floor = int(rng.integers(1, 3))
+        C = int(rng.integers(P * floor, 6 * P + 40))
+        g = int(rng.integers(1, 5))
+        N = g * C * int(rng.integers(1, 20))
+        window = int(rng.integers(2, 4))
+        fit_window = int(rng.integers(2, 10))
+        never = bool(rng.integers(0, 2))
+        o = A.alloc_init(N, [1.0] * P, C=C, g=g, floor=floor)
+        o.model, o.fit_window, o.window, o.never_freeze = "affine", fit_window, window, never
+        l = pr.alloc_init(N, [1.0] * P, C=C, g=g, floor=floor)
+        l.set_policy(window=window, never_freeze=never, model=pr.ALLOC_MODEL_AFFINE, fit_window=fit_window)
+        fixed = rng.uniform(0.0, 3.0, P) * rng.integers(0, 2)
+        per = rng.uniform(0.05, 2.0, P)
+        for ep in range(8):
+            kind = int(rng.integers(0, 5))
+            w = np.array(o.w, dtype=float)
+            if kind == 0:
+                t = fixed + per * w                                   # affine, noise-free
+            elif kind == 1:
+                t = (fixed + per * w) * rng.uniform(0.9, 1.1, P)      # noisy (fits may fall back)
+            elif kind == 2:
+                t = per * w                                           # linear (the paper's model)
+            elif kind == 3:
+                t = np.full(P, 1.5)                                   # ties
+            else:
+                t = rng.uniform(0.1, 5.0, P)
+                if ep % 3 == 0:
+                    t[int(rng.integers(0, P))] = [0.0, float("nan")][ep % 2]
+            try:
+                ch_o = A.alloc_update(o, list(t))
+                err = None
+            except A.ZeroTiming:
+                err = pr.PR_ERR_ZERO_TIMING
+            if err is None:
+                assert l.update(list(t)) == ch_o
+            else:
+                with pytest.raises(pr.PropringError) as e:
+                    l.update(list(t))
+                assert e.value.code == err
+            v = l.view()
+            assert v["w"] == o.w and v["frozen"] == o.frozen and v["hist_len"] == len(o.history), (case, ep)
+            if ep == 4:                                               # checkpoint / restore mid-trajectory
+                l = pr.Alloc.load(l.save())
+                assert l.view() == v

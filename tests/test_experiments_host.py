@@ -76,3 +76,24 @@ def test_fit_affine():
     a, b = E.fit_affine([64, 128, 256], [1.3e-3 + 1.5e-6 * n for n in (64, 128, 256)])
     assert abs(a - 1.3e-3) < 1e-12 and abs(b - 1.5e-6) < 1e-15
     assert E.fit_affine([100], [2.0]) == (2.0, 0.0)
+
+
+def test_make_policy_from_command_line():
+    """--model affine / --ema / --never-freeze each reach Alloc.set_policy, alone or together (the EMA is no
+    longer dropped when the stop rule stays on)."""
+    import argparse
+
+    import paper_2111_08272_b200 as pr
+
+    def ns(**kw):
+        d = dict(never_freeze=False, scenario="c4", ema=1.0, model="proportional")
+        d.update(kw)
+        return argparse.Namespace(**d)
+
+    assert E.make_policy(ns()) is None
+    assert E.make_policy(ns(ema=0.5)) == {"ema_alpha": 0.5}
+    assert E.make_policy(ns(model="affine")) == {"model": pr.ALLOC_MODEL_AFFINE}
+    assert E.make_policy(ns(never_freeze=True, model="affine")) == {"never_freeze": True, "model": pr.ALLOC_MODEL_AFFINE}
+    assert E.make_policy(ns(scenario="n3-swap")) == {"never_freeze": True}
+    a = pr.alloc_init(50_000, [1] * 8, C=64, g=16)
+    a.set_policy(**E.make_policy(ns(model="affine", ema=0.7)))

@@ -111,6 +111,14 @@ def test_vgg16_size_C3_full_parity():
     _check(P, 138_357_544, "f32", [16 * w for w in (11, 11, 21, 21)], comms)
 
 
+def test_c5_maximum_size_1GiB():
+    """C5's largest buffer (2^30 B per rank, fp32) at P = 2 with C5's skewed weights [1,3]·256, and bf16
+    256 MiB per rank (2^27 elements) at P = 4 [1,1,2,4]·256 — ring replay on every element + the fp64
+    tolerance, mixed-scale inputs."""
+    _check(2, 2 ** 28, "f32", [256, 768], group(2), kind="mixed", seed=30)
+    _check(4, 2 ** 27, "bf16", [256, 256, 512, 1024], group(4), kind="mixed", seed=31)
+
+
 def test_resnet18_size_bf16_P8():
     """C5's bf16 leg at the ResNet-18 size, skewed weights 1:1:1:1:2:2:4:4."""
     P = 8

@@ -247,3 +247,91 @@ def test_ema_smoothing_definition():
     A.alloc_update(a, [1.0, 1.0])
     A.alloc_update(a, [3.0, 1.0])
     assert a.t_prev == [0.5 * 3.0 + 0.5 * 1.0, 1.0]
+
+
+# ---- affine step-cost model (DESIGN.md §3 #49; opt-in extension, not the paper's Eq. 10) -------------
+
+def _brute_minmax(models, C, floor):
+    """Every composition of C into len(models) parts >= floor: the smallest achievable max cost."""
+    import itertools
+
+    P = len(models)
+    best = None
+    for w in itertools.product(range(floor, C - floor * (P - 1) + 1), repeat=P):
+        if sum(w) != C:
+            continue
+        m = max(a + b * float(x) for (a, b), x in zip(models, w))
+        best = m if best is None or m < best else best
+    return best
+
+
+def test_minmax_greedy_is_the_brute_force_optimum():
+    """Pin of the greedy: for increasing affine costs its max equals the exhaustive min-max (P <= 4,
+    C <= 12, floor 1 or 2), and the result is a valid allocation."""
+    rng = np.random.Generator(np.random.PCG64(49))
+    for case in range(400):
+        P = int(rng.integers(1, 5))
+        floor = int(rng.integers(1, 3))
+        C = int(rng.integers(P * floor, 13))
+        models = [(float(rng.choice([0.0, rng.uniform(0, 3)])), float(rng.uniform(0.1, 4))) for _ in range(P)]
+        w = A.minmax_greedy(models, C, floor)
+        assert sum(w) == C and min(w) >= floor
+        got = max(a + b * float(x) for (a, b), x in zip(models, w))
+        assert got == _brute_minmax(models, C, floor), (models, C, floor, w)
+
+
+def test_affine_fit_recovers_exact_lines_and_matches_polyfit():
+    """Pin of the least-squares fit: noise-free t = a + b·w is recovered to rounding; noisy data agree with
+    numpy.polyfit (library routine) to 1e-9; one distinct w -> None; a falling line -> the proportional
+    fallback through the latest point."""
+    rng = np.random.Generator(np.random.PCG64(7))
+    for _ in range(200):
+        a, b = float(rng.uniform(0, 5)), float(rng.uniform(0.01, 3))
+        ws = [int(x) for x in rng.integers(1, 40, int(rng.integers(2, 9)))]
+        if len(set(ws)) < 2:
+            ws.append(ws[0] + 1)
+        fa, fb = A.affine_fit(ws, [a + b * w for w in ws])
+        assert abs(fa - a) <= 1e-9 * (1 + a) and abs(fb - b) <= 1e-9 * b
+        ts = [a + b * w + float(rng.normal(0, 0.01)) for w in ws]
+        f = A.affine_fit(ws, ts)
+        pb, pa = np.polyfit(np.array(ws, float), np.array(ts), 1)
+        if pb > 0 and pa >= 0:
+            assert abs(f[0] - pa) <= 1e-9 * (1 + abs(pa)) and abs(f[1] - pb) <= 1e-9 * (1 + abs(pb))
+        else:
+            assert f == (0.0, ts[-1] / ws[-1])
+    assert A.affine_fit([4, 4, 4], [1.0, 1.1, 0.9]) is None
+    assert A.affine_fit([2, 4], [3.0, 1.0]) == (0.0, 1.0 / 4)
+
+
+def test_affine_model_first_update_is_eq10_and_second_reaches_the_optimum():
+    """From a uniform start no rank has two distinct w, so the first update IS Eq. 10 + Hamilton; with
+    noise-free affine costs the second update (two observations per rank) lands on the exact min-max
+    allocation of the true costs (brute force over P = 3, C = 12), and the stop rule then freezes it."""
+    cost = [(2.0, 0.5), (2.0, 1.0), (2.0, 2.0)]                  # fixed cost 2, speeds 4:2:1
+
+    def times(w):
+        return [a + b * float(x) for (a, b), x in zip(cost, w)]
+
+    a = A.alloc_init(10_000, [1, 1, 1], C=12, g=1)
+    e = A.alloc_init(10_000, [1, 1, 1], C=12, g=1)
+    a.model = "affine"
+    A.alloc_update(a, times(a.w))
+    A.alloc_update(e, times(e.w))
+    assert a.w == e.w
+    A.alloc_update(a, times(a.w))
+    assert max(times(a.w)) == _brute_minmax(cost, 12, 1)
+    A.alloc_update(a, times(a.w))
+    A.alloc_update(a, times(a.w))
+    assert a.frozen
+
+
+def test_affine_model_on_linear_costs_is_eq8_up_to_rounding():
+    """Linear costs (a = 0, the paper's model, Eq. 6-8): the affine model's allocation is the min-max of
+    b_i·w_i, i.e. w ∝ v_i = 1/b_i (Eq. 8) to within one unit per rank."""
+    b = [1.0, 1.0, 2.0, 4.0]                                      # speeds 4:4:2:1 -> 16:16:8:4 of C = 44
+    a = A.alloc_init(10_000, [1, 1, 1, 1], C=44, g=1)
+    a.model = "affine"
+    a.never_freeze = True
+    for _ in range(4):
+        A.alloc_update(a, [bi * float(w) for bi, w in zip(b, a.w)])
+    assert all(abs(x - y) <= 1 for x, y in zip(a.w, [16, 16, 8, 4]))
