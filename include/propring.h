@@ -223,6 +223,8 @@ typedef struct pr_comm pr_comm;
 #define PR_COMM_FLAG_FORCE_STAGED 1   /* all-gather through staging even when buffers are registered */
 #define PR_COMM_FLAG_BULK_STORE   4   /* ring data path: results pushed with TMA bulk stores (one thread,
                                          * whole tiles) instead of 16-byte stores from every consumer lane */
+#define PR_COMM_FLAG_L2_PREFETCH  8   /* ring data path: each slice's own-gradient range is prefetched into
+                                         * L2 (cp.async.bulk.prefetch.L2) before the slice's flag waits */
 #define PR_COMM_FLAG_SYS_SCOPE    2   /* system-scope release/acquire even when every rank shares one GPU
                                          (by default .gpu scope is used exactly when that is the case) */
 

@@ -81,7 +81,7 @@ static_assert(sizeof(ChanState) == 128, "state");
 struct DevTable {
     int32_t rank, P, channels, slots;
     int32_t stages, tile_bytes;     // TMA pipeline: depth, bytes per input per stage
-    int32_t sysscope, pad0;         // 1: some peer is another GPU (use .sys release/acquire)
+    int32_t sysscope, l2pf;         // 1: some peer is another GPU (use .sys release/acquire); 1: L2 prefetch of g
     int64_t slot_bytes;
     int64_t watchdog_ns;
     uint64_t off_flags, off_hs, off_state, off_ag, off_staging, window_bytes;
@@ -295,6 +295,10 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 // generic-proxy writes (peer stores observed through an acquire) -> visible to the async proxy (TMA)
+// cp.async.bulk.prefetch.L2: bring [p, p+bytes) into L2 ahead of the TMA loads (16-byte aligned and sized)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 // this thread's st.shared writes -> visible to a later bulk store's (async proxy) reads of shared memory
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -721,6 +725,13 @@ __global__ void __launch_bounds__(576, 1) ring_kernel(const __grid_constant__ La
             for_each_step(P, r, nsl, G, [&](int kind, int c, int64_t i) {
                 int64_t lo, len;
                 range(c, i, lo, len);
+                if (tab->l2pf && !bad && needs_g(kind)) {
+                    // PR_COMM_FLAG_L2_PREFETCH: the own gradient of this slice does not depend on any peer;
+                    // start pulling it into L2 before the flag waits so the tiles' TMA loads hit L2
+                    const uint8_t* p0 = reinterpret_cast<const uint8_t*>(buf + lo);
+                    const int64_t bytes = (len * (int64_t)sizeof(T)) & ~15ll;
+                    for (int64_t o = 0; o < bytes; o += 65536) prefetch_l2(p0 + o, (uint32_t)min((int64_t)65536, bytes - o));
+                }
                 if (!bad) {
                     bool ok = true;
                     if (reads_slot(kind)) ok = wait_ge(&myf->rs_ready, consJ + 1, deadline, sys);
@@ -1686,7 +1697,8 @@ void resolve_config(pr_comm_config& c, bool cross_gpu) {
 }
 
 int check_config(const pr_comm_config& c) {
-    if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE | PR_COMM_FLAG_BULK_STORE)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
+    if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE | PR_COMM_FLAG_BULK_STORE |
+                     PR_COMM_FLAG_L2_PREFETCH)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
         (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_NVLS ||
@@ -2152,6 +2164,7 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
         c->tab.win[q] = (uint8_t*)p;
     }
     c->tab.sysscope = (c->cfg.flags & PR_COMM_FLAG_SYS_SCOPE) ? 1 : 0;
+    c->tab.l2pf = (c->cfg.flags & PR_COMM_FLAG_L2_PREFETCH) ? 1 : 0;
     for (int q = 0; q < P; ++q)
         if (std::memcmp(all[q].uuid, me.uuid, 16) != 0) c->tab.sysscope = 1;   // a peer on another GPU
     if (!rc) rc = push_table(c);
@@ -2185,6 +2198,7 @@ extern "C" int pr_comm_init_local(pr_comm** out, int32_t P, int32_t device, cons
                 cs[r]->tab.reg[0][q] = nullptr;   // local region 0: the whole address space, base 0
             }
             cs[r]->tab.sysscope = (cf.flags & PR_COMM_FLAG_SYS_SCOPE) ? 1 : 0;   // one device: .gpu suffices
+            cs[r]->tab.l2pf = (cf.flags & PR_COMM_FLAG_L2_PREFETCH) ? 1 : 0;
             if ((rc = push_table(cs[r]))) break;
         }
     }

@@ -731,3 +731,14 @@ def test_nvls_kernel_emulated_within_tolerance(P):
         err, zb = W.error_metric(outs[0].astype(np.float64), ref, den)
         assert zb == 0 and err <= TOL["f32"], (L, err)
     _check(P, 4099, "bf16", [1 + r for r in range(P)], comms, seed=9)         # bf16: the ring's bits
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_l2_prefetch_ring_bit_identical_to_ring_replay(P):
+    """PR_COMM_FLAG_L2_PREFETCH only adds cp.async.bulk.prefetch.L2 hints: same bits as the ring replay, fp32
+    and bf16, direct and staged."""
+    for staged in (False, True):
+        comms = group(P, l2_prefetch=True, force_staged=staged, channels=4, slot_bytes=1 << 16)
+        for L in (1, 7, 4099, 2 ** 20 + 3):
+            for dtype in ("f32", "bf16"):
+                _check(P, L, dtype, [16 * (r + 1) for r in range(P)], comms, kind="mixed", seed=L + P)

@@ -1,5 +1,9 @@
-"""A/B of the ring's TMA bulk-store data path (PR_COMM_FLAG_BULK_STORE) against the 16-byte-STG path, same
-call, same box, alternating:
+"""A/B of a ring data-path option against the default, same call, same box, alternating:
+
+    python tools/ab_bulk.py [bulk_store|l2_prefetch]
+
+bulk_store (PR_COMM_FLAG_BULK_STORE): TMA bulk stores instead of 16-byte STGs; l2_prefetch
+(PR_COMM_FLAG_L2_PREFETCH): each slice's own gradient prefetched into L2 before the flag waits.  Measures:
   (a) per-rank CTA throughput, P = 2 co-located (HBM far from saturated: each channel CTA's own data path is
       the limit, the regime of a multi-GPU rank), 256 MiB fp32, 16 / 32 channels, 1 MiB slots, .gpu / .sys;
   (b) P = 8 co-located at the ResNet-18 gradient size (HBM-bound proxy), plain ring and fused a6-a9.
@@ -29,6 +33,7 @@ def timed(fn, reps=5, warm=2):
 
 
 def main():
+    opt = sys.argv[1] if len(sys.argv) > 1 else "bulk_store"
     L2 = (256 << 20) // 4
     x2 = [torch.randn(L2, device="cuda") for _ in range(2)]
     L8 = 11_689_512
@@ -39,18 +44,18 @@ def main():
         for bulk in (False, True):
             for ch, sysv in ((16, False), (32, False), (32, True)):
                 cs = pr.comm_init_local(2, 0, pr.comm_config(channels=ch, slot_bytes=1 << 20, sys_scope=sysv,
-                                                             bulk_store=bulk))
+                                                             **{opt: bulk}))
                 us = timed(lambda: pr.weighted_allreduce_local(cs, x2, [1, 2]))
                 bus = L2 * 4 / (us * 1e-6) / 1e9
-                print(json.dumps({"rep": rep, "test": "P2_cta", "bulk": bulk, "channels": ch, "sys": sysv,
+                print(json.dumps({"rep": rep, "test": "P2_cta", opt: bulk, "channels": ch, "sys": sysv,
                                   "us": round(us, 1), "busbw_equiv_GBs": round(bus, 1),
                                   "per_channel_GBs": round(bus / ch, 2)}), flush=True)
                 for c in cs:
                     c.destroy()
-            cs = pr.comm_init_local(8, 0, pr.comm_config(bulk_store=bulk))
+            cs = pr.comm_init_local(8, 0, pr.comm_config(**{opt: bulk}))
             us = timed(lambda: pr.weighted_allreduce_local(cs, g8, n8), reps=20)
             uf = timed(lambda: pr.weighted_allreduce_sgd_local(cs, g8, t8, n8, 1e-6, 0.0, zero_grad=False), reps=20)
-            print(json.dumps({"rep": rep, "test": "P8_resnet18", "bulk": bulk, "ring_us": round(us, 1),
+            print(json.dumps({"rep": rep, "test": "P8_resnet18", opt: bulk, "ring_us": round(us, 1),
                               "fused_us": round(uf, 1)}), flush=True)
             for c in cs:
                 c.destroy()

@@ -32,8 +32,10 @@ def main():
         nsrc = X.shape[0]
         idx = np.arange(n) % nsrc
         dX, didx = torch.from_numpy(np.ascontiguousarray(X)).cuda(), torch.from_numpy(idx).cuda()
-        for impl in (pr.GATHER_IMPL_LSU, pr.GATHER_IMPL_TMA):
+        for impl in (pr.GATHER_IMPL_LSU, pr.GATHER_IMPL_TMA, pr.GATHER_IMPL_BULK):
             for layout, lname in ((pr.GATHER_LAYOUT_CHW, "chw"), (pr.GATHER_LAYOUT_HWC, "hwc")):
+                if impl == pr.GATHER_IMPL_BULK and layout == pr.GATHER_LAYOUT_CHW:
+                    continue                                  # channels-last only
                 o = torch.empty((n, row_bytes), dtype=torch.bfloat16, device="cuda")
                 op = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE, [0.02] * 3, [100.0] * 3, plane, impl=impl,
                                        layout=layout)
@@ -49,6 +51,18 @@ def main():
     pr.gather_rows(torch.from_numpy(X).cuda(), 256, 3072, torch.from_numpy(idx).cuda(), 8192, o, op)
     ref, _ = OG.gather_rows(X, idx, OG.U8_TO_BF16_AFFINE, np.float32([0.02] * 3), np.float32([100.0] * 3), 1024)
     assert np.array_equal(o.view(torch.int16).cpu().numpy().view(np.uint16), ref)
+    # K2 bulk-store kernel with smem-tile reuse (2,048 units over at most 592 CTAs: every CTA rewrites both
+    # tiles behind cp.async.bulk.wait_group.read) and labels
+    Y = np.arange(256, dtype=np.int64) * 3
+    lab = torch.empty(8192, dtype=torch.int64, device="cuda")
+    op = pr.make_gather_op(pr.GATHER_U8_TO_BF16_AFFINE, [0.02] * 3, [100.0] * 3, 1024, impl=pr.GATHER_IMPL_BULK,
+                           layout=pr.GATHER_LAYOUT_HWC)
+    pr.gather_rows(torch.from_numpy(X).cuda(), 256, 3072, torch.from_numpy(idx).cuda(), 8192, o, op,
+                   torch.from_numpy(Y).cuda(), lab)
+    ref, rlab = OG.gather_rows(X, idx, OG.U8_TO_BF16_AFFINE, np.float32([0.02] * 3), np.float32([100.0] * 3), 1024,
+                               Y=Y, layout="hwc")
+    assert np.array_equal(o.view(torch.int16).cpu().numpy().view(np.uint16), ref)
+    assert np.array_equal(lab.cpu().numpy(), rlab)
     # K4
     pr.spin(10_000)
     # K3: local groups, both scopes, direct and staged, ragged counts
