@@ -750,11 +750,13 @@ extern "C" int pr_gather_rows(const void* d_src, int64_t n_src, int64_t row_byte
     if (blocks > resident_n) blocks = resident_n;
     if (host_src) {
         // rows read over PCIe: a few CTAs keep enough loads in flight for the link, and the rest of the GPU
-        // stays free for the compute this gather runs beside (the trainer prefetches on a side stream)
+        // stays free for the compute this gather runs beside (the trainer prefetches on a side stream).
+        // Bench e2e, ResNet-18 leg (profiles/round2_e2e_host_grid_ab.jsonl): 16 / 32 CTAs 368-370k samples/s,
+        // 64 364-366k, 128 364-365k.
         static const int host_grid = [] {
             const char* e = getenv("PR_GATHER_HOST_GRID");
-            const int v = e ? atoi(e) : 64;
-            return v < 1 ? 64 : v;
+            const int v = e ? atoi(e) : 32;
+            return v < 1 ? 32 : v;
         }();
         if (blocks > host_grid) blocks = host_grid;
     }

@@ -89,7 +89,7 @@ def run_colocated(P, max_mib, reps, algo=0):
         c.destroy()
 
 
-def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0, bulk=False):
+def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0, bulk=False, l2pf=False):
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -103,7 +103,7 @@ def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0, bulk=False):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, P = dist.get_rank(), dist.get_world_size()
     comm = pr.comm_init(rank, P, local, config=pr.comm_config(algo=algo, channels=channels, min_slice_bytes=min_slice,
-                                                              bulk_store=bulk))
+                                                              bulk_store=bulk, l2_prefetch=l2pf))
     n = weights(P)
     s = n[rank] / sum(n)
     Zmax = max_mib << 20
@@ -168,8 +168,9 @@ if __name__ == "__main__":
     ap.add_argument("--channels", type=int, default=0, help="CTAs per rank (multi-GPU mode; 0 = topology default)")
     ap.add_argument("--min-slice", type=int, default=0, help="ring min_slice_bytes (0 = slot-sized slices)")
     ap.add_argument("--bulk", action="store_true", help="ring data path with TMA bulk stores")
+    ap.add_argument("--l2pf", action="store_true", help="ring: L2 prefetch of each slice's own gradient")
     a = ap.parse_args()
     if a.colocated:
         run_colocated(a.colocated, a.max_mib, a.reps, a.algo)
     else:
-        run_multi(a.max_mib, a.reps, a.algo, a.channels, a.min_slice, a.bulk)
+        run_multi(a.max_mib, a.reps, a.algo, a.channels, a.min_slice, a.bulk, a.l2pf)

@@ -20,6 +20,9 @@ for P in 2 4 8; do
   # TMA bulk-store data path vs 16-byte STG over real NVLink (co-located proxy: 5-8 % slower)
   timeout 900 $TR --nproc-per-node $P --master-port $((29670 + P)) tools/ar_sweep.py --max-mib 256 --bulk \
       > gpurun_out/mg_ar_sweep_bulk_p$P.jsonl 2> gpurun_out/mg_ar_sweep_bulk_p$P.err
+  # L2 prefetch of the own gradient before the flag waits (co-located proxy: 13 % slower per channel)
+  timeout 900 $TR --nproc-per-node $P --master-port $((29690 + P)) tools/ar_sweep.py --max-mib 256 --l2pf \
+      > gpurun_out/mg_ar_sweep_l2pf_p$P.jsonl 2> gpurun_out/mg_ar_sweep_l2pf_p$P.err
   # NVLS (in-switch reduction), where the box can create a multicast object
   timeout 900 $TR --nproc-per-node $P --master-port $((29680 + P)) tools/ar_sweep.py --max-mib 1024 --algo 5 \
       > gpurun_out/mg_ar_sweep_nvls_p$P.jsonl 2> gpurun_out/mg_ar_sweep_nvls_p$P.err
@@ -40,6 +43,8 @@ timeout 1200 $TR --nproc-per-node $G --master-port 29630 tools/ar_sweep.py --max
 # emulated heterogeneity one rank per GPU (C4 scenarios need 8)
 [ $G -ge 8 ] && timeout 1800 $TR --nproc-per-node 8 --master-port 29640 experiments.py --scenario c4 \
     > gpurun_out/mg_c4.jsonl 2> gpurun_out/mg_c4.err
+[ $G -ge 8 ] && timeout 1800 $TR --nproc-per-node 8 --master-port 29642 experiments.py --scenario c4 --spin sample \
+    --model affine > gpurun_out/mg_c4_affine.jsonl 2> gpurun_out/mg_c4_affine.err
 [ $G -ge 4 ] && timeout 1800 $TR --nproc-per-node 4 --master-port 29641 experiments.py --scenario c3 \
     > gpurun_out/mg_c3.jsonl 2> gpurun_out/mg_c3.err
 ls -la gpurun_out/mg_*
