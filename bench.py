@@ -553,6 +553,29 @@ def colocated_allreduce(hbm, peak_kind, P=8, reps=20):
     # algorithmic HBM bytes of one call, all P ranks (direct all-gather): per rank
     # hop0 2·Z/P, P−2 middle hops 3·Z/P, last hop 4·Z/P, P−2 forwards 2·Z/P  => (6 + 5(P−2))·Z/P
     byts = P * (6 + 5 * (P - 2)) * Z / P
+    # C3's VGG-16 gradient (553 MB per rank, the >= 64 MB regime of the north-star target) at P = 4 with the
+    # allocation C3 converges to (n = 16·[11,11,21,21]): same proxy, same byte count formula
+    del bufs
+    P3, L3 = 4, L_VGG16
+    c3 = pr.comm_init_local(P3, torch.cuda.current_device(), pr.comm_config())
+    b3 = [torch.randn(L3, device="cuda") for _ in range(P3)]
+    n3 = [16 * w for w in (11, 11, 21, 21)]
+    for _ in range(2):
+        pr.weighted_allreduce_local(c3, b3, n3)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(5):
+        pr.weighted_allreduce_local(c3, b3, n3)
+    b.record()
+    torch.cuda.synchronize()
+    t3 = a.elapsed_time(b) / 5
+    byts3 = P3 * (6 + 5 * (P3 - 2)) * (L3 * 4) / P3
+    vgg = {"P": P3, "bytes_per_rank": L3 * 4, "n_local": n3, "avg_us": t3 * 1e3,
+           "achieved": byts3 / (t3 * 1e-3) / 1e9, "frac": byts3 / (t3 * 1e-3) / 1e9 / hbm,
+           "algorithmic_bytes_per_call": byts3}
+    del b3
+    for c in c3:
+        c.destroy()
     store = [torch.randn(2 * L, device="cuda") for _ in range(P)]
     grads, thetas = [x[:L] for x in store], [x[L:] for x in store]
 
@@ -575,7 +598,7 @@ def colocated_allreduce(hbm, peak_kind, P=8, reps=20):
 
     fused_us = timed(lambda: pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 1e-6, 0.0, zero_grad=True))
     composed_us = timed(composed)
-    del bufs, store, grads, thetas
+    del store, grads, thetas
     for c in comms:
         c.destroy()
     # C1 (BASELINE configs[0]): the logistic-regression gradient (1,024 fp32 = 4 KiB), 2 ranks, n = [25, 75];
@@ -623,7 +646,7 @@ def colocated_allreduce(hbm, peak_kind, P=8, reps=20):
         c.destroy()
     return {"kernel": "ring_kernel<float> (K3), all ranks on one GPU", "P": P, "bytes_per_rank": Z,
             "fused_a6_a9_us": fused_us, "composed_a6_a9_us": composed_us,
-            "c1_allreduce_4KiB_P2_us": c1_us,
+            "c1_allreduce_4KiB_P2_us": c1_us, "vgg16_C3_P4": vgg,
             "cross_gpu_config_per_rank_busbw_equiv": {
                 "GBs": per_rank_bus, "us": x_us, "bytes": Lx * 4, "P": 2, "channels": 32,
                 "vs_nvlink_770": per_rank_bus / NVLINK_PEER_GBS,
