@@ -232,7 +232,7 @@ typedef struct pr_comm pr_comm;
  * groups, co-located processes) -> the HBM-bound optimum; on different GPUs -> more channels with larger
  * tiles and slots, since each rank then has only its own channels' SMs. */
 typedef struct {
-    int32_t channels;     /* ring channels = CTAs per rank (topology: 16 one GPU / 32 across GPUs)    */
+    int32_t channels;     /* ring channels = CTAs per rank (topology: 128/P, <= 64, one GPU / 32 across) */
     int32_t slots;        /* staging slots per channel, >= 2 (default 8)                    */
     int32_t threads;      /* consumer threads per CTA, <= 512 (default 512)                                         */
     int32_t flags;        /* PR_COMM_FLAG_* (default 0)                                                */

@@ -1688,9 +1688,12 @@ pr_comm_config default_config() {
 // channels' SMs, and a channel CTA moves ≈ 22-27 GB/s of bus bandwidth (its SM↔L2 traffic is ≈ 3.5
 // bytes per bus byte; tools/sweep_cta.py, P = 2 co-located with HBM far from saturated), so 770 GB/s per
 // direction needs > 30 of them: 32 channels of 6 × 16 KiB stages and 1 MiB slots (≈ 860 GB/s
-// bus-equivalent per rank in that proxy).
-void resolve_config(pr_comm_config& c, bool cross_gpu) {
-    if (c.channels == 0) c.channels = cross_gpu ? 32 : 16;
+// bus-equivalent per rank in that proxy).  Same GPU with fewer than 8 ranks: the 16-channel
+// optimum was found at P = 8, where 128 CTAs saturate HBM; at P = 4 the same 16 channels per rank (64 CTAs)
+// left the VGG-16 gradient CTA-bound (0.76 of HBM), so a co-located group keeps ≈ 128 CTAs in total:
+// 128 / P channels per rank (at most 64) — which also keeps P > 8 groups co-resident (one CTA per SM).
+void resolve_config(pr_comm_config& c, bool cross_gpu, int P) {
+    if (c.channels == 0) c.channels = cross_gpu ? 32 : std::max(1, std::min(64, 128 / std::max(P, 1)));
     if (c.stages == 0) c.stages = 6;
     if (c.tile_bytes == 0) c.tile_bytes = 16384;
     if (c.slot_bytes == 0) c.slot_bytes = cross_gpu ? (1ll << 20) : (256 * 1024);
@@ -2115,7 +2118,7 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
     if (int xrc = exchange(c, &mine, sizeof(Probe), probes)) { free_comm(c); return xrc; }
     bool cross = false;
     for (int q = 0; q < P; ++q) cross = cross || std::memcmp(probes[q].uuid, mine.uuid, 16) != 0;
-    resolve_config(c->cfg, cross);
+    resolve_config(c->cfg, cross, P);
     int rc = check_config(c->cfg);
     if (!rc) rc = alloc_common(c);
     Hello me;
@@ -2181,7 +2184,7 @@ extern "C" int pr_comm_init(pr_comm** out, int32_t rank, int32_t P, int32_t devi
 extern "C" int pr_comm_init_local(pr_comm** out, int32_t P, int32_t device, const pr_comm_config* cfg) {
     if (!out || P < 1 || P > PR_MAX_RANKS || device < 0) return PR_ERR_INVALID;
     pr_comm_config cf = cfg ? *cfg : default_config();
-    resolve_config(cf, false);                                    // one device
+    resolve_config(cf, false, P);                                 // one device
     if (int rc = check_config(cf)) return rc;
     std::vector<pr_comm*> cs(P, nullptr);
     int rc = PR_OK;

@@ -88,8 +88,8 @@ def ring_fused(reps, P=8, L=11_689_512, only_fused=False):
         c.destroy()
 
 
-def ring(reps, P=8, L=11_689_512):
-    comms = pr.comm_init_local(P, 0, pr.comm_config())
+def ring(reps, P=8, L=11_689_512, **cfg):
+    comms = pr.comm_init_local(P, 0, pr.comm_config(**cfg))
     bufs = [torch.randn(L, device="cuda") for _ in range(P)]
     n = [64, 64, 64, 64, 128, 128, 256, 256][:P]
     us = timed(lambda: pr.weighted_allreduce_local(comms, bufs, n), reps)
@@ -134,6 +134,12 @@ if __name__ == "__main__":
         sgd(reps, L=138_357_544)
     if what == "gather_imagenet_epoch_hwc_lsu":        # the VGG-16 leg's launch kind (LSU, channels-last)
         gather(16384, 150528, 16384, reps, 50176, impls=(1,), layout=1)
+    if what == "ring_sizes":                            # default channels: P = 2 / 4 / 8 at the ResNet-18 and VGG-16 sizes
+        for P in (2, 4, 8):
+            for L in (11_689_512, 138_357_544):
+                ring(max(2, reps // (4 if L > 2e7 else 1)), P=P, L=L)
+    if what == "ring_cta":                              # the cross-GPU configuration, 2 ranks: per-channel CTA path
+        ring(reps, P=2, L=(256 << 20) // 4, channels=32, slot_bytes=1 << 20)
     if what in ("ring_fused", "all"):
         ring_fused(reps)
     if what == "ring_fused_only":
