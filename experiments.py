@@ -271,7 +271,10 @@ def run_virtual(args):
     wmax = C - (P - 1) * cfg.floor
     # --opt-stride k: time every k-th unit count (plus the ends and the final allocation's) and interpolate
     # linearly between them (VGG-16 captures cost seconds each); 1 = every unit count
-    meas = sorted(set(range(cfg.floor, wmax + 1, max(1, args.opt_stride))) | {wmax} | set(v["w"]) - {0})
+    # (0 = automatic: every unit count, but every 8th for VGG-16, whose 61 graph captures at every row count
+    # outgrew the shared CUDA-graph pool on one GPU)
+    stride = args.opt_stride if args.opt_stride > 0 else (8 if model == "vgg16" else 1)
+    meas = sorted(set(range(cfg.floor, wmax + 1, stride)) | {wmax} | set(v["w"]) - {0})
     t1m = {u: w.t1(g * u) for u in meas}
     t1tab = {}
     for u in range(cfg.floor, wmax + 1):
@@ -322,8 +325,9 @@ def main():
     ap.add_argument("--model", default="proportional", choices=["proportional", "affine"],
                     help="controller step-cost model: the paper's Eq. 10, or the affine extension (DESIGN §3 #49)")
     ap.add_argument("--metrics-csv", default="", help="append the per-(epoch, rank) metrics CSV (SURVEY §5) here")
-    ap.add_argument("--opt-stride", type=int, default=1,
-                    help="measured-cost bound: time t1 at every k-th unit count and interpolate (1 = all)")
+    ap.add_argument("--opt-stride", type=int, default=0,
+                    help="measured-cost bound: time t1 at every k-th unit count and interpolate (1 = all; "
+                         "0 = all, every 8th for VGG-16)")
     ap.add_argument("--spin", default="t1", choices=["t1", "sample"],
                     help="K4 emulation: t1 = (σ−1)·t1(n_r) per step; sample = (σ−1)·c0·n_r (SURVEY §8(a) a4)")
     args = ap.parse_args()
