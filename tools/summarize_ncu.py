@@ -96,7 +96,8 @@ def main():
                     "gather" if "gather" in kname else "sgd" if "sgd_kernel" in kname else
                     "ring_ll" if "ring_ll" in kname else
                     "ring_fused" if ("ring_kernel<float, 1" in kname or "ring_kernel<float, true" in kname) else
-                    "twoshot" if "twoshot" in kname else "ring_colocated" if "ring" in kname else
+                    "twoshot" if "twoshot" in kname else "ring_cta" if ("ring" in kname and "cta" in name) else
+                    "ring_colocated" if "ring" in kname else
                     "permute" if "permute" in kname else name)
             if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d:
                 traffic[kind] = {"dram_bytes_per_launch": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"],
