@@ -62,7 +62,7 @@ def main():
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) / 3 * 1e3
         bus = L * 4 * 2 * (P - 1) / P / (us * 1e-6) / 1e9
-        print(json.dumps({**cfg, "channels": a.channels, "sys": a.sys, "bulk": a.bulk, "us": round(us, 1),
+        print(json.dumps({**cfg, "P": P, "channels": a.channels, "sys": a.sys, "bulk": a.bulk, "us": round(us, 1),
                           "busbw_equiv_GBs": round(bus),
                           "per_channel_GBs": round(bus / a.channels, 1)}), flush=True)
         for c in comms:
