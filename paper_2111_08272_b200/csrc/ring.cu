@@ -1693,7 +1693,8 @@ pr_comm_config default_config() {
 // left the VGG-16 gradient CTA-bound (0.76 of HBM), so a co-located group keeps ≈ 128 CTAs in total:
 // 128 / P channels per rank (at most 64) — which also keeps P > 8 groups co-resident (one CTA per SM).
 void resolve_config(pr_comm_config& c, bool cross_gpu, int P) {
-    if (c.channels == 0) c.channels = cross_gpu ? 32 : std::max(1, std::min(64, 128 / std::max(P, 1)));
+    // (P = 1 runs no ring: keep the window small)
+    if (c.channels == 0) c.channels = cross_gpu ? 32 : (P <= 1 ? 16 : std::max(1, std::min(64, 128 / P)));
     if (c.stages == 0) c.stages = 6;
     if (c.tile_bytes == 0) c.tile_bytes = 16384;
     if (c.slot_bytes == 0) c.slot_bytes = cross_gpu ? (1ll << 20) : (256 * 1024);
