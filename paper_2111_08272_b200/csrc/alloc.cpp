@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstring>
 #include <new>
+#include <utility>
 #include <vector>
 
 #include "common.h"
@@ -173,18 +174,24 @@ bool affine_fit(const std::vector<const std::vector<int64_t>*>& ow, const std::v
 // floor and hand out the remaining units one at a time to the rank whose cost after taking it is the
 // smallest (ties -> lowest rank).  With increasing costs the k-th unit handed out is the k-th smallest
 // marginal cost, so the final maximum is the minimum possible (greedy is exact for min-max).
+// A binary heap keyed on (cost after the next unit, rank) gives the same choice as a scan for the smallest
+// cost with ties to the lowest rank, in O(C log P) (C may be 2^20).
 void minmax_greedy(const std::vector<double>& a, const std::vector<double>& b, int64_t C, int64_t floor,
                    std::vector<int64_t>& w) {
     const size_t P = a.size();
     w.assign(P, floor);
+    using Key = std::pair<double, size_t>;
+    std::vector<Key> heap;
+    heap.reserve(P);
+    for (size_t i = 0; i < P; ++i) heap.push_back({a[i] + b[i] * (double)(w[i] + 1), i});
+    auto after = [](const Key& x, const Key& y) { return x.first > y.first || (x.first == y.first && x.second > y.second); };
+    std::make_heap(heap.begin(), heap.end(), after);                   // top = smallest (cost, rank)
     for (int64_t left = C - (int64_t)P * floor; left > 0; --left) {
-        size_t best = 0;
-        double bc = 0.0;
-        for (size_t i = 0; i < P; ++i) {
-            const double c = a[i] + b[i] * (double)(w[i] + 1);
-            if (i == 0 || c < bc) { best = i; bc = c; }
-        }
-        w[best] += 1;
+        std::pop_heap(heap.begin(), heap.end(), after);
+        const size_t i = heap.back().second;
+        w[i] += 1;
+        heap.back() = {a[i] + b[i] * (double)(w[i] + 1), i};
+        std::push_heap(heap.begin(), heap.end(), after);
     }
 }
 
