@@ -267,16 +267,18 @@ def _torchrun(args, env_extra, timeout=900):
 
 
 @pytest.mark.gpu
-def test_experiments_multiprocess_path_two_ranks(tmp_path):
+@pytest.mark.parametrize("model", ["proportional", "affine"])
+def test_experiments_multiprocess_path_two_ranks(tmp_path, model):
     """experiments.py's one-rank-per-process path — real barrier inside K3, measured t_w, the K6 t_s allgather,
-    the replicated controller — with 2 processes sharing the test GPU (PR_BENCH_SHARED_GPU=1: functional only,
-    the ranks time-share one GPU), plus the per-(epoch, rank) metrics CSV of SURVEY §5."""
+    the replicated controller (the paper's Eq. 10 and the affine step-cost model) — with 2 processes sharing
+    the test GPU (PR_BENCH_SHARED_GPU=1: functional only, the ranks time-share one GPU), plus the per-(epoch,
+    rank) metrics CSV of SURVEY §5."""
     import json
 
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     csv = tmp_path / "m.csv"
-    r = _torchrun(["experiments.py", "--scenario", "c2-5x", "--epochs", "3", "--N", "8192",
+    r = _torchrun(["experiments.py", "--scenario", "c2-5x", "--epochs", "3", "--N", "8192", "--model", model,
                    "--metrics-csv", str(csv)], {"PR_BENCH_SHARED_GPU": "1"})
     assert r.returncode == 0, r.stderr[-3000:]
     recs = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
