@@ -238,7 +238,7 @@ typedef struct {
     int32_t flags;        /* PR_COMM_FLAG_* (default 0)                                                */
     int64_t slot_bytes;   /* bytes per staging slot, multiple of 256 (topology: 256 KiB / 1 MiB)      */
     int64_t watchdog_ns;  /* spin-wait deadline per call (default 10 s); <= 0 disables               */
-    int32_t stages;       /* TMA smem pipeline depth per CTA, 2..16 (0: 6)                            */
+    int32_t stages;       /* TMA smem pipeline depth per CTA, 2..16, stages·2·tile <= 224 KiB (0: 7)    */
     int32_t tile_bytes;   /* bytes per input per pipeline stage, multiple of 16, <= 32768 (0: 16 KiB) */
     int32_t algo;         /* PR_ALGO_* (default PR_ALGO_RING)                                         */
     int32_t ts_slots;     /* two-shot staging slots per (channel, source), >= 2 (default 2)          */

@@ -271,8 +271,8 @@ def comm_config(channels=0, slots=8, threads=512, slot_bytes=0, watchdog_ns=10_0
                 ts_slot_bytes=256 * 1024, ts_max_bytes=4 << 20, ll_max_bytes=256 * 1024,
                 os_max_bytes=64 * 1024, min_slice_bytes=0, bulk_store=False, l2_prefetch=False):
     """K3 launch/pipeline configuration.  channels / slot_bytes / stages / tile_bytes = 0: chosen at init from
-    the topology (one GPU: 128/P channels (16 at P = 8, at most 64) / 256 KiB / 6 / 16 KiB, the co-located
-    optimum of tools/sweep_ring.py; ranks on different GPUs: 32 / 1 MiB / 6 / 16 KiB, from the per-channel
+    the topology (one GPU: 128/P channels (16 at P = 8, at most 64) / 256 KiB / 7 / 16 KiB, the co-located
+    optimum of tools/sweep_ring.py; ranks on different GPUs: 32 / 1 MiB / 7 / 16 KiB, from the per-channel
     throughput of tools/sweep_cta.py).
     sys_scope=True forces system-scope synchronisation even when all ranks share one GPU (tests).
     algo: ALGO_RING (the paper's ring), ALGO_LL (the ring with the low-latency line protocol, buffers up to

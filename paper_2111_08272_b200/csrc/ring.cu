@@ -1683,11 +1683,11 @@ pr_comm_config default_config() {
 }
 
 // Topology defaults for the fields a caller leaves 0 (channels, stages, tile_bytes, slot_bytes).  Same GPU
-// (co-located ranks share the HBM and the SMs): 16 channels of 6 × 16 KiB stages, 256 KiB slots — the
+// (co-located ranks share the HBM and the SMs): 16 channels of 7 × 16 KiB stages, 256 KiB slots — the
 // HBM-bound optimum of tools/sweep_ring.py.  Ranks on different GPUs: each rank has only its own
 // channels' SMs, and a channel CTA moves ≈ 22-27 GB/s of bus bandwidth (its SM↔L2 traffic is ≈ 3.5
 // bytes per bus byte; tools/sweep_cta.py, P = 2 co-located with HBM far from saturated), so 770 GB/s per
-// direction needs > 30 of them: 32 channels of 6 × 16 KiB stages and 1 MiB slots (≈ 860 GB/s
+// direction needs > 30 of them: 32 channels of 7 × 16 KiB stages and 1 MiB slots (≈ 860 GB/s
 // bus-equivalent per rank in that proxy).  Same GPU with fewer than 8 ranks: the 16-channel
 // optimum was found at P = 8, where 128 CTAs saturate HBM; at P = 4 the same 16 channels per rank (64 CTAs)
 // left the VGG-16 gradient CTA-bound (0.76 of HBM), so a co-located group keeps ≈ 128 CTAs in total:
@@ -1695,7 +1695,9 @@ pr_comm_config default_config() {
 void resolve_config(pr_comm_config& c, bool cross_gpu, int P) {
     // (P = 1 runs no ring: keep the window small)
     if (c.channels == 0) c.channels = cross_gpu ? 32 : (P <= 1 ? 16 : std::max(1, std::min(64, 128 / P)));
-    if (c.stages == 0) c.stages = 6;
+    // 7 × 2 × 16 KiB = 224 KiB of the 227 KB a CTA may use: the co-located P = 8 ResNet-18 ring 243 -> 234 µs
+    // against 6 stages (profiles/round2_k3_stages7.jsonl)
+    if (c.stages == 0) c.stages = 7;
     if (c.tile_bytes == 0) c.tile_bytes = 16384;
     if (c.slot_bytes == 0) c.slot_bytes = cross_gpu ? (1ll << 20) : (256 * 1024);
 }
@@ -1705,7 +1707,7 @@ int check_config(const pr_comm_config& c) {
                      PR_COMM_FLAG_L2_PREFETCH)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
-        (int64_t)c.stages * 2 * c.tile_bytes > 200 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_NVLS ||
+        (int64_t)c.stages * 2 * c.tile_bytes > 224 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_NVLS ||
         c.ll_max_bytes < 0 || c.ll_max_bytes > (64ll << 20) || c.os_max_bytes < 0 || c.os_max_bytes > (16ll << 20) ||
         c.min_slice_bytes < 0 || c.min_slice_bytes % 16 ||
         c.ts_slots < 2 || c.ts_slots > 16 || c.ts_slot_bytes < 256 || c.ts_slot_bytes % 256 ||

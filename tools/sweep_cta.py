@@ -43,7 +43,7 @@ def main():
     if a.cfg:
         cfgs = [json.loads(a.cfg)]
     for cfg in cfgs:
-        if cfg["stages"] * 2 * cfg["tile_bytes"] > 200 * 1024 or cfg["stages"] * cfg["tile_bytes"] < 32768:
+        if cfg["stages"] * 2 * cfg["tile_bytes"] > 224 * 1024 or cfg["stages"] * cfg["tile_bytes"] < 32768:
             continue
         try:
             comms = pr.comm_init_local(P, 0, pr.comm_config(channels=a.channels, sys_scope=a.sys, bulk_store=a.bulk,
