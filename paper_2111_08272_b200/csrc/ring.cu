@@ -2059,7 +2059,13 @@ extern "C" int pr_comm_nvls_alloc(pr_comm* c, size_t bytes, void** d_ptr) {
     }
     if (!rc) rc = nv_sync(c, me, all);
     if (c->rank == 0 && me.kind == 2 && me.fd >= 0) close(me.fd);   // every peer has duplicated it
-    // step 3: every rank adds its device, allocates and binds its memory, maps both aliases
+    // step 3: every rank adds its device to the team — all of them before anyone binds memory (a multicast
+    // object accepts bindings only once its team is complete) — then allocates and binds its memory and
+    // maps both aliases
+    if (!rc) {
+        if (d.mcAdd(mc, dev) != CUDA_SUCCESS) me.err = PR_ERR_UNSUPPORTED;
+        rc = nv_sync(c, me, all);
+    }
     CUdeviceptr uc = 0, mcp = 0;
     if (!rc) {
         CUmemAllocationProp ap;
@@ -2072,7 +2078,7 @@ extern "C" int pr_comm_nvls_alloc(pr_comm* c, size_t bytes, void** d_ptr) {
         acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
         acc.location.id = c->device;
         acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-        if (d.mcAdd(mc, dev) != CUDA_SUCCESS || d.memCreate(&mem, size, &ap, 0) != CUDA_SUCCESS ||
+        if (d.memCreate(&mem, size, &ap, 0) != CUDA_SUCCESS ||
             d.mcBind(mc, 0, mem, 0, size, 0) != CUDA_SUCCESS || d.addrReserve(&uc, size, gran, 0, 0) != CUDA_SUCCESS ||
             d.memMap(uc, size, 0, mem, 0) != CUDA_SUCCESS || d.setAccess(uc, size, &acc, 1) != CUDA_SUCCESS ||
             d.addrReserve(&mcp, size, gran, 0, 0) != CUDA_SUCCESS || d.memMap(mcp, size, 0, mc, 0) != CUDA_SUCCESS ||
