@@ -7,9 +7,11 @@
 // [0, N).  Shard r = π(off_r .. off_r + len_r − 1).
 //
 // Bound: integer ALU (≈4 Philox-10 evaluations per Feistel pass, ≈M/N passes per index); the only
-// memory traffic is the 8-byte index written per output.  One thread per output index,
-// grid = min(ceil(count/256), 148·8) with a grid-stride loop.
+// memory traffic is the 8-byte index written per output.  Default kernel: lane-refill
+// cycle walk, one contiguous range of outputs per warp (walk_refill_kernel below).
 #include <curand_philox4x32_x.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "common.h"
 
@@ -52,27 +54,109 @@ __device__ __forceinline__ uint64_t feistel(uint64_t x, const FeistelKey& fk) {
     return (L << fk.h) | R;
 }
 
-__global__ void __launch_bounds__(256) permute_kernel(uint64_t N, FeistelKey fk, uint64_t begin, uint64_t count,
-                                                      int64_t* __restrict__ out) {
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
-        uint64_t y = feistel(begin + t, fk);
-        while (y >= N) y = feistel(y, fk);  // cycle walking: terminates, π restricted to [0, N) is a bijection
-        out[t] = (int64_t)y;
-    }
-}
+constexpr int kRefillWarpsPerSM = 16;   // A/B at N = 1,281,167 (profiles/round2_k1_refill_ab.jsonl): 8 → 68.2 µs, 16 → 62.1, 24 → 63.0, 32 → 68.2, 64 → 78.8
 
-// Step-interleaved shard (N3): out[i] = π(s·B + o + t) with s = step0 + i / n, t = i mod n.
-__global__ void __launch_bounds__(256) shard_steps_kernel(uint64_t N, FeistelKey fk, uint64_t B, uint64_t o,
-                                                          uint64_t n, uint64_t step0, uint64_t count,
+// Index maps: output position i -> the Feistel input whose cycle-walked image is out[i].
+struct RangeMap {  // pr_permute / pr_shard_indices: π(begin + i)
+    uint64_t begin;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return begin + i; }
+};
+struct StepMap {   // pr_shard_steps (N3): π(s·B + o + t), s = step0 + i / n, t = i mod n
+    uint64_t B, o, n, step0;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+        const uint64_t q = i / n;
+        return (step0 + q) * B + o + (i - q * n);
+    }
+};
+
+// One thread per output index (round 1).  A warp runs as long as its longest cycle walk: with
+// p = N/M accepted draws the walk length is geometric(p), so at N = 1,281,167 (p = 0.305, mean 3.27
+// Feistel passes) the warp's maximum over 32 lanes is ≈ 3× the mean and two thirds of the issued
+// Feistel passes belong to lanes that have already finished.  Kept for the A/B (PR_K1_KERNEL=direct).
+template <class Map>
+__global__ void __launch_bounds__(256) walk_direct_kernel(uint64_t N, FeistelKey fk, Map map, uint64_t count,
                                                           int64_t* __restrict__ out) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-        const uint64_t s = step0 + i / n, t = i - (i / n) * n;
-        uint64_t y = feistel(s * B + o + t, fk);
-        while (y >= N) y = feistel(y, fk);
+        uint64_t y = feistel(map(i), fk);
+        while (y >= N) y = feistel(y, fk);  // cycle walking: terminates, π restricted to [0, N) is a bijection
         out[i] = (int64_t)y;
     }
+}
+
+// Lane-refill walk (round 2, default): each warp owns a contiguous range of output positions and every
+// lane carries one walk in flight.  Per iteration all lanes take one Feistel pass; a lane whose image
+// fell inside [0, N) stores it and takes the warp's next position (ballot + popc hands positions out in
+// lane order), the others keep walking.  Every issued pass is useful work until the warp's range runs
+// dry, so the issue cost per index is the mean walk (M/N passes), not the warp's maximum.  Same π, same
+// bits; only the order in which the outputs are written changes.
+template <class Map>
+__global__ void __launch_bounds__(256) walk_refill_kernel(uint64_t N, FeistelKey fk, Map map, uint64_t count,
+                                                          uint64_t per_warp, int64_t* __restrict__ out) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned below = (1u << lane) - 1u;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t jb = warp * per_warp;
+    if (jb >= count) return;  // warp-uniform
+    const uint64_t je = (jb + per_warp < count) ? jb + per_warp : count;
+    uint64_t j = jb + lane;
+    bool active = j < je;
+    uint64_t x = active ? map(j) : 0;
+    uint64_t next = jb + 32;
+    while (__any_sync(0xffffffffu, active)) {
+        const uint64_t y = feistel(x, fk);
+        const bool done = active && y < N;
+        const unsigned dm = __ballot_sync(0xffffffffu, done);
+        if (done) {
+            out[j] = (int64_t)y;
+            j = next + __popc(dm & below);
+            active = j < je;
+            if (active) x = map(j);
+        } else {
+            x = y;  // keep walking (inactive lanes compute on a dead value)
+        }
+        next += __popc(dm);
+    }
+}
+
+int refill_warps_per_sm() {   // A/B knob PR_K1_WARPS_PER_SM (8..64, multiple of 8); see launch_walk
+    static const int w = [] {
+        const char* e = getenv("PR_K1_WARPS_PER_SM");
+        const int v = e ? atoi(e) : 0;
+        return (v >= 8 && v <= 64 && v % 8 == 0) ? v : kRefillWarpsPerSM;
+    }();
+    return w;
+}
+
+bool use_direct_kernel() {
+    static const bool direct = [] {
+        const char* e = getenv("PR_K1_KERNEL");
+        return e && !strcmp(e, "direct");
+    }();
+    return direct;
+}
+
+// Launch K1 over `count` outputs.  Refill: warps = min(148·W, ceil(count/32)) (each lane ≥ 1 position),
+// contiguous ranges of ceil(count/warps) positions.  W = warps per SM trades the range's tail (the last
+// lanes' walks finish while the rest of the warp idles: fewer, longer ranges amortise it) against latency
+// hiding (IMAD.WIDE chains; the fmaheavy pipe saturates with a few warps per scheduler).
+template <class Map>
+int launch_walk(uint64_t N, const FeistelKey& fk, Map map, uint64_t count, int64_t* d_out, cudaStream_t st) {
+    if (use_direct_kernel()) {
+        uint64_t blocks = (count + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        walk_direct_kernel<Map><<<(unsigned)blocks, 256, 0, st>>>(N, fk, map, count, d_out);
+    } else {
+        uint64_t warps = (count + 31) / 32;
+        const uint64_t wmax = 148ull * (uint64_t)refill_warps_per_sm();
+        if (warps > wmax) warps = wmax;
+        const uint64_t per_warp = (count + warps - 1) / warps;
+        warps = (count + per_warp - 1) / per_warp;
+        const uint64_t blocks = (warps + 7) / 8;
+        walk_refill_kernel<Map><<<(unsigned)blocks, 256, 0, st>>>(N, fk, map, count, per_warp, d_out);
+    }
+    PR_CUDA_TRY(cudaGetLastError());
+    return PR_OK;
 }
 
 __global__ void philox_test_kernel(const uint32_t* __restrict__ ctr, int64_t n, uint32_t k0, uint32_t k1,
@@ -112,12 +196,7 @@ extern "C" int pr_permute(int64_t N, uint64_t seed, int64_t epoch, int64_t begin
     if (count == 0) return PR_OK;
     if (!d_out) return PR_ERR_INVALID;
     const FeistelKey fk = make_key(N, seed, epoch);
-    int64_t blocks = (count + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    permute_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((uint64_t)N, fk, (uint64_t)begin,
-                                                                        (uint64_t)count, d_out);
-    PR_CUDA_TRY(cudaGetLastError());
-    return PR_OK;
+    return launch_walk((uint64_t)N, fk, RangeMap{(uint64_t)begin}, (uint64_t)count, d_out, (cudaStream_t)stream);
 }
 
 extern "C" int pr_shard_indices(const pr_alloc* a, int32_t rank, int64_t epoch, uint64_t seed, int64_t* d_out,
@@ -140,12 +219,8 @@ extern "C" int pr_shard_steps(const pr_alloc* a, int32_t rank, int64_t epoch, ui
     if (count == 0) return PR_OK;
     if (!d_out) return PR_ERR_INVALID;
     const FeistelKey fk = make_key(N, seed, epoch);
-    int64_t blocks = (count + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    shard_steps_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-        (uint64_t)N, fk, (uint64_t)B, (uint64_t)o, (uint64_t)n, (uint64_t)step0, (uint64_t)count, d_out);
-    PR_CUDA_TRY(cudaGetLastError());
-    return PR_OK;
+    return launch_walk((uint64_t)N, fk, StepMap{(uint64_t)B, (uint64_t)o, (uint64_t)n, (uint64_t)step0},
+                       (uint64_t)count, d_out, (cudaStream_t)stream);
 }
 
 extern "C" int pr_test_philox(const uint32_t* d_ctr, int64_t n, uint64_t key, int32_t use_curand, uint32_t* d_out,

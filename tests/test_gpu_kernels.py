@@ -85,6 +85,28 @@ def test_permute_subrange_and_edges():
         pr.permute(N, 9, 4, 12000, 1000, part)
 
 
+def test_permute_warp_range_boundaries():
+    """K1's lane-refill walk hands each warp a contiguous range of ceil(count / warps) outputs; counts
+    around 32 · k (partial last warp, one lane, ranges shorter than a warp) and offset ranges must give
+    the oracle's π element for element, including the largest grid (148 · 32 warps) with a ragged tail."""
+    rng = np.random.Generator(np.random.PCG64(77))
+    for N in (5, 33, 257, 4099, 65537):
+        full = PM.permute(np.arange(N), N, 31, 2)
+        for count in sorted({1, 2, 31, 32, 33, 63, 64, 65, N // 2, N - 1, N} - {0}):
+            if count > N:
+                continue
+            begin = int(rng.integers(0, N - count + 1))
+            out = torch.full((count + 5,), -7, dtype=torch.int64, device="cuda")
+            pr.permute(N, 31, 2, begin, count, out)
+            got = out.cpu().numpy()
+            assert np.array_equal(got[:count], full[begin:begin + count]), (N, begin, count)
+            assert (got[count:] == -7).all()                  # nothing written past count
+    N = 148 * 32 * 7 + 13                                      # every warp 7 outputs + a ragged tail
+    out = torch.empty(N, dtype=torch.int64, device="cuda")
+    pr.permute(N, 5, 9, 0, N, out)
+    assert np.array_equal(out.cpu().numpy(), PM.permute(np.arange(N), N, 5, 9))
+
+
 @pytest.mark.parametrize("N,ratios,C,g", [(1000, [1, 3], 4, 25), (50000, [1, 2], 3, 128),
                                           (51200, [1, 1, 1, 1], 64, 16), (50000, [1, 1, 1, 1, 2, 2, 4, 4], 64, 16),
                                           (1281167, [3, 1, 4, 1, 5], 14, 2)])

@@ -7,7 +7,7 @@ $NCU --set full --import-source on -k regex:'gather_kernel' -s 2 -c 1 -f -o gpur
 $NCU --set full --import-source on -k regex:ring_kernel -s 2 -c 1 -f -o gpurun_out/prof_ring python tools/profile_kernels.py ring 3 > gpurun_out/ncu_ring.log 2>&1
 $NCU --set full --import-source on -k regex:ring_kernel -s 2 -c 1 -f -o gpurun_out/prof_ring_fused python tools/profile_kernels.py ring_fused_only 3 > gpurun_out/ncu_ring_fused.log 2>&1
 $NCU --set full --import-source on -k regex:sgd_kernel -s 2 -c 1 -f -o gpurun_out/prof_sgd python tools/profile_kernels.py sgd 3 > gpurun_out/ncu_sgd.log 2>&1
-$NCU --set full --import-source on -k regex:permute_kernel -s 1 -c 1 -f -o gpurun_out/prof_permute python tools/profile_kernels.py shard 2 > gpurun_out/ncu_permute.log 2>&1
+$NCU --set full --import-source on -k regex:walk_ -s 1 -c 1 -f -o gpurun_out/prof_permute python tools/profile_kernels.py shard 2 > gpurun_out/ncu_permute.log 2>&1
 BENCH="bench.py --steps 1 --warmup 1 --e2e-epochs 0 --no-cpu-baseline --no-colocated"
 python $BENCH > gpurun_out/bench_profiling_variant.json 2> gpurun_out/bench_profiling_variant.err
 timeout 1500 $NCU --metrics gpu__time_duration.sum --csv --log-file gpurun_out/launches.csv python $BENCH > gpurun_out/ncu_bench.log 2>&1

@@ -122,7 +122,7 @@ def main():
             per[k][0] += 1
             per[k][1] += t
             total += t
-        mine = ("gather_tma_kernel", "gather_kernel", "gather_hwc_bulk_kernel", "permute_kernel", "ring_kernel", "ring_ll_kernel", "twoshot_kernel",
+        mine = ("gather_tma_kernel", "gather_kernel", "gather_hwc_bulk_kernel", "permute_kernel", "walk_refill_kernel", "walk_direct_kernel", "ring_kernel", "ring_ll_kernel", "twoshot_kernel",
                 "sgd_kernel", "spin_kernel", "stamp_kernel", "allgather_f64", "oneshot_ll_kernel", "nvls_kernel",
                 "stamp_seconds_kernel")
         lines += ["## Launch list of the bench command (`ncu --metrics gpu__time_duration.sum`)", "",
