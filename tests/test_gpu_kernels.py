@@ -101,10 +101,11 @@ def test_permute_warp_range_boundaries():
             got = out.cpu().numpy()
             assert np.array_equal(got[:count], full[begin:begin + count]), (N, begin, count)
             assert (got[count:] == -7).all()                  # nothing written past count
-    N = 148 * 32 * 7 + 13                                      # every warp 7 outputs + a ragged tail
-    out = torch.empty(N, dtype=torch.int64, device="cuda")
-    pr.permute(N, 5, 9, 0, N, out)
-    assert np.array_equal(out.cpu().numpy(), PM.permute(np.arange(N), N, 5, 9))
+    for N in (148 * 32 * 7 + 13,                               # every refill warp 7 outputs + a ragged tail
+              148 * 4 * 256 * 3 + 77):                         # ranges of 24 per lane (the full grid) + a ragged tail
+        out = torch.empty(N, dtype=torch.int64, device="cuda")
+        pr.permute(N, 5, 9, 0, N, out)
+        assert np.array_equal(out.cpu().numpy(), PM.permute(np.arange(N), N, 5, 9))
 
 
 @pytest.mark.parametrize("N,ratios,C,g", [(1000, [1, 3], 4, 25), (50000, [1, 2], 3, 128),
