@@ -644,9 +644,10 @@ def colocated_allreduce(hbm, peak_kind, P=8, reps=20):
     del gx
     for c in cx:
         c.destroy()
+    pull = colocated_pull(hbm, n, n3, reps)
     return {"kernel": "ring_kernel<float> (K3), all ranks on one GPU", "P": P, "bytes_per_rank": Z,
             "fused_a6_a9_us": fused_us, "composed_a6_a9_us": composed_us,
-            "c1_allreduce_4KiB_P2_us": c1_us, "vgg16_C3_P4": vgg,
+            "c1_allreduce_4KiB_P2_us": c1_us, "vgg16_C3_P4": vgg, "pull_two_shot": pull,
             "cross_gpu_config_per_rank_busbw_equiv": {
                 "GBs": per_rank_bus, "us": x_us, "bytes": Lx * 4, "P": 2, "channels": 32,
                 "vs_nvlink_770": per_rank_bus / NVLINK_PEER_GBS,
@@ -657,6 +658,46 @@ def colocated_allreduce(hbm, peak_kind, P=8, reps=20):
             "note": "P virtual ranks co-resident on one GPU exercise the same kernel and protocol; peer stores "
                     "land in local HBM, so this is an HBM roofline, not an NVLink number (the algorithmic bytes "
                     "count every staging round trip at HBM, part of which the 126 MB L2 serves: frac can exceed 1)"}
+
+
+def colocated_pull(hbm, n8, n3, reps):
+    """The pull two-shot (PR_ALGO_TWO_SHOT_PULL, N2; the ring's bits) on the same co-located cases as the
+    ring: ResNet-18 gradient at P = 8, C3's VGG-16 gradient at P = 4, and the cross-GPU configuration's
+    per-rank CTA proxy (P = 2, 32 channels, 256 MiB).  Algorithmic HBM bytes per call: every rank reads its
+    chunk from the P buffers and writes it into the P buffers — 2·Z per rank."""
+    import torch
+
+    import paper_2111_08272_b200 as pr
+
+    def one(P, L, n, k, **cfg):
+        comms = pr.comm_init_local(P, torch.cuda.current_device(), pr.comm_config(algo=pr.ALGO_TWO_SHOT_PULL, **cfg))
+        bufs = [torch.randn(L, device="cuda") for _ in range(P)]
+        for _ in range(2):
+            pr.weighted_allreduce_local(comms, bufs, n)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            pr.weighted_allreduce_local(comms, bufs, n)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / k * 1e3
+        del bufs
+        for c in comms:
+            c.destroy()
+        Z = L * 4
+        return {"P": P, "bytes_per_rank": Z, "avg_us": us, "algorithmic_bytes_per_call": 2 * P * Z,
+                "achieved": 2 * P * Z / (us * 1e-6) / 1e9, "frac": 2 * P * Z / (us * 1e-6) / 1e9 / hbm,
+                "busbw_equiv_per_rank_GBs": Z * 2 * (P - 1) / P / (us * 1e-6) / 1e9}
+
+    out = {"kernel": "twoshot_pull_kernel<float> (K3 variant, N2), all ranks on one GPU",
+           "resnet18_P8": one(8, L_RESNET18, n8, reps), "vgg16_C3_P4": one(4, L_VGG16, n3, 5)}
+    x = one(2, (256 << 20) // 4, [1, 2], 5, channels=32, slot_bytes=1 << 20)
+    x["channels"] = 32
+    x["vs_nvlink_770"] = x["busbw_equiv_per_rank_GBs"] / NVLINK_PEER_GBS
+    x["note"] = "CTA-throughput proxy with both ranks on one GPU: not NVLink"
+    out["cross_gpu_config_per_rank"] = x
+    return out
 
 
 # ---------------------------------------------------------------------------------------------------
@@ -932,7 +973,7 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    # AUTO: the step buffers take the ring (with K7 fused); N1's buckets take the two-shot at P >= 8
+    # AUTO: the step buffers take the ring (with K7 fused); N1's buckets take the pull two-shot (<= 16 MiB at P >= 8)
     comm = pr.comm_init(rank, world, local, config=pr.comm_config(algo=pr.ALGO_AUTO)) if world > 1 else None
     ctx = {"world": world, "rank": rank, "local": local, "comm": comm, "tdev": tdev, "shared": shared}
     strong = not args.weak

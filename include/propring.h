@@ -260,8 +260,9 @@ typedef struct {
  * buffer registered (else PR_ERR_INVALID is latched on all ranks). */
 #define PR_ALGO_RING     0
 #define PR_ALGO_TWO_SHOT 1
-#define PR_ALGO_AUTO     2   /* one-shot up to os_max_bytes, LL ring up to ll_max_bytes, two-shot up to
-                                 ts_max_bytes (× 2 for P >= 4, × 4 for P >= 8), ring above */
+#define PR_ALGO_AUTO     2   /* one-shot up to os_max_bytes, LL ring up to ll_max_bytes, the PULL two-shot
+                                 (registered buffers) up to ts_max_bytes (× 2 for P >= 4, × 4 for P >= 8),
+                                 ring above */
 /* LL ring: the ring's schedule, order and rounding (same bits) with a low-latency line protocol — every
  * 16-byte line pushed to the next rank carries 8 payload bytes and the call's sequence number in both
  * 64-bit halves, so the receiver polls the data itself (no fence / flag / credit round trip per hop).
@@ -278,6 +279,14 @@ typedef struct {
                               * reduces its chunk with multimem.ld_reduce and multicasts it with multimem.st.
                               * The switch's summation order is unspecified: within tolerance of the fp64
                               * mean, NOT the ring's bits.  Buffers outside the region take the ring. */
+/* Pull two-shot (round 2): after the handshake rank r LOADS its chunk r from every rank's registered
+ * buffer (instead of each rank pushing it into r's staging), reduces it in the ring's order with the
+ * ring's rounding (same bits) and stores the result into every rank's buffer.  Stores per rank fall from
+ * (2P−1)/P·Z to Z — the SM store path is what bounds a channel.  Needs every rank's buffer registered
+ * (else PR_ERR_INVALID is latched on all ranks).  PR_ALGO_AUTO takes it instead of the push two-shot
+ * (registered buffers up to ts_max_bytes); above that AUTO keeps the ring (the paper's algorithm, and the
+ * only one with the fused update), since the pull's peer loads are unmeasured over NVLink. */
+#define PR_ALGO_TWO_SHOT_PULL 6
 
 /* Byte allgather supplied by the caller (e.g. over a torch process group): every rank passes `len`
  * bytes in `send` and receives the P·len bytes of all ranks, rank-ordered, in `recv`.  Returns 0 on

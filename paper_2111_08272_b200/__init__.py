@@ -264,6 +264,7 @@ ALGO_AUTO = 2
 ALGO_LL = 3
 ALGO_ONESHOT = 4
 ALGO_NVLS = 5
+ALGO_TWO_SHOT_PULL = 6
 
 
 def comm_config(channels=0, slots=8, threads=512, slot_bytes=0, watchdog_ns=10_000_000_000,
@@ -276,8 +277,10 @@ def comm_config(channels=0, slots=8, threads=512, slot_bytes=0, watchdog_ns=10_0
     throughput of tools/sweep_cta.py).
     sys_scope=True forces system-scope synchronisation even when all ranks share one GPU (tests).
     algo: ALGO_RING (the paper's ring), ALGO_LL (the ring with the low-latency line protocol, buffers up to
-    ll_max_bytes), ALGO_ONESHOT (one hop, buffers up to os_max_bytes), ALGO_TWO_SHOT, or ALGO_AUTO (one-shot up
-    to os_max_bytes, LL up to ll_max_bytes, two-shot up to ts_max_bytes, ring above)."""
+    ll_max_bytes), ALGO_ONESHOT (one hop, buffers up to os_max_bytes), ALGO_TWO_SHOT, ALGO_TWO_SHOT_PULL (the
+    two-shot with its first phase as loads from the peers' registered buffers), or ALGO_AUTO (one-shot up to
+    os_max_bytes, LL up to ll_max_bytes, the pull two-shot for registered buffers up to ts_max_bytes, ring
+    above)."""
     flags = ((COMM_FLAG_FORCE_STAGED if force_staged else 0) | (COMM_FLAG_SYS_SCOPE if sys_scope else 0)
              | (COMM_FLAG_BULK_STORE if bulk_store else 0) | (COMM_FLAG_L2_PREFETCH if l2_prefetch else 0))
     return CommConfig(channels=channels, slots=slots, threads=threads, flags=flags, slot_bytes=slot_bytes,

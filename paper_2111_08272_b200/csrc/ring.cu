@@ -1163,6 +1163,155 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__
 }
 
 // =====================================================================================================
+// Pull two-shot (PR_ALGO_TWO_SHOT_PULL, round 2): the two-shot's reduction with phase A replaced by loads.
+// After the handshake (the barrier: every rank's gradient is final) rank r reads its chunk r straight out
+// of the P ranks' registered buffers, in the ring's order for chunk r (r, r+1, …, r+P−1) with the ring's
+// per-hop rounding — the ring's bits — and stores the result into all P buffers.  No staging, no per-slice
+// flags: one release per peer at the end ("my reduced chunk is in your buffer, and I have finished reading
+// yours") and one wait for all P−1 of them.  No hazard between ranks: chunk r of every buffer is read and
+// then written only by rank r (same thread, same address, program order).
+// Why: a channel's bound is the SM's store path (≈ 62 GB/s per SM).  The ring and the push
+// two-shot store (2P−1)/P·Z per rank for a bus volume of 2(P−1)/P·Z — 1.5 (P = 2) to 1.07 (P = 8) stored
+// bytes per bus byte; pulling phase A leaves only phase B's Z of stores: P/(2(P−1)) = 1.0 (P = 2) to 0.57
+// (P = 8).  The loads are the same Z per rank (own chunk + P−1 peer slices), issued as P independent
+// 16-byte L2-coherent loads per vector and thread.
+// =====================================================================================================
+// The pull two-shot's reduction: like ts_reduce, but U vectors per thread per iteration with all U·P loads
+// issued before any store.  The own buffer is both a source and a destination, so the compiler cannot
+// hoist the next iteration's loads above this iteration's stores by itself; with P = 2 one vector per
+// iteration left 2 loads in flight per thread and the channel latency-bound.
+template <typename T, int PP, int U>
+__device__ __forceinline__ void ts_pull_reduce(int64_t nv, const uint8_t* const* src, const float* wt, const int* act,
+                                               uint8_t* const* dst) {
+    constexpr int V = Vec<T>::V;
+    const int64_t B = blockDim.x;
+    for (int64_t v0 = threadIdx.x; v0 < nv; v0 += B * U) {
+        uint4 x[U][PP];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t v = v0 + u * B;
+#pragma unroll
+            for (int h = 0; h < PP; ++h)
+                x[u][h] = (v < nv && act[h]) ? ld_cg_v4(src[h] + (size_t)v * 16) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t v = v0 + u * B;
+            if (v >= nv) break;
+            float acc[V];
+#pragma unroll
+            for (int j = 0; j < V; ++j) acc[j] = 0.0f;
+#pragma unroll
+            for (int h = 0; h < PP; ++h) {
+                if (!act[h]) continue;                        // n_q = 0 contributes nothing (never multiplied)
+                const float sq = wt[h];
+#pragma unroll
+                for (int j = 0; j < V; ++j)
+                    acc[j] = rnd_dtype<T>(h == 0 ? __fmul_rn(sq, lane_f<T>(x[u][h], j))
+                                                 : __fmaf_rn(sq, lane_f<T>(x[u][h], j), acc[j]));
+            }
+            const uint4 y = pack_f<T>(acc);
+#pragma unroll
+            for (int q = 0; q < PP; ++q) st_v4(dst[q] + (size_t)v * 16, y);
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, 1) twoshot_pull_kernel(const __grid_constant__ LaunchArgs A) {
+    __shared__ int s_err;
+    __shared__ long long s_n[PR_MAX_RANKS];
+    __shared__ uint8_t* s_bufs[PR_MAX_RANKS];
+    __shared__ float s_w[PR_MAX_RANKS];
+    __shared__ const uint8_t* s_src[PR_MAX_RANKS];
+    __shared__ uint8_t* s_dst[PR_MAX_RANKS];
+    __shared__ float s_wt[PR_MAX_RANKS];
+    __shared__ int s_act[PR_MAX_RANKS];
+    __shared__ int s_abort;
+    const RankCall& rc = A.calls[blockIdx.y];
+    const DevTable* tab = rc.tab;
+    const int ch = blockIdx.x;
+    const int r = tab->rank, P = tab->P;
+    uint8_t* my = tab->win[r];
+    ChanState* st = state_of(my, tab, ch);
+    TsFlags* mf = ts_flags_of(my, tab, ch);
+    const bool t0 = threadIdx.x == 0;
+    const bool sys = tab->sysscope != 0;
+    unsigned long long deadline = ~0ull;
+    if (threadIdx.x < 32) {                           // warp 0 runs the handshake
+        const unsigned long long start = gtimer();
+        if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
+        if (t0 && ch == 0) tab->stamps[0] = (long long)start;
+        const HsOut hs = handshake(A, rc, tab, st, ch, sys, deadline, s_n, s_bufs);
+        __syncwarp();
+        for (int q = (int)threadIdx.x; q < P; q += 32)
+            s_w[q] = hs.sumn > 0 ? (float)((double)s_n[q] / (double)hs.sumn) : 0.0f;
+        if (t0) {
+            s_err = hs.err ? hs.err : (hs.direct ? 0 : PR_ERR_INVALID);   // reads and writes registered buffers
+            s_abort = 0;
+            if (ch == 0) tab->stamps[1] = (long long)gtimer();
+        }
+    }
+    __syncthreads();
+    if (s_err) {
+        if (t0) latch(tab, s_err);
+        return;
+    }
+    constexpr int V = Vec<T>::V;
+    const int64_t count = A.count;
+    const int64_t per = (count + P - 1) / P;
+    const int64_t cs = (per + V - 1) / V * V;
+    const int64_t subp = (cs + tab->channels - 1) / tab->channels;
+    const int64_t sub = (subp + V - 1) / V * V;
+    const unsigned long long base = st->ts_base;
+    // this channel's share of chunk r (the ring's chunk / channel geometry, DESIGN.md §3 #14)
+    const int64_t clo = (int64_t)r * cs;
+    const int64_t lo = clo + (int64_t)ch * sub;
+    const int64_t hi = min(clo + min((int64_t)(ch + 1) * sub, cs), count);
+    const int64_t len = hi > lo ? hi - lo : 0;
+    const int64_t nv = len / V;
+    for (int h = (int)threadIdx.x; h < P; h += (int)blockDim.x) {     // the P sources in ring order, once
+        const int q = (r + h) % P;
+        s_src[h] = reinterpret_cast<const uint8_t*>(reinterpret_cast<const T*>(s_bufs[q]) + lo);
+        s_wt[h] = s_w[q];
+        s_act[h] = s_n[q] > 0 ? 1 : 0;
+        s_dst[h] = reinterpret_cast<uint8_t*>(reinterpret_cast<T*>(s_bufs[h]) + lo);
+    }
+    __syncthreads();
+    if (len > 0) {
+        if (P == 8) ts_pull_reduce<T, 8, 2>(nv, s_src, s_wt, s_act, s_dst);
+        else if (P == 4) ts_pull_reduce<T, 4, 2>(nv, s_src, s_wt, s_act, s_dst);
+        else if (P == 2) ts_pull_reduce<T, 2, 4>(nv, s_src, s_wt, s_act, s_dst);
+        else ts_reduce<T, 0>(P, nv, s_src, s_wt, s_act, s_dst);
+        for (int64_t e = nv * V + threadIdx.x; e < len; e += blockDim.x) {   // ragged tail: end of buffer
+            float acc = 0.0f;
+            for (int h = 0; h < P; ++h) {
+                const int q = (r + h) % P;
+                if (s_n[q] <= 0) continue;
+                const T xv = reinterpret_cast<const T*>(s_bufs[q])[lo + e];
+                acc = rnd_dtype<T>(h == 0 ? __fmul_rn(s_w[q], Vec<T>::to_f(xv)) : __fmaf_rn(s_w[q], Vec<T>::to_f(xv), acc));
+            }
+            for (int q = 0; q < P; ++q) reinterpret_cast<T*>(s_bufs[q])[lo + e] = Vec<T>::from_f(acc);
+        }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < P - 1) {                                  // one releasing thread per peer
+        const int q = (r + 1 + (int)threadIdx.x) % P;
+        st_release(&ts_flags_of(tab->win[q], tab, ch)->ag[r], base + 1, sys);
+    }
+    if (threadIdx.x < 32)
+        if (!warp_wait_peers(mf->ag, base + 1, r, P, deadline, sys) && t0) {
+            s_abort = 1;
+            latch(tab, PR_ERR_PEER_TIMEOUT);
+        }
+    __syncthreads();
+    if (t0) {
+        if (!s_abort) st->ts_base = base + 1;   // the push two-shot's counters stay consistent (targets are >=)
+        if (ch == 0) tab->stamps[2] = (long long)gtimer();
+    }
+}
+
+// =====================================================================================================
 // LL ring (low-latency protocol for small buffers): the SAME ring schedule, order and per-hop rounding as
 // ring_kernel — so the result is bit-identical — but every 16-byte line a rank pushes carries its own
 // validity: two 64-bit elements, each (flag << 32 | 32 payload bits), flag = the call's handshake sequence.
@@ -1707,7 +1856,7 @@ int check_config(const pr_comm_config& c) {
                      PR_COMM_FLAG_L2_PREFETCH)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
-        (int64_t)c.stages * 2 * c.tile_bytes > 224 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_NVLS ||
+        (int64_t)c.stages * 2 * c.tile_bytes > 224 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_TWO_SHOT_PULL ||
         c.ll_max_bytes < 0 || c.ll_max_bytes > (64ll << 20) || c.os_max_bytes < 0 || c.os_max_bytes > (16ll << 20) ||
         c.min_slice_bytes < 0 || c.min_slice_bytes % 16 ||
         c.ts_slots < 2 || c.ts_slots > 16 || c.ts_slot_bytes < 256 || c.ts_slot_bytes % 256 ||
@@ -1823,21 +1972,25 @@ size_t dtype_size(int32_t dt) { return dt == PR_DTYPE_F32 ? 4 : (dt == PR_DTYPE_
 // The algorithm a call takes: a pure function of (config, count, dtype, P, registered).
 // AUTO's two-shot limit grows with P: the ring pays 2P−2 flag round trips per call, the two-shot 2; at
 // `.sys` scope and P = 8 the two-shot won up to 16 MiB (tools/ar_latency.py --sys), at P = 2 the ring wins
-// from 4 MiB — so ts_max_bytes × 4 for P >= 8, × 2 for P >= 4.  The two-shot stores its reduced slices
-// straight into every peer's registered buffer, so AUTO takes it only for a registered buffer (and never
-// under FORCE_STAGED); an explicit PR_ALGO_TWO_SHOT on an unregistered buffer latches PR_ERR_INVALID.
+// from 4 MiB — so ts_max_bytes × 4 for P >= 8, × 2 for P >= 4 (kept for the pull two-shot, which beat
+// the ring at every size co-located — unmeasured over NVLink).  Both two-shots read / write every peer's
+// registered buffer, so AUTO takes one only for a registered buffer (and never under FORCE_STAGED); an
+// explicit PR_ALGO_TWO_SHOT[_PULL] on an unregistered buffer latches PR_ERR_INVALID.
 // `registered` is per rank: a job whose ranks differ there picks different kernels, and the handshake
 // (which carries the algorithm) turns that into PR_ERR_LENGTH_MISMATCH on every rank.
 int pick_algo(const pr_comm_config& cfg, int64_t count, int32_t dtype, int P, bool registered, bool in_nvls = false) {
     const int64_t bytes = count * (dtype == PR_DTYPE_F32 ? 4 : 2);
     // NVLS only when asked for, on an fp32 buffer inside the communicator's NVLS region; otherwise the ring
     if (cfg.algo == PR_ALGO_NVLS) return (in_nvls && dtype == PR_DTYPE_F32 && P > 1) ? PR_ALGO_NVLS : PR_ALGO_RING;
+    if (cfg.algo == PR_ALGO_TWO_SHOT_PULL) return PR_ALGO_TWO_SHOT_PULL;   // explicit only (see the header)
     const int64_t ts_max = cfg.ts_max_bytes * (P >= 8 ? 4 : (P >= 4 ? 2 : 1));
     const bool direct_ok = registered && !(cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
     if ((cfg.algo == PR_ALGO_ONESHOT || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.os_max_bytes) return PR_ALGO_ONESHOT;
     if ((cfg.algo == PR_ALGO_LL || cfg.algo == PR_ALGO_AUTO) && bytes <= cfg.ll_max_bytes) return PR_ALGO_LL;
-    if (cfg.algo == PR_ALGO_TWO_SHOT || (cfg.algo == PR_ALGO_AUTO && direct_ok && bytes <= ts_max))
-        return PR_ALGO_TWO_SHOT;
+    if (cfg.algo == PR_ALGO_TWO_SHOT) return PR_ALGO_TWO_SHOT;
+    // AUTO's two-shot slot takes the pull variant (round 2): same bits, same registration requirement, and
+    // faster than the push two-shot at every size / P / scope measured (profiles/round2_k3_pull_latency.txt)
+    if (cfg.algo == PR_ALGO_AUTO && direct_ok && bytes <= ts_max) return PR_ALGO_TWO_SHOT_PULL;
     return PR_ALGO_RING;
 }
 
@@ -1877,6 +2030,9 @@ int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_conf
         case PR_ALGO_TWO_SHOT:
             return launch_k3(f32 ? (void*)twoshot_kernel<float> : (void*)twoshot_kernel<__nv_bfloat16>, a, nranks,
                              channels, threads, 0, s, coop);
+        case PR_ALGO_TWO_SHOT_PULL:
+            return launch_k3(f32 ? (void*)twoshot_pull_kernel<float> : (void*)twoshot_pull_kernel<__nv_bfloat16>, a,
+                             nranks, channels, threads, 0, s, coop);
         default: break;
     }
     const bool bulk = (cfg.flags & PR_COMM_FLAG_BULK_STORE) != 0;

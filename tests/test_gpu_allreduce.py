@@ -316,8 +316,68 @@ def test_two_shot_small_slots_many_slices_and_sys_scope():
                 _check(P, L, "bf16", [2] * P, comms, seed=L)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 8])
+def test_pull_two_shot_bit_identical_to_ring_replay(P, dtype):
+    """PR_ALGO_TWO_SHOT_PULL: chunk r read straight out of every rank's buffer, reduced in the ring's order
+    with the ring's rounding — the ring replay's bits, including n_r = 0 ranks and ragged tails."""
+    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL)
+    rng = np.random.Generator(np.random.PCG64(300 + P))
+    for L in (1, 7, P + 1, 4099, 2 ** 20 + 3):
+        n = [int(x) * 16 for x in rng.integers(1, 9, P)]
+        if L % 2:
+            n[int(rng.integers(0, P))] = 0
+        _check(P, L, dtype, n, comms, kind="mixed" if L % 3 == 0 else "gaussian", seed=L)
+
+
+def test_pull_two_shot_channels_sys_scope_and_graph_replay():
+    for cfg in (dict(channels=1), dict(channels=3, sys_scope=True), dict(channels=64, threads=128)):
+        for P in (2, 4, 7):
+            comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL, **cfg)
+            for it, L in enumerate((999, 300_001, 5)):                # back to back: monotone counters
+                _check(P, L, "f32" if it % 2 == 0 else "bf16", [5] * (P - 1) + [it], comms, seed=L)
+    P, L = 3, 40_000
+    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL)
+    host, dev = _inputs(P, L, "f32", seed=22)
+    src = [d.clone() for d in dev]
+    n = [3, 1, 2]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        pr.weighted_allreduce_local(comms, dev, n, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            pr.weighted_allreduce_local(comms, dev, n, stream=s)
+    emu = W.ring_emulate(host, n, "f32")
+    for _ in range(3):
+        for d, s0 in zip(dev, src):
+            d.copy_(s0)
+        g.replay()
+        torch.cuda.synchronize()
+        assert all(np.array_equal(d.cpu().numpy(), emu) for d in dev)
+
+
+@pytest.mark.parametrize("P,L", [(8, 11_689_512), (4, 138_357_544)])
+def test_pull_two_shot_full_sizes_against_oracle(P, L):
+    """ResNet-18 gradient at P = 8 and VGG-16 at P = 4 (C3): sampled elements against the fp64 weighted mean
+    (the oracle's definition, one element at a time) and every rank identical to rank 0."""
+    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL)
+    g = torch.Generator(device="cuda").manual_seed(L % 1000 + P)
+    dev = [torch.randn(L, device="cuda", generator=g) for _ in range(P)]
+    idx = torch.from_numpy(np.random.Generator(np.random.PCG64(L)).integers(0, L, 20000)).cuda()
+    samp = np.stack([d[idx].cpu().numpy() for d in dev])
+    n = [int(x) for x in np.random.Generator(np.random.PCG64(P)).integers(1, 400, P)]
+    pr.weighted_allreduce_local(comms, dev, n)
+    torch.cuda.synchronize()
+    assert all(c.status() == 0 for c in comms)
+    ref, den = W.weighted_average(samp.astype(np.float64), n)
+    err, zb = W.error_metric(dev[0][idx].cpu().numpy().astype(np.float64), ref, den)
+    assert zb == 0 and err <= TOL["f32"], err
+    assert all(torch.equal(d, dev[0]) for d in dev[1:])
+
+
 def test_auto_mixes_algorithms_back_to_back():
-    """ALGO_AUTO: LL ring up to ll_max_bytes (256 KiB), two-shot up to ts_max_bytes, ring above; interleaved
+    """ALGO_AUTO: LL ring up to ll_max_bytes (256 KiB), pull two-shot up to ts_max_bytes, ring above; interleaved
     calls share the handshake sequence (the LL line flag) and the counters."""
     P = 4
     comms = group(P, algo=pr.ALGO_AUTO, ts_max_bytes=1 << 20)
@@ -529,7 +589,7 @@ def test_randomized_configs_all_algorithms():
     """Seeded sweep over communicator configurations × algorithms × P × counts × dtypes × weights: every
     result bit-identical to the oracle's ring replay (and, for fused calls, to ring + K7)."""
     rng = np.random.Generator(np.random.PCG64(2024))
-    algos = [pr.ALGO_RING, pr.ALGO_TWO_SHOT, pr.ALGO_LL, pr.ALGO_ONESHOT, pr.ALGO_AUTO]
+    algos = [pr.ALGO_RING, pr.ALGO_TWO_SHOT, pr.ALGO_LL, pr.ALGO_ONESHOT, pr.ALGO_AUTO, pr.ALGO_TWO_SHOT_PULL]
     for case in range(80):
         P = int(rng.choice([2, 3, 4, 5, 6, 7, 8]))
         stages = int(rng.integers(2, 7))

@@ -97,7 +97,8 @@ def _gpu_worker(rank, world, port, q):
         bad = []
         # every algorithm over real CUDA-IPC peer windows; the LL ring also at forced system scope
         for algo, sys_scope in ((pr.ALGO_RING, False), (pr.ALGO_TWO_SHOT, False), (pr.ALGO_LL, False),
-                                (pr.ALGO_LL, True), (pr.ALGO_ONESHOT, True)):
+                                (pr.ALGO_LL, True), (pr.ALGO_ONESHOT, True), (pr.ALGO_TWO_SHOT_PULL, False),
+                                (pr.ALGO_TWO_SHOT_PULL, True)):
             comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=2, watchdog_ns=30_000_000_000,
                                                                       algo=algo, sys_scope=sys_scope))
             L = 4099

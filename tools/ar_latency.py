@@ -41,7 +41,7 @@ def main():
     sizes = [int(s) for s in a.sizes.split(",")]
     for algo_name in a.algos.split(","):
         algo = {"ring": pr.ALGO_RING, "two_shot": pr.ALGO_TWO_SHOT, "ll": pr.ALGO_LL, "oneshot": pr.ALGO_ONESHOT,
-                "auto": pr.ALGO_AUTO}[algo_name]
+                "auto": pr.ALGO_AUTO, "pull": pr.ALGO_TWO_SHOT_PULL}[algo_name]
         comms = pr.comm_init_local(P, 0, pr.comm_config(algo=algo, sys_scope=a.sys, channels=a.channels,
                                                          ll_max_bytes=a.ll_max, os_max_bytes=a.os_max,
                                                          slots=a.slots,

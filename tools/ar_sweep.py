@@ -164,7 +164,7 @@ if __name__ == "__main__":
     ap.add_argument("--colocated", type=int, default=0)
     ap.add_argument("--max-mib", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--algo", type=int, default=0, help="0 ring, 1 two-shot, 2 auto, 3 LL ring, 4 one-shot LL, 5 NVLS")
+    ap.add_argument("--algo", type=int, default=0, help="0 ring, 1 two-shot, 2 auto, 3 LL ring, 4 one-shot LL, 5 NVLS, 6 pull two-shot")
     ap.add_argument("--channels", type=int, default=0, help="CTAs per rank (multi-GPU mode; 0 = topology default)")
     ap.add_argument("--min-slice", type=int, default=0, help="ring min_slice_bytes (0 = slot-sized slices)")
     ap.add_argument("--bulk", action="store_true", help="ring data path with TMA bulk stores")

@@ -1,6 +1,6 @@
 """Run each library kernel in isolation at bench sizes (target for `ncu --set full`, one GPU).
 
-    python tools/profile_kernels.py [gather|gather_imagenet|shard|ring|all] [reps]
+    python tools/profile_kernels.py [gather|gather_imagenet|shard|ring|pull|pull_cta|ring_cta|all] [reps]
 
 gather          K2 at the bench step size: 1024 CIFAR rows (3,072 B u8 -> 6,144 B bf16)
 gather_imagenet K2 at the C3 fast-rank size: 336 ImageNet-shaped rows (150,528 B -> 301,056 B)
@@ -99,6 +99,20 @@ def ring(reps, P=8, L=11_689_512, **cfg):
         c.destroy()
 
 
+def pull(reps, P=8, L=11_689_512, **cfg):
+    """K3 pull two-shot (PR_ALGO_TWO_SHOT_PULL); algorithmic HBM bytes co-located: every rank reads its
+    chunk from P buffers (Z) and writes it into P buffers (Z) -> 2·Z per rank."""
+    comms = pr.comm_init_local(P, 0, pr.comm_config(algo=pr.ALGO_TWO_SHOT_PULL, **cfg))
+    bufs = [torch.randn(L, device="cuda") for _ in range(P)]
+    n = [64, 64, 64, 64, 128, 128, 256, 256][:P]
+    us = timed(lambda: pr.weighted_allreduce_local(comms, bufs, n), reps)
+    byts = 2 * P * L * 4
+    print(f"pull two-shot P={P} L={L}: {us:.1f} us, {byts / us / 1e3:.1f} GB/s algorithmic HBM (all ranks), "
+          f"bus-equivalent per rank {L * 4 * 2 * (P - 1) / P / us / 1e3:.1f} GB/s")
+    for c in comms:
+        c.destroy()
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
@@ -134,6 +148,12 @@ if __name__ == "__main__":
         sgd(reps, L=138_357_544)
     if what == "gather_imagenet_epoch_hwc_lsu":        # the VGG-16 leg's launch kind (LSU, channels-last)
         gather(16384, 150528, 16384, reps, 50176, impls=(1,), layout=1)
+    if what == "pull":                                  # co-located ResNet-18 gradient, 8 ranks, default channels
+        pull(reps)
+    if what == "pull_cta":                              # per-channel regime: P = 2, 4 channels, 256 MiB
+        pull(max(2, reps // 4), P=2, L=(256 << 20) // 4, channels=4)
+    if what == "ring_cta":                              # the ring in the same per-channel regime
+        ring(max(2, reps // 4), P=2, L=(256 << 20) // 4, channels=4)
     if what == "ring_sizes":                            # default channels: P = 2 / 4 / 8 at the ResNet-18 and VGG-16 sizes
         for P in (2, 4, 8):
             for L in (11_689_512, 138_357_544):
