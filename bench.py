@@ -692,6 +692,25 @@ def colocated_pull(hbm, n8, n3, reps):
 
     out = {"kernel": "twoshot_pull_kernel<float> (K3 variant, N2), all ranks on one GPU",
            "resnet18_P8": one(8, L_RESNET18, n8, reps), "vgg16_C3_P4": one(4, L_VGG16, n3, 5)}
+    # rows a6-a9 fused into the pull two-shot (K7 applied by the chunk owner, gradient reset), as the ring's
+    # fused_a6_a9_us beside it
+    P, L = 8, L_RESNET18
+    comms = pr.comm_init_local(P, torch.cuda.current_device(), pr.comm_config(algo=pr.ALGO_TWO_SHOT_PULL))
+    store = [torch.randn(2 * L, device="cuda") for _ in range(P)]
+    grads, thetas = [x[:L] for x in store], [x[L:] for x in store]
+    for _ in range(3):
+        pr.weighted_allreduce_sgd_local(comms, grads, thetas, n8, 1e-6, 0.0, zero_grad=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        pr.weighted_allreduce_sgd_local(comms, grads, thetas, n8, 1e-6, 0.0, zero_grad=True)
+    e1.record()
+    torch.cuda.synchronize()
+    out["fused_a6_a9_resnet18_P8_us"] = e0.elapsed_time(e1) / reps * 1e3
+    del store, grads, thetas
+    for c in comms:
+        c.destroy()
     x = one(2, (256 << 20) // 4, [1, 2], 5, channels=32, slot_bytes=1 << 20)
     x["channels"] = 32
     x["vs_nvlink_770"] = x["busbw_equiv_per_rank_GBs"] / NVLINK_PEER_GBS

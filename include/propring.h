@@ -341,10 +341,13 @@ int pr_weighted_allreduce_local(pr_comm *const *comms, void *const *d_bufs, int6
  * d_grad (as pr_weighted_allreduce) followed by pr_sgd_update(d_theta, ḡ, lr, wd, zero_grad) — with the TMA
  * ring and registered buffers, ONE kernel: the owner of each reduced chunk applies the update to its θ
  * chunk and the all-gather carries θ' (into every rank's d_theta) instead of ḡ; the gradient is reset as
- * the reduce-scatter consumes it.  d_theta must hold identical values on every rank (replicated
+ * the reduce-scatter consumes it.  With the pull two-shot (PR_ALGO_TWO_SHOT_PULL, or AUTO at its sizes)
+ * likewise one kernel: the owner of chunk r stores θ' into every rank's θ, and each rank resets its own
+ * gradient after the final wait (when every peer has read it).  d_theta must hold identical values on every rank (replicated
  * parameters) and lie at the same byte offset from d_grad inside the same registered region on every rank
  * (e.g. one pr_comm_alloc of 2·count floats: [grad | theta]); else — or when the configured algorithm for
- * this size is not the ring — the call is composed of the two operations (same bits).  After the call
+ * this size is neither the ring nor the pull two-shot — the call is composed of the two operations (same
+ * bits).  After the call
  * d_theta holds θ' on every rank; d_grad holds 0 if zero_grad, else unspecified (the reduced ḡ is not
  * materialised in the fused path).  Errors: as pr_weighted_allreduce (+ PR_ERR_INVALID latched when the
  * ranks' θ layouts differ). */

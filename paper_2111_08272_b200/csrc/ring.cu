@@ -1180,9 +1180,10 @@ __global__ void __launch_bounds__(512, 1) twoshot_kernel(const __grid_constant__
 // issued before any store.  The own buffer is both a source and a destination, so the compiler cannot
 // hoist the next iteration's loads above this iteration's stores by itself; with P = 2 one vector per
 // iteration left 2 loads in flight per thread and the channel latency-bound.
-template <typename T, int PP, int U>
+// FUSE (fp32): ḡ is not stored; θ' = K7(θ, ḡ) from the owner's θ replica (`thp`) goes to the P θ buffers (dst).
+template <typename T, int PP, int U, bool FUSE>
 __device__ __forceinline__ void ts_pull_reduce(int64_t nv, const uint8_t* const* src, const float* wt, const int* act,
-                                               uint8_t* const* dst) {
+                                               uint8_t* const* dst, const uint8_t* thp, float nlr, float wd) {
     constexpr int V = Vec<T>::V;
     const int64_t B = blockDim.x;
     for (int64_t v0 = threadIdx.x; v0 < nv; v0 += B * U) {
@@ -1210,14 +1211,43 @@ __device__ __forceinline__ void ts_pull_reduce(int64_t nv, const uint8_t* const*
                     acc[j] = rnd_dtype<T>(h == 0 ? __fmul_rn(sq, lane_f<T>(x[u][h], j))
                                                  : __fmaf_rn(sq, lane_f<T>(x[u][h], j), acc[j]));
             }
-            const uint4 y = pack_f<T>(acc);
+            uint4 y = pack_f<T>(acc);
+            if (FUSE) y = sgd_v4<T>(*reinterpret_cast<const uint4*>(thp + (size_t)v * 16), y, nlr, wd);
 #pragma unroll
             for (int q = 0; q < PP; ++q) st_v4(dst[q] + (size_t)v * 16, y);
         }
     }
 }
 
-template <typename T>
+// Any P (not unrolled), one vector per iteration; FUSE as above.
+template <typename T, bool FUSE>
+__device__ __forceinline__ void ts_pull_reduce_any(int P, int64_t nv, const uint8_t* const* src, const float* wt,
+                                                   const int* act, uint8_t* const* dst, const uint8_t* thp, float nlr,
+                                                   float wd) {
+    constexpr int V = Vec<T>::V;
+    for (int64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+        float acc[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = 0.0f;
+        for (int h = 0; h < P; ++h) {
+            if (!act[h]) continue;
+            const uint4 x = ld_cg_v4(src[h] + (size_t)v * 16);
+            const float sq = wt[h];
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                acc[j] = rnd_dtype<T>(h == 0 ? __fmul_rn(sq, lane_f<T>(x, j)) : __fmaf_rn(sq, lane_f<T>(x, j), acc[j]));
+        }
+        uint4 y = pack_f<T>(acc);
+        if (FUSE) y = sgd_v4<T>(*reinterpret_cast<const uint4*>(thp + (size_t)v * 16), y, nlr, wd);
+        for (int q = 0; q < P; ++q) st_v4(dst[q] + (size_t)v * 16, y);
+    }
+}
+
+// FUSE (fp32, rows a6-a9 in one kernel as ring_kernel<float, true>): the owner of chunk r applies K7 to its θ
+// replica and stores θ' into the P θ buffers (buf + th_delta on every rank) instead of ḡ; ḡ is never
+// materialised.  With A.zero each rank resets its own gradient after the final wait (every peer has then
+// finished reading it).  Same bits as ring + K7.
+template <typename T, bool FUSE>
 __global__ void __launch_bounds__(512, 1) twoshot_pull_kernel(const __grid_constant__ LaunchArgs A) {
     __shared__ int s_err;
     __shared__ long long s_n[PR_MAX_RANKS];
@@ -1248,6 +1278,7 @@ __global__ void __launch_bounds__(512, 1) twoshot_pull_kernel(const __grid_const
             s_w[q] = hs.sumn > 0 ? (float)((double)s_n[q] / (double)hs.sumn) : 0.0f;
         if (t0) {
             s_err = hs.err ? hs.err : (hs.direct ? 0 : PR_ERR_INVALID);   // reads and writes registered buffers
+            if (FUSE && A.fuse == 0) s_err = PR_ERR_INVALID;
             s_abort = 0;
             if (ch == 0) tab->stamps[1] = (long long)gtimer();
         }
@@ -1275,14 +1306,18 @@ __global__ void __launch_bounds__(512, 1) twoshot_pull_kernel(const __grid_const
         s_src[h] = reinterpret_cast<const uint8_t*>(reinterpret_cast<const T*>(s_bufs[q]) + lo);
         s_wt[h] = s_w[q];
         s_act[h] = s_n[q] > 0 ? 1 : 0;
-        s_dst[h] = reinterpret_cast<uint8_t*>(reinterpret_cast<T*>(s_bufs[h]) + lo);
+        // destinations: the P gradient buffers, or (FUSE) the P θ buffers = gradient + th_delta bytes
+        s_dst[h] = reinterpret_cast<uint8_t*>(reinterpret_cast<T*>(s_bufs[h] + (FUSE ? rc.th_delta : 0)) + lo);
     }
     __syncthreads();
+    const uint8_t* thp = FUSE ? reinterpret_cast<const uint8_t*>(reinterpret_cast<const T*>(
+                                    reinterpret_cast<const uint8_t*>(rc.buf) + rc.th_delta) + lo)
+                              : nullptr;
     if (len > 0) {
-        if (P == 8) ts_pull_reduce<T, 8, 2>(nv, s_src, s_wt, s_act, s_dst);
-        else if (P == 4) ts_pull_reduce<T, 4, 2>(nv, s_src, s_wt, s_act, s_dst);
-        else if (P == 2) ts_pull_reduce<T, 2, 4>(nv, s_src, s_wt, s_act, s_dst);
-        else ts_reduce<T, 0>(P, nv, s_src, s_wt, s_act, s_dst);
+        if (P == 8) ts_pull_reduce<T, 8, 2, FUSE>(nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
+        else if (P == 4) ts_pull_reduce<T, 4, 2, FUSE>(nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
+        else if (P == 2) ts_pull_reduce<T, 2, 4, FUSE>(nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
+        else ts_pull_reduce_any<T, FUSE>(P, nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
         for (int64_t e = nv * V + threadIdx.x; e < len; e += blockDim.x) {   // ragged tail: end of buffer
             float acc = 0.0f;
             for (int h = 0; h < P; ++h) {
@@ -1291,7 +1326,11 @@ __global__ void __launch_bounds__(512, 1) twoshot_pull_kernel(const __grid_const
                 const T xv = reinterpret_cast<const T*>(s_bufs[q])[lo + e];
                 acc = rnd_dtype<T>(h == 0 ? __fmul_rn(s_w[q], Vec<T>::to_f(xv)) : __fmaf_rn(s_w[q], Vec<T>::to_f(xv), acc));
             }
-            for (int q = 0; q < P; ++q) reinterpret_cast<T*>(s_bufs[q])[lo + e] = Vec<T>::from_f(acc);
+            if (FUSE) {
+                const float tv = Vec<T>::to_f(reinterpret_cast<const T*>(thp)[e]);
+                acc = __fmaf_rn(A.nlr, __fmaf_rn(A.wd, tv, acc), tv);
+            }
+            for (int q = 0; q < P; ++q) reinterpret_cast<T*>(s_dst[q])[e] = Vec<T>::from_f(acc);
         }
     }
     __syncthreads();
@@ -1305,6 +1344,18 @@ __global__ void __launch_bounds__(512, 1) twoshot_pull_kernel(const __grid_const
             latch(tab, PR_ERR_PEER_TIMEOUT);
         }
     __syncthreads();
+    if (FUSE && A.zero && !s_abort) {
+        // every peer has read its slices of this rank's gradient: reset this channel's share of every chunk
+        T* g = reinterpret_cast<T*>(rc.buf);
+        for (int c = 0; c < P; ++c) {
+            const int64_t a0 = (int64_t)c * cs + (int64_t)ch * sub;
+            const int64_t a1 = min((int64_t)c * cs + min((int64_t)(ch + 1) * sub, cs), count);
+            const int64_t zl = a1 > a0 ? a1 - a0 : 0;
+            const int64_t zv = zl / V;
+            for (int64_t v = threadIdx.x; v < zv; v += blockDim.x) st_v4(g + a0 + v * V, make_uint4(0, 0, 0, 0));
+            for (int64_t e = zv * V + threadIdx.x; e < zl; e += blockDim.x) g[a0 + e] = Vec<T>::from_f(0.0f);
+        }
+    }
     if (t0) {
         if (!s_abort) st->ts_base = base + 1;   // the push two-shot's counters stay consistent (targets are >=)
         if (ch == 0) tab->stamps[2] = (long long)gtimer();
@@ -2014,8 +2065,9 @@ int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_conf
     const bool f32 = a.dtype == PR_DTYPE_F32;
     bool registered = true;
     for (int r = 0; r < nranks; ++r) registered = registered && a.calls[r].reg_id >= 0;
-    // the fused update (K7 inside K3) exists in the TMA ring only (its callers check pick_algo)
-    const int algo = a.fuse ? PR_ALGO_RING : pick_algo(cfg, a.count, a.dtype, P, registered, in_nvls);
+    // the fused update (K7 inside K3) exists in the TMA ring and the pull two-shot (callers check fusable_algo)
+    int algo = pick_algo(cfg, a.count, a.dtype, P, registered, in_nvls);
+    if (a.fuse && algo != PR_ALGO_TWO_SHOT_PULL) algo = PR_ALGO_RING;
     a.algo = algo;
     switch (algo) {
         case PR_ALGO_NVLS:   // a local group (coop) runs the emulation: no multicast object on one device
@@ -2031,8 +2083,10 @@ int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_conf
             return launch_k3(f32 ? (void*)twoshot_kernel<float> : (void*)twoshot_kernel<__nv_bfloat16>, a, nranks,
                              channels, threads, 0, s, coop);
         case PR_ALGO_TWO_SHOT_PULL:
-            return launch_k3(f32 ? (void*)twoshot_pull_kernel<float> : (void*)twoshot_pull_kernel<__nv_bfloat16>, a,
-                             nranks, channels, threads, 0, s, coop);
+            return launch_k3(a.fuse ? (void*)twoshot_pull_kernel<float, true>
+                                    : f32 ? (void*)twoshot_pull_kernel<float, false>
+                                          : (void*)twoshot_pull_kernel<__nv_bfloat16, false>,
+                             a, nranks, channels, threads, 0, s, coop);
         default: break;
     }
     const bool bulk = (cfg.flags & PR_COMM_FLAG_BULK_STORE) != 0;
@@ -2527,7 +2581,8 @@ extern "C" int pr_weighted_allreduce_sgd(pr_comm* c, float* d_grad, float* d_the
     int32_t trid = -1;
     int64_t toff = 0;
     find_reg(c, d_theta, (size_t)count * 4, &trid, &toff);
-    const bool fusable = pick_algo(c->cfg, count, PR_DTYPE_F32, c->P, a.calls[0].reg_id >= 0) == PR_ALGO_RING &&
+    const int falgo = pick_algo(c->cfg, count, PR_DTYPE_F32, c->P, a.calls[0].reg_id >= 0);
+    const bool fusable = (falgo == PR_ALGO_RING || falgo == PR_ALGO_TWO_SHOT_PULL) &&
                          a.calls[0].reg_id >= 0 && trid == a.calls[0].reg_id && !(c->cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
     if (!fusable) {   // composed: the same bits (the ring's ḡ, then K7's two FMAs)
         if (int rc = pr_weighted_allreduce(c, d_grad, count, PR_DTYPE_F32, n_local, stream)) return rc;
@@ -2563,7 +2618,8 @@ extern "C" int pr_weighted_allreduce_sgd_local(pr_comm* const* comms, float* con
     }
     if (sumn <= 0) return PR_ERR_ZERO_SAMPLES;
     PR_CUDA_TRY(cudaSetDevice(c0->device));
-    const bool fusable = P > 1 && pick_algo(c0->cfg, count, PR_DTYPE_F32, P, true) == PR_ALGO_RING && same_delta &&
+    const int falgo = P > 1 ? pick_algo(c0->cfg, count, PR_DTYPE_F32, P, true) : PR_ALGO_RING;
+    const bool fusable = P > 1 && (falgo == PR_ALGO_RING || falgo == PR_ALGO_TWO_SHOT_PULL) && same_delta &&
                          !(c0->cfg.flags & PR_COMM_FLAG_FORCE_STAGED);
     if (!fusable) {
         if (P > 1) {

@@ -546,6 +546,75 @@ def test_fused_allreduce_sgd_resnet18_size_against_oracle():
     assert np.all(np.abs(out.astype(np.float64) - ref) <= bound + 1e-45)
 
 
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 8])
+def test_fused_pull_two_shot_bit_identical_to_composed(P):
+    """Rows a6-a9 in the pull two-shot: the owner of chunk r applies K7 and stores θ' into every rank's θ;
+    same bits as ring + K7, gradients reset (zero_grad) or left untouched (zero_grad=False)."""
+    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL)
+    rng = np.random.Generator(np.random.PCG64(310 + P))
+    for L in (1, 7, 1000, 4099, 2 ** 20 + 3):
+        n = [int(x) * 16 for x in rng.integers(1, 9, P)]
+        if L % 2:
+            n[int(rng.integers(0, P))] = 0
+        _fused_case(P, L, n, comms, seed=L + 3)
+    L = 5003
+    g = synth.gradients(P, L, seed_base=8)
+    theta0 = torch.from_numpy(synth.gradients(1, L, seed_base=9)[0]).cuda()
+    store = [torch.zeros(2 * 5004, device="cuda") for _ in range(P)]
+    grads, thetas = [x[:L] for x in store], [x[5004:5004 + L] for x in store]
+    for r in range(P):
+        grads[r].copy_(torch.from_numpy(g[r]))
+        thetas[r].copy_(theta0)
+    n = [1 + r for r in range(P)]
+    pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 0.05, 1e-3, zero_grad=False)
+    ref_g = [torch.from_numpy(g[r].copy()).cuda() for r in range(P)]
+    pr.weighted_allreduce_local(group(P), ref_g, n)                    # the ring's ḡ
+    ref = theta0.clone()
+    pr.sgd_update(ref, ref_g[0], 0.05, 1e-3, zero_grad=False)
+    torch.cuda.synchronize()
+    for r in range(P):
+        assert torch.equal(thetas[r], ref)
+        assert np.array_equal(grads[r].cpu().numpy(), g[r])              # zero_grad=False: untouched
+
+
+def test_fused_pull_two_shot_resnet18_size_and_graph_replay():
+    from oracle import linmodel as LM
+
+    P, L = 8, 11_689_512
+    n = [64, 64, 64, 64, 128, 128, 256, 256]
+    g, theta0, out = _fused_case(P, L, n, group(P, algo=pr.ALGO_TWO_SHOT_PULL), seed=78)
+    gbar = W.ring_emulate(g, n, "f32").astype(np.float64)
+    ref = LM.sgd_step(theta0.astype(np.float64), gbar, float(np.float32(1e-2)), float(np.float32(1e-4)))
+    bound = 2.0 ** -24 * (np.abs(ref) + np.float32(1e-2) * np.abs(gbar + np.float32(1e-4) * theta0)) * 1.01
+    assert np.all(np.abs(out.astype(np.float64) - ref) <= bound + 1e-45)
+    P, L = 3, 40_000
+    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL)
+    store = [torch.zeros(2 * L, device="cuda") for _ in range(P)]
+    grads, thetas = [s_[:L] for s_ in store], [s_[L:] for s_ in store]
+    g = synth.gradients(P, L, seed_base=43)
+    theta0 = torch.from_numpy(synth.gradients(1, L, seed_base=44)[0]).cuda()
+    n = [3, 1, 2]
+    s = torch.cuda.Stream()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 0.1, 0.0, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(gr, stream=s):
+            pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 0.1, 0.0, stream=s)
+    rg = [torch.from_numpy(g[r].copy()).cuda() for r in range(P)]
+    pr.weighted_allreduce_local(comms, rg, n)
+    ref = theta0.clone()
+    pr.sgd_update(ref, rg[0].clone(), 0.1, 0.0)
+    for _ in range(3):
+        for r in range(P):
+            grads[r].copy_(torch.from_numpy(g[r]))
+            thetas[r].copy_(theta0)
+        gr.replay()
+        torch.cuda.synchronize()
+        assert all(torch.equal(t, ref) for t in thetas)
+        assert all(torch.count_nonzero(x) == 0 for x in grads)
+
+
 def test_fused_allreduce_sgd_small_slices_staged_and_layout_fallbacks():
     for cfg in (dict(channels=3, slots=4, slot_bytes=4096, tile_bytes=1024, stages=3), dict(force_staged=True),
                 dict(algo=pr.ALGO_AUTO)):
@@ -608,7 +677,7 @@ def test_randomized_configs_all_algorithms():
                 if sum(n) == 0:
                     n[0] = 1
                 _check(P, L, dtype, n, comms, kind="mixed" if L % 2 else "gaussian", seed=case * 7 + L)
-            if cfg["algo"] in (pr.ALGO_RING, pr.ALGO_AUTO):
+            if cfg["algo"] in (pr.ALGO_RING, pr.ALGO_AUTO, pr.ALGO_TWO_SHOT_PULL):
                 _fused_case(P, int(rng.choice([7, 5000, 200_003])), [1 + (r % 3) for r in range(P)], comms,
                             seed=case + 900)
         finally:

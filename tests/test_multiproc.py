@@ -115,7 +115,7 @@ def _gpu_worker(rank, world, port, q):
             ok = ok and t == [1.5, 2.5]
             if not ok:
                 bad.append(f"algo={algo} sys={sys_scope} status={st}")
-            if algo == pr.ALGO_RING and not sys_scope:
+            if algo in (pr.ALGO_RING, pr.ALGO_TWO_SHOT_PULL) and not sys_scope:
                 # rows a6-a9 fused (K7 in K3) over IPC: one [grad | theta] region per rank
                 raw = comm.alloc(2 * 4100 * 4, dtype=torch.float32)
                 gr, th = raw[:L], raw[4100:4100 + L]
