@@ -278,3 +278,17 @@ def test_affine_model_trajectories_bit_exact():
             if ep == 4:                                               # checkpoint / restore mid-trajectory
                 l = pr.Alloc.load(l.save())
                 assert l.view() == v
+
+
+def test_binding_constants_match_the_header():
+    """Every PR_ALGO_* / PR_COMM_FLAG_* / PR_ERR_* / PR_DTYPE_* #define in include/propring.h has the same value
+    in the Python binding (the binding only marshals: a drifted constant would select another kernel)."""
+    txt = open(os.path.join(ROOT, "include", "propring.h")).read()
+    defs = dict(re.findall(r"#define\s+(PR_(?:ALGO|COMM_FLAG|ERR|DTYPE)_[A-Z0-9_]+)\s+(-?\d+)", txt))
+    assert len(defs) >= 15
+    for name, val in defs.items():
+        py = name[3:]                       # PR_ALGO_RING -> ALGO_RING
+        alt = name                          # some error codes keep the PR_ prefix in the binding
+        got = getattr(pr, py, getattr(pr, alt, None))
+        assert got is not None, f"binding lacks {name}"
+        assert int(got) == int(val), (name, got, val)

@@ -150,6 +150,16 @@ if __name__ == "__main__":
         gather(16384, 150528, 16384, reps, 50176, impls=(1,), layout=1)
     if what == "pull":                                  # co-located ResNet-18 gradient, 8 ranks, default channels
         pull(reps)
+    if what == "pull_fused":                            # a6-a9 fused into the pull two-shot, P = 8 co-located
+        P, L = 8, 11_689_512
+        comms = pr.comm_init_local(P, 0, pr.comm_config(algo=pr.ALGO_TWO_SHOT_PULL))
+        store = [torch.randn(2 * L, device="cuda") for _ in range(P)]
+        grads, thetas = [x[:L] for x in store], [x[L:] for x in store]
+        n = [64, 64, 64, 64, 128, 128, 256, 256]
+        us = timed(lambda: pr.weighted_allreduce_sgd_local(comms, grads, thetas, n, 1e-6, 0.0, zero_grad=True), reps)
+        print(f"fused pull two-shot a6-a9 P={P} L={L}: {us:.1f} us")
+        for c in comms:
+            c.destroy()
     if what == "pull_cta":                              # per-channel regime: P = 2, 4 channels, 256 MiB
         pull(max(2, reps // 4), P=2, L=(256 << 20) // 4, channels=4)
     if what == "ring_cta":                              # the ring in the same per-channel regime
