@@ -160,7 +160,7 @@ def test_c1_through_worker_matches_oracle_elementwise(micro):
         assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b), s
 
 
-def _n1_worker(rank, world, port, q):
+def _n1_worker(rank, world, port, q, algo=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -169,7 +169,7 @@ def _n1_worker(rank, world, port, q):
         from paper_2111_08272_b200.trainer import RunConfig, Worker
 
         torch.cuda.set_device(0)
-        comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=4, watchdog_ns=60_000_000_000))
+        comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=4, watchdog_ns=60_000_000_000, algo=algo))
         cfg = RunConfig(N=4096, shape=(1024,), classes=10, model="mlp", num_classes=10, ratios=[1, 3], C=4, g=64,
                         lr=0.05, wd=1e-4, micro=96, bf16_compute=False, channels_last=False, fused_sgd=False,
                         overlap=True, bucket_mb=0.004)
@@ -205,10 +205,14 @@ def _n1_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_n1_overlapped_buckets_match_oracle_elementwise():
+@pytest.mark.parametrize("algo", ["ring", "pull"])
+def test_n1_overlapped_buckets_match_oracle_elementwise(algo):
+    """N1's buckets through the ring and through the pull two-shot (AUTO's two-shot slot): every bucket the
+    oracle's ring replay of its range."""
     from oracle import wavg as OW
 
-    res = _spawn(_n1_worker)
+    import paper_2111_08272_b200 as pr
+    res = _spawn(_n1_worker, algo={"ring": pr.ALGO_RING, "pull": pr.ALGO_TWO_SHOT_PULL}[algo])
     r0, r1 = res[0], res[1]
     assert r0["status"] == 0 and r1["status"] == 0
     assert len(r0["buckets"]) >= 3, r0["buckets"]                     # the model is cut into several buckets
@@ -224,6 +228,59 @@ def test_n1_overlapped_buckets_match_oracle_elementwise():
             for lo, hi in r0["buckets"]:
                 emu = OW.ring_emulate(np.ascontiguousarray(g[:, lo:hi]), n, "f32")
                 assert np.array_equal(r0["red"][s][lo:hi], emu), (s, lo, hi)
+
+
+def _n1_fused_worker(rank, world, port, q, algo=0):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2111_08272_b200 as pr
+        from paper_2111_08272_b200.trainer import RunConfig, Worker
+
+        torch.cuda.set_device(0)
+        torch.manual_seed(5)
+        comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=4, watchdog_ns=60_000_000_000, algo=algo))
+        cfg = RunConfig(N=4096, shape=(1024,), classes=10, model="mlp", num_classes=10, ratios=[1, 3], C=4, g=64,
+                        lr=0.05, wd=1e-4, micro=96, bf16_compute=False, channels_last=False, fused_sgd=True,
+                        overlap=True, bucket_mb=0.004)
+        w = Worker(cfg, rank, world, 0, comm)
+        v = w.alloc.view()
+        n_r = v["n"][rank]
+        w.prepare(n_r)
+        xe, ye, _, _ = w._data(0, n_r, v["S"], False)
+        theta0 = w.pflat.clone()
+        for s in range(4):
+            w.compute_graphed(xe[s * n_r:(s + 1) * n_r], ye[s * n_r:(s + 1) * n_r], n_r)
+            w.allreduce_and_update(n_r)                   # every bucket's update ran fused with its allreduce
+        torch.cuda.synchronize()
+        out = {"theta0": theta0.cpu().numpy(), "theta": w.pflat.cpu().numpy(), "status": comm.status(),
+               "grad_zero": bool(torch.count_nonzero(w.flat) == 0)}
+        del w
+        comm.destroy()
+        q.put((rank, out))
+    except Exception as e:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, repr(e) + traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_n1_fused_buckets_pull_equals_ring():
+    """N1 with the update fused per bucket (two processes over IPC): the pull two-shot's fused kernel and the
+    ring's fused kernel give the same θ bit for bit, identical on both ranks, gradients reset."""
+    import paper_2111_08272_b200 as pr
+
+    ring = _spawn(_n1_fused_worker, algo=pr.ALGO_RING)
+    pull = _spawn(_n1_fused_worker, algo=pr.ALGO_TWO_SHOT_PULL)
+    for res in (ring, pull):
+        assert res[0]["status"] == 0 and res[1]["status"] == 0
+        assert np.array_equal(res[0]["theta"], res[1]["theta"])
+        assert res[0]["grad_zero"] and res[1]["grad_zero"]
+    assert np.array_equal(ring[0]["theta0"], pull[0]["theta0"])        # same initial parameters
+    assert not np.array_equal(ring[0]["theta"], ring[0]["theta0"])     # the steps moved θ
+    assert np.array_equal(ring[0]["theta"], pull[0]["theta"])
 
 
 def _n3_async_worker(rank, world, port, q):
