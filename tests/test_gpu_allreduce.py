@@ -282,6 +282,40 @@ def test_length_mismatch_and_timeout_latch():
         c.destroy()
 
 
+def test_pull_two_shot_mismatch_unregistered_and_timeout_latch():
+    """Pull two-shot error paths, per-rank launches on separate streams: count mismatch -> LENGTH_MISMATCH on
+    every rank, buffers untouched; buffers that cannot be addressed directly (force_staged) -> INVALID on
+    every rank; a missing peer -> PEER_TIMEOUT.  (Ranks picking different kernels: tests/test_multiproc.py.)"""
+    P, L = 2, 1 << 18
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, watchdog_ns=1_000_000_000, algo=pr.ALGO_TWO_SHOT_PULL))
+    a, b = torch.randn(L, device="cuda"), torch.randn(L, device="cuda")
+    a0, b0 = a.clone(), b.clone()
+    torch.cuda.synchronize()
+    pr.weighted_allreduce(comms[0], a, 1, stream=s0, count=L)
+    pr.weighted_allreduce(comms[1], b, 1, stream=s1, count=L - 1)
+    torch.cuda.synchronize()
+    assert comms[0].status() == pr.PR_ERR_LENGTH_MISMATCH and comms[1].status() == pr.PR_ERR_LENGTH_MISMATCH
+    assert torch.equal(a, a0) and torch.equal(b, b0)
+    for c in comms:
+        c.destroy()
+    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, watchdog_ns=1_000_000_000, force_staged=True,
+                                                    algo=pr.ALGO_TWO_SHOT_PULL))
+    pr.weighted_allreduce(comms[0], a, 1, stream=s0)
+    pr.weighted_allreduce(comms[1], b, 1, stream=s1)
+    torch.cuda.synchronize()
+    assert comms[0].status() == pr.PR_ERR_INVALID and comms[1].status() == pr.PR_ERR_INVALID
+    assert torch.equal(a, a0) and torch.equal(b, b0)
+    for c in comms:
+        c.destroy()
+    comms = pr.comm_init_local(P, 0, pr.comm_config(channels=2, watchdog_ns=300_000_000, algo=pr.ALGO_TWO_SHOT_PULL))
+    pr.weighted_allreduce(comms[0], a, 1, stream=s0)
+    torch.cuda.synchronize()
+    assert comms[0].status() == pr.PR_ERR_PEER_TIMEOUT
+    for c in comms:
+        c.destroy()
+
+
 def test_timestamps_and_status():
     P = 3
     comms = group(P)

@@ -132,6 +132,23 @@ def _gpu_worker(rank, world, port, q):
                     bad.append(f"fused status={comm.status()}")
             dist.barrier()
             comm.destroy()
+        # AUTO at a two-shot size, rank 0 on its registered buffer (-> pull two-shot), rank 1 on an unregistered
+        # tensor (-> ring): the algorithm travels in the handshake, so both latch LENGTH_MISMATCH, no hang
+        comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=2, watchdog_ns=30_000_000_000,
+                                                                  algo=pr.ALGO_AUTO))
+        L = 1 << 18
+        reg = comm.alloc(L * 4, dtype=torch.float32)
+        buf = reg if rank == 0 else torch.zeros(L, device="cuda")
+        buf.fill_(1.0 + rank)
+        try:
+            pr.weighted_allreduce(comm, buf, 1)
+        except pr.PropringError:
+            pass
+        torch.cuda.synchronize()
+        if comm.status() != pr.PR_ERR_LENGTH_MISMATCH or not bool((buf == 1.0 + rank).all()):
+            bad.append(f"mixed kernels status={comm.status()}")
+        dist.barrier()
+        comm.destroy()
         # a registration that fails on any rank leaves nothing behind (the next one gets region 0
         # and the direct all-gather works); NVLS (N2) is set up or refused on every rank together
         comm = pr.comm_init(rank, world, 0, config=pr.comm_config(channels=2, watchdog_ns=30_000_000_000,
