@@ -119,6 +119,13 @@ def test_c5_maximum_size_1GiB():
     _check(4, 2 ** 27, "bf16", [256, 256, 512, 1024], group(4), kind="mixed", seed=31)
 
 
+def test_c5_maximum_size_1GiB_pull_two_shot():
+    """The same C5 maximum-size cases through the pull two-shot (and P = 8 at 64 MiB fp32)."""
+    _check(2, 2 ** 28, "f32", [256, 768], group(2, algo=pr.ALGO_TWO_SHOT_PULL), kind="mixed", seed=32)
+    _check(4, 2 ** 27, "bf16", [256, 256, 512, 1024], group(4, algo=pr.ALGO_TWO_SHOT_PULL), kind="mixed", seed=33)
+    _check(8, 2 ** 24, "f32", [64, 64, 64, 64, 128, 128, 256, 256], group(8, algo=pr.ALGO_TWO_SHOT_PULL), seed=34)
+
+
 def test_resnet18_size_bf16_P8():
     """C5's bf16 leg at the ResNet-18 size, skewed weights 1:1:1:1:2:2:4:4."""
     P = 8
