@@ -790,6 +790,21 @@ def test_cross_gpu_default_config_fused(P, model):
     assert np.all(np.abs(out[pos].astype(np.float64) - ref) <= bound + 1e-45)
 
 
+CROSS_PULL = dict(CROSS, algo=pr.ALGO_TWO_SHOT_PULL)
+CROSS_PULL8 = dict(CROSS_PULL, threads=256)      # 8 × 32 CTAs co-resident: two 256-thread CTAs per SM
+
+
+@pytest.mark.parametrize("model", ["resnet18", "vgg16"])
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_cross_gpu_default_config_pull(P, model):
+    """The pull two-shot under the cross-GPU configuration (32 channels, `.sys` scope): the ring replay on
+    every element, the fp64 mean on sampled positions; and its fused a6-a9 form = ring + K7 bit for bit."""
+    cfg = CROSS_PULL8 if P == 8 else CROSS_PULL
+    _check_sampled(P, SIZES[model], SKEW[-P:], group(P, **cfg), seed=P + len(model) + 50)
+    if model == "resnet18":
+        _fused_case(P, SIZES[model], SKEW[-P:], group(P, **cfg), seed=150 + P)
+
+
 def test_auto_with_unregistered_or_staged_buffers_skips_two_shot():
     """AUTO at a two-shot size (1-4 MiB) on a group whose buffers cannot take the direct
     all-gather (force_staged) must take the staged ring, not latch PR_ERR_INVALID in the two-shot."""
