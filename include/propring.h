@@ -284,8 +284,8 @@ typedef struct {
  * ring's rounding (same bits) and stores the result into every rank's buffer.  Stores per rank fall from
  * (2P−1)/P·Z to Z — the SM store path is what bounds a channel.  Needs every rank's buffer registered
  * (else PR_ERR_INVALID is latched on all ranks).  PR_ALGO_AUTO takes it instead of the push two-shot
- * (registered buffers up to ts_max_bytes); above that AUTO keeps the ring (the paper's algorithm, and the
- * only one with the fused update), since the pull's peer loads are unmeasured over NVLink. */
+ * (registered buffers up to ts_max_bytes); above that AUTO keeps the ring (the paper's algorithm), since the
+ * pull's peer loads are unmeasured over NVLink.  pr_weighted_allreduce_sgd fuses the update into it too. */
 #define PR_ALGO_TWO_SHOT_PULL 6
 
 /* Byte allgather supplied by the caller (e.g. over a torch process group): every rank passes `len`
