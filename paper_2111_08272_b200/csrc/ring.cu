@@ -1314,9 +1314,11 @@ __global__ void __launch_bounds__(512, 1) twoshot_pull_kernel(const __grid_const
                                     reinterpret_cast<const uint8_t*>(rc.buf) + rc.th_delta) + lo)
                               : nullptr;
     if (len > 0) {
+        // U = 16/P: 16 loads (256 B) in flight per thread at every P — 128 KiB per channel, for the latency of
+        // peer reads (U = 8/P measured 0-11 % slower per channel co-located, profiles/round2_k3_pull_deep_ab.jsonl)
         if (P == 8) ts_pull_reduce<T, 8, 2, FUSE>(nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
-        else if (P == 4) ts_pull_reduce<T, 4, 2, FUSE>(nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
-        else if (P == 2) ts_pull_reduce<T, 2, 4, FUSE>(nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
+        else if (P == 4) ts_pull_reduce<T, 4, 4, FUSE>(nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
+        else if (P == 2) ts_pull_reduce<T, 2, 8, FUSE>(nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
         else ts_pull_reduce_any<T, FUSE>(P, nv, s_src, s_wt, s_act, s_dst, thp, A.nlr, A.wd);
         for (int64_t e = nv * V + threadIdx.x; e < len; e += blockDim.x) {   // ragged tail: end of buffer
             float acc = 0.0f;
