@@ -225,6 +225,9 @@ typedef struct pr_comm pr_comm;
                                          * whole tiles) instead of 16-byte stores from every consumer lane */
 #define PR_COMM_FLAG_L2_PREFETCH  8   /* ring data path: each slice's own-gradient range is prefetched into
                                          * L2 (cp.async.bulk.prefetch.L2) before the slice's flag waits */
+#define PR_COMM_FLAG_PULL_TMA    16   /* pull two-shot: the P source tiles staged in shared memory by TMA bulk
+                                        loads (4 stages, up to 192 KiB in flight per channel) instead of
+                                        register-queued loads — for peer reads over NVLink; same bits */
 #define PR_COMM_FLAG_SYS_SCOPE    2   /* system-scope release/acquire even when every rank shares one GPU
                                          (by default .gpu scope is used exactly when that is the case) */
 

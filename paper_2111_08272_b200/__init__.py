@@ -258,6 +258,7 @@ COMM_FLAG_FORCE_STAGED = 1
 COMM_FLAG_SYS_SCOPE = 2
 COMM_FLAG_BULK_STORE = 4
 COMM_FLAG_L2_PREFETCH = 8
+COMM_FLAG_PULL_TMA = 16
 ALGO_RING = 0
 ALGO_TWO_SHOT = 1
 ALGO_AUTO = 2
@@ -270,7 +271,7 @@ ALGO_TWO_SHOT_PULL = 6
 def comm_config(channels=0, slots=8, threads=512, slot_bytes=0, watchdog_ns=10_000_000_000,
                 force_staged=False, stages=0, tile_bytes=0, sys_scope=False, algo=ALGO_RING, ts_slots=2,
                 ts_slot_bytes=256 * 1024, ts_max_bytes=4 << 20, ll_max_bytes=256 * 1024,
-                os_max_bytes=64 * 1024, min_slice_bytes=0, bulk_store=False, l2_prefetch=False):
+                os_max_bytes=64 * 1024, min_slice_bytes=0, bulk_store=False, l2_prefetch=False, pull_tma=False):
     """K3 launch/pipeline configuration.  channels / slot_bytes / stages / tile_bytes = 0: chosen at init from
     the topology (one GPU: 128/P channels (16 at P = 8, at most 64) / 256 KiB / 7 / 16 KiB, the co-located
     optimum of tools/sweep_ring.py; ranks on different GPUs: 32 / 1 MiB / 7 / 16 KiB, from the per-channel
@@ -282,7 +283,8 @@ def comm_config(channels=0, slots=8, threads=512, slot_bytes=0, watchdog_ns=10_0
     os_max_bytes, LL up to ll_max_bytes, the pull two-shot for registered buffers up to ts_max_bytes, ring
     above)."""
     flags = ((COMM_FLAG_FORCE_STAGED if force_staged else 0) | (COMM_FLAG_SYS_SCOPE if sys_scope else 0)
-             | (COMM_FLAG_BULK_STORE if bulk_store else 0) | (COMM_FLAG_L2_PREFETCH if l2_prefetch else 0))
+             | (COMM_FLAG_BULK_STORE if bulk_store else 0) | (COMM_FLAG_L2_PREFETCH if l2_prefetch else 0)
+             | (COMM_FLAG_PULL_TMA if pull_tma else 0))
     return CommConfig(channels=channels, slots=slots, threads=threads, flags=flags, slot_bytes=slot_bytes,
                       watchdog_ns=watchdog_ns, stages=stages, tile_bytes=tile_bytes, algo=algo, ts_slots=ts_slots,
                       ts_slot_bytes=ts_slot_bytes, ts_max_bytes=ts_max_bytes, ll_max_bytes=ll_max_bytes,

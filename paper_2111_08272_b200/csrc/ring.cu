@@ -1364,6 +1364,180 @@ __global__ void __launch_bounds__(512, 1) twoshot_pull_kernel(const __grid_const
     }
 }
 
+// TMA-staged pull (PR_COMM_FLAG_PULL_TMA, opt-in): the same reduction, order, rounding and flags as
+// twoshot_pull_kernel, but the P source tiles are brought into shared memory by one producer thread with
+// cp.async.bulk (kPullStages deep, up to 192 KiB in flight per channel instead of 128 KiB in registers)
+// and the consumer warps reduce from shared memory.  For peer reads over NVLink, whose round trip the
+// register-queued loads expose; co-located the two are compared in profiles/round2_k3_pull_tma_ab.jsonl.
+constexpr int kPullStages = 4;
+__host__ __device__ constexpr int pull_tile_bytes(int P) {
+    return ((196608 / (kPullStages * P)) & ~15) < 32768 ? ((196608 / (kPullStages * P)) & ~15) : 32768;
+}
+
+template <typename T, bool FUSE>
+__global__ void __launch_bounds__(544, 1) twoshot_pull_tma_kernel(const __grid_constant__ LaunchArgs A) {
+    extern __shared__ __align__(128) uint8_t smem[];   // [kPullStages][P][tile]
+    __shared__ uint64_t full[kPullStages], empty[kPullStages];
+    __shared__ int s_err;
+    __shared__ long long s_n[PR_MAX_RANKS];
+    __shared__ uint8_t* s_bufs[PR_MAX_RANKS];
+    __shared__ float s_w[PR_MAX_RANKS];
+    __shared__ const uint8_t* s_src[PR_MAX_RANKS];
+    __shared__ uint8_t* s_dst[PR_MAX_RANKS];
+    __shared__ float s_wt[PR_MAX_RANKS];
+    __shared__ int s_act[PR_MAX_RANKS];
+    __shared__ int s_abort;
+    const RankCall& rc = A.calls[blockIdx.y];
+    const DevTable* tab = rc.tab;
+    const int ch = blockIdx.x;
+    const int r = tab->rank, P = tab->P;
+    uint8_t* my = tab->win[r];
+    ChanState* st = state_of(my, tab, ch);
+    TsFlags* mf = ts_flags_of(my, tab, ch);
+    const bool t0 = threadIdx.x == 0;
+    const bool sys = tab->sysscope != 0;
+    const int nc = blockDim.x - 32;                   // consumer threads (warps 1..); warp 0: producer
+    unsigned long long deadline = ~0ull;
+    if (threadIdx.x < 32) {
+        const unsigned long long start = gtimer();
+        if (tab->watchdog_ns > 0) deadline = start + (unsigned long long)tab->watchdog_ns;
+        if (t0) {
+            if (ch == 0) tab->stamps[0] = (long long)start;
+            for (int k = 0; k < kPullStages; ++k) {
+                mbar_init(&full[k], 1);
+                mbar_init(&empty[k], (uint32_t)(nc / 32));
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        const HsOut hs = handshake(A, rc, tab, st, ch, sys, deadline, s_n, s_bufs);
+        __syncwarp();
+        for (int q = (int)threadIdx.x; q < P; q += 32)
+            s_w[q] = hs.sumn > 0 ? (float)((double)s_n[q] / (double)hs.sumn) : 0.0f;
+        if (t0) {
+            s_err = hs.err ? hs.err : (hs.direct ? 0 : PR_ERR_INVALID);
+            if (FUSE && A.fuse == 0) s_err = PR_ERR_INVALID;
+            s_abort = 0;
+            if (ch == 0) tab->stamps[1] = (long long)gtimer();
+        }
+    }
+    __syncthreads();
+    if (s_err) {
+        if (t0) latch(tab, s_err);
+        return;
+    }
+    constexpr int V = Vec<T>::V;
+    const int64_t count = A.count;
+    const int64_t per = (count + P - 1) / P;
+    const int64_t cs = (per + V - 1) / V * V;
+    const int64_t subp = (cs + tab->channels - 1) / tab->channels;
+    const int64_t sub = (subp + V - 1) / V * V;
+    const unsigned long long base = st->ts_base;
+    const int64_t clo = (int64_t)r * cs;
+    const int64_t lo = clo + (int64_t)ch * sub;
+    const int64_t hi = min(clo + min((int64_t)(ch + 1) * sub, cs), count);
+    const int64_t len = hi > lo ? hi - lo : 0;
+    const int64_t nv = len / V;
+    for (int h = (int)threadIdx.x; h < P; h += (int)blockDim.x) {
+        const int q = (r + h) % P;
+        s_src[h] = reinterpret_cast<const uint8_t*>(reinterpret_cast<const T*>(s_bufs[q]) + lo);
+        s_wt[h] = s_w[q];
+        s_act[h] = s_n[q] > 0 ? 1 : 0;
+        s_dst[h] = reinterpret_cast<uint8_t*>(reinterpret_cast<T*>(s_bufs[h] + (FUSE ? rc.th_delta : 0)) + lo);
+    }
+    __syncthreads();
+    const uint8_t* thp = FUSE ? reinterpret_cast<const uint8_t*>(reinterpret_cast<const T*>(
+                                    reinterpret_cast<const uint8_t*>(rc.buf) + rc.th_delta) + lo)
+                              : nullptr;
+    const int tb = pull_tile_bytes(P);
+    const int64_t vbytes = nv * 16;
+    const int64_t ntiles = (vbytes + tb - 1) / tb;
+    if (threadIdx.x < 32) {
+        if (t0) {                                     // producer: P bulk loads per tile into one stage
+            fence_proxy_async_global();               // peers' gradients (acquired in the handshake) -> TMA
+            uint32_t nact = 0;
+            for (int h = 0; h < P; ++h) nact += (uint32_t)s_act[h];
+            for (int64_t t = 0; t < ntiles; ++t) {
+                const int stg = (int)(t % kPullStages);
+                if (t >= kPullStages) mbar_wait(&empty[stg], (uint32_t)(((t / kPullStages) - 1) & 1));
+                const uint32_t bytes = (uint32_t)min((int64_t)tb, vbytes - t * tb);
+                mbar_arrive_expect_tx(&full[stg], bytes * nact);
+                for (int h = 0; h < P; ++h)
+                    if (s_act[h])
+                        tma_load(smem + ((size_t)stg * P + h) * tb, s_src[h] + t * tb, bytes, &full[stg]);
+            }
+        }
+    } else {
+        const int cid = threadIdx.x - 32;
+        const int lane = threadIdx.x & 31;
+        for (int64_t t = 0; t < ntiles; ++t) {
+            const int stg = (int)(t % kPullStages);
+            mbar_wait(&full[stg], (uint32_t)((t / kPullStages) & 1));
+            const int64_t bytes = min((int64_t)tb, vbytes - t * tb);
+            const int nvt = (int)(bytes / 16);
+            const uint8_t* tile = smem + (size_t)stg * P * tb;
+            for (int v = cid; v < nvt; v += nc) {
+                float acc[V];
+#pragma unroll
+                for (int j = 0; j < V; ++j) acc[j] = 0.0f;
+                for (int h = 0; h < P; ++h) {
+                    if (!s_act[h]) continue;
+                    const uint4 x = *reinterpret_cast<const uint4*>(tile + (size_t)h * tb + (size_t)v * 16);
+                    const float sq = s_wt[h];
+#pragma unroll
+                    for (int j = 0; j < V; ++j)
+                        acc[j] = rnd_dtype<T>(h == 0 ? __fmul_rn(sq, lane_f<T>(x, j)) : __fmaf_rn(sq, lane_f<T>(x, j), acc[j]));
+                }
+                uint4 y = pack_f<T>(acc);
+                const size_t off = (size_t)t * tb + (size_t)v * 16;
+                if (FUSE) y = sgd_v4<T>(*reinterpret_cast<const uint4*>(thp + off), y, A.nlr, A.wd);
+                for (int q = 0; q < P; ++q) st_v4(s_dst[q] + off, y);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stg]);   // this warp's smem reads of the stage are done
+        }
+        for (int64_t e = nv * V + cid; e < len; e += nc) {   // ragged tail: end of buffer
+            float acc = 0.0f;
+            for (int h = 0; h < P; ++h) {
+                const int q = (r + h) % P;
+                if (s_n[q] <= 0) continue;
+                const T xv = reinterpret_cast<const T*>(s_bufs[q])[lo + e];
+                acc = rnd_dtype<T>(h == 0 ? __fmul_rn(s_w[q], Vec<T>::to_f(xv)) : __fmaf_rn(s_w[q], Vec<T>::to_f(xv), acc));
+            }
+            if (FUSE) {
+                const float tv = Vec<T>::to_f(reinterpret_cast<const T*>(thp)[e]);
+                acc = __fmaf_rn(A.nlr, __fmaf_rn(A.wd, tv, acc), tv);
+            }
+            for (int q = 0; q < P; ++q) reinterpret_cast<T*>(s_dst[q])[e] = Vec<T>::from_f(acc);
+        }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < P - 1) {
+        const int q = (r + 1 + (int)threadIdx.x) % P;
+        st_release(&ts_flags_of(tab->win[q], tab, ch)->ag[r], base + 1, sys);
+    }
+    if (threadIdx.x < 32)
+        if (!warp_wait_peers(mf->ag, base + 1, r, P, deadline, sys) && t0) {
+            s_abort = 1;
+            latch(tab, PR_ERR_PEER_TIMEOUT);
+        }
+    __syncthreads();
+    if (FUSE && A.zero && !s_abort) {
+        T* g = reinterpret_cast<T*>(rc.buf);
+        for (int c = 0; c < P; ++c) {
+            const int64_t a0 = (int64_t)c * cs + (int64_t)ch * sub;
+            const int64_t a1 = min((int64_t)c * cs + min((int64_t)(ch + 1) * sub, cs), count);
+            const int64_t zl = a1 > a0 ? a1 - a0 : 0;
+            const int64_t zv = zl / V;
+            for (int64_t v = threadIdx.x; v < zv; v += blockDim.x) st_v4(g + a0 + v * V, make_uint4(0, 0, 0, 0));
+            for (int64_t e = zv * V + threadIdx.x; e < zl; e += blockDim.x) g[a0 + e] = Vec<T>::from_f(0.0f);
+        }
+    }
+    if (t0) {
+        if (!s_abort) st->ts_base = base + 1;
+        if (ch == 0) tab->stamps[2] = (long long)gtimer();
+    }
+}
+
 // =====================================================================================================
 // LL ring (low-latency protocol for small buffers): the SAME ring schedule, order and per-hop rounding as
 // ring_kernel — so the result is bit-identical — but every 16-byte line a rank pushes carries its own
@@ -1906,7 +2080,7 @@ void resolve_config(pr_comm_config& c, bool cross_gpu, int P) {
 
 int check_config(const pr_comm_config& c) {
     if ((c.flags & ~(PR_COMM_FLAG_FORCE_STAGED | PR_COMM_FLAG_SYS_SCOPE | PR_COMM_FLAG_BULK_STORE |
-                     PR_COMM_FLAG_L2_PREFETCH)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
+                     PR_COMM_FLAG_L2_PREFETCH | PR_COMM_FLAG_PULL_TMA)) || c.channels < 1 || c.channels > 128 || c.slots < 2 || c.slots > 64 || c.threads < 32 || c.threads > 512 ||
         c.threads % 32 || c.slot_bytes < 256 || c.slot_bytes % 256 || c.slot_bytes > (64ll << 20) ||
         c.stages < 2 || c.stages > kMaxStages || c.tile_bytes < 256 || c.tile_bytes % 16 || c.tile_bytes > 32768 ||
         (int64_t)c.stages * 2 * c.tile_bytes > 224 * 1024 || c.algo < PR_ALGO_RING || c.algo > PR_ALGO_TWO_SHOT_PULL ||
@@ -2085,6 +2259,24 @@ int launch_ring(LaunchArgs& a, int nranks, int P, int device, const pr_comm_conf
             return launch_k3(f32 ? (void*)twoshot_kernel<float> : (void*)twoshot_kernel<__nv_bfloat16>, a, nranks,
                              channels, threads, 0, s, coop);
         case PR_ALGO_TWO_SHOT_PULL:
+            if (cfg.flags & PR_COMM_FLAG_PULL_TMA) {
+                void* fn = a.fuse ? (void*)twoshot_pull_tma_kernel<float, true>
+                                  : f32 ? (void*)twoshot_pull_tma_kernel<float, false>
+                                        : (void*)twoshot_pull_tma_kernel<__nv_bfloat16, false>;
+                const size_t smem = (size_t)kPullStages * P * pull_tile_bytes(P);
+                static std::mutex mu;
+                static bool attr_set[PR_MAX_DEVICES][3];
+                const int di = a.fuse ? 2 : (f32 ? 0 : 1);
+                if (device < 0 || device >= PR_MAX_DEVICES) return PR_ERR_INVALID;
+                {
+                    std::lock_guard<std::mutex> lk(mu);
+                    if (!attr_set[device][di]) {
+                        PR_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 196608));
+                        attr_set[device][di] = true;
+                    }
+                }
+                return launch_k3(fn, a, nranks, channels, threads + 32, smem, s, coop);
+            }
             return launch_k3(a.fuse ? (void*)twoshot_pull_kernel<float, true>
                                     : f32 ? (void*)twoshot_pull_kernel<float, false>
                                           : (void*)twoshot_pull_kernel<__nv_bfloat16, false>,

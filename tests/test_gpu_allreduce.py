@@ -119,6 +119,37 @@ def test_c5_maximum_size_1GiB():
     _check(4, 2 ** 27, "bf16", [256, 256, 512, 1024], group(4), kind="mixed", seed=31)
 
 
+def test_pull_tma_channels_graph_replay_and_full_sizes():
+    """The TMA-staged pull: few and many channels, `.sys` scope, back-to-back calls, graph replay, the
+    ResNet-18 gradient at P = 8 and C3's VGG-16 gradient at P = 4 (ring replay on every element)."""
+    for cfg in (dict(channels=1), dict(channels=3, sys_scope=True, threads=128)):
+        for P in (2, 4, 7):
+            comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL, pull_tma=True, **cfg)
+            for it, L in enumerate((999, 300_001, 5)):
+                _check(P, L, "f32" if it % 2 == 0 else "bf16", [5] * (P - 1) + [it], comms, seed=L + 1)
+    P, L = 3, 40_000
+    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL, pull_tma=True)
+    host, dev = _inputs(P, L, "f32", seed=23)
+    src = [d.clone() for d in dev]
+    n = [3, 1, 2]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        pr.weighted_allreduce_local(comms, dev, n, stream=s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            pr.weighted_allreduce_local(comms, dev, n, stream=s)
+    emu = W.ring_emulate(host, n, "f32")
+    for _ in range(3):
+        for d, s0 in zip(dev, src):
+            d.copy_(s0)
+        g.replay()
+        torch.cuda.synchronize()
+        assert all(np.array_equal(d.cpu().numpy(), emu) for d in dev)
+    _check_sampled(8, SIZES["resnet18"], SKEW, group(8, algo=pr.ALGO_TWO_SHOT_PULL, pull_tma=True), seed=61)
+    _check_sampled(4, SIZES["vgg16"], SKEW[-4:], group(4, algo=pr.ALGO_TWO_SHOT_PULL, pull_tma=True), seed=62)
+
+
 def test_c5_maximum_size_1GiB_pull_two_shot():
     """The same C5 maximum-size cases through the pull two-shot (and P = 8 at 64 MiB fp32)."""
     _check(2, 2 ** 28, "f32", [256, 768], group(2, algo=pr.ALGO_TWO_SHOT_PULL), kind="mixed", seed=32)
@@ -357,12 +388,14 @@ def test_two_shot_small_slots_many_slices_and_sys_scope():
                 _check(P, L, "bf16", [2] * P, comms, seed=L)
 
 
+@pytest.mark.parametrize("tma", [False, True])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("P", [2, 3, 4, 5, 8])
-def test_pull_two_shot_bit_identical_to_ring_replay(P, dtype):
+def test_pull_two_shot_bit_identical_to_ring_replay(P, dtype, tma):
     """PR_ALGO_TWO_SHOT_PULL: chunk r read straight out of every rank's buffer, reduced in the ring's order
-    with the ring's rounding — the ring replay's bits, including n_r = 0 ranks and ragged tails."""
-    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL)
+    with the ring's rounding — the ring replay's bits, including n_r = 0 ranks and ragged tails; with
+    PR_COMM_FLAG_PULL_TMA the source tiles are staged in shared memory by TMA (same bits)."""
+    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL, pull_tma=tma)
     rng = np.random.Generator(np.random.PCG64(300 + P))
     for L in (1, 7, P + 1, 4099, 2 ** 20 + 3):
         n = [int(x) * 16 for x in rng.integers(1, 9, P)]
@@ -587,11 +620,12 @@ def test_fused_allreduce_sgd_resnet18_size_against_oracle():
     assert np.all(np.abs(out.astype(np.float64) - ref) <= bound + 1e-45)
 
 
+@pytest.mark.parametrize("tma", [False, True])
 @pytest.mark.parametrize("P", [2, 3, 4, 5, 8])
-def test_fused_pull_two_shot_bit_identical_to_composed(P):
+def test_fused_pull_two_shot_bit_identical_to_composed(P, tma):
     """Rows a6-a9 in the pull two-shot: the owner of chunk r applies K7 and stores θ' into every rank's θ;
     same bits as ring + K7, gradients reset (zero_grad) or left untouched (zero_grad=False)."""
-    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL)
+    comms = group(P, algo=pr.ALGO_TWO_SHOT_PULL, pull_tma=tma)
     rng = np.random.Generator(np.random.PCG64(310 + P))
     for L in (1, 7, 1000, 4099, 2 ** 20 + 3):
         n = [int(x) * 16 for x in rng.integers(1, 9, P)]

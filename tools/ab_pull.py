@@ -22,7 +22,8 @@ import torch  # noqa: E402
 
 import paper_2111_08272_b200 as pr  # noqa: E402
 
-ALGOS = {"ring": pr.ALGO_RING, "twoshot_push": pr.ALGO_TWO_SHOT, "twoshot_pull": pr.ALGO_TWO_SHOT_PULL}
+ALGOS = {"ring": pr.ALGO_RING, "twoshot_push": pr.ALGO_TWO_SHOT, "twoshot_pull": pr.ALGO_TWO_SHOT_PULL,
+         "twoshot_pull_tma": pr.ALGO_TWO_SHOT_PULL}
 
 
 def time_case(P, L, channels, algo, sys_scope=False, check=None):
@@ -31,7 +32,7 @@ def time_case(P, L, channels, algo, sys_scope=False, check=None):
     bufs = [s.clone() for s in src]
     n = [1 + r for r in range(P)]
     comms = pr.comm_init_local(P, 0, pr.comm_config(channels=channels, algo=ALGOS[algo], sys_scope=sys_scope,
-                                                    watchdog_ns=20_000_000_000))
+                                                    watchdog_ns=20_000_000_000, pull_tma=algo.endswith("_tma")))
     try:
         pr.weighted_allreduce_local(comms, bufs, n)
         torch.cuda.synchronize()

@@ -103,6 +103,7 @@ def run_multi(max_mib, reps, algo=0, channels=0, min_slice=0, bulk=False, l2pf=F
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, P = dist.get_rank(), dist.get_world_size()
     comm = pr.comm_init(rank, P, local, config=pr.comm_config(algo=algo, channels=channels, min_slice_bytes=min_slice,
+                                                              pull_tma=os.environ.get("PR_AR_SWEEP_PULL_TMA") == "1",
                                                               bulk_store=bulk, l2_prefetch=l2pf))
     n = weights(P)
     s = n[rank] / sum(n)

@@ -26,6 +26,9 @@ for P in 2 4 8; do
   # pull two-shot (peer loads instead of pushes; co-located proxy: 1.6-2.3x the ring per channel)
   timeout 900 $TR --nproc-per-node $P --master-port $((29710 + P)) tools/ar_sweep.py --max-mib 1024 --algo 6 \
       > gpurun_out/mg_ar_sweep_pull_p$P.jsonl 2> gpurun_out/mg_ar_sweep_pull_p$P.err
+  # the same with its source tiles TMA-staged in shared memory (deeper queue for remote reads)
+  PR_AR_SWEEP_PULL_TMA=1 timeout 900 $TR --nproc-per-node $P --master-port $((29730 + P)) tools/ar_sweep.py --max-mib 1024 --algo 6 \
+      > gpurun_out/mg_ar_sweep_pull_tma_p$P.jsonl 2> gpurun_out/mg_ar_sweep_pull_tma_p$P.err
   # NVLS (in-switch reduction), where the box can create a multicast object
   timeout 900 $TR --nproc-per-node $P --master-port $((29680 + P)) tools/ar_sweep.py --max-mib 1024 --algo 5 \
       > gpurun_out/mg_ar_sweep_nvls_p$P.jsonl 2> gpurun_out/mg_ar_sweep_nvls_p$P.err
