@@ -691,7 +691,10 @@ def colocated_pull(hbm, n8, n3, reps):
                 "busbw_equiv_per_rank_GBs": Z * 2 * (P - 1) / P / (us * 1e-6) / 1e9}
 
     out = {"kernel": "twoshot_pull_kernel<float> (K3 variant, N2), all ranks on one GPU",
-           "resnet18_P8": one(8, L_RESNET18, n8, reps), "vgg16_C3_P4": one(4, L_VGG16, n3, 5)}
+           "resnet18_P8": one(8, L_RESNET18, n8, reps), "vgg16_C3_P4": one(4, L_VGG16, n3, 5),
+           # the TMA-staged data path (PR_COMM_FLAG_PULL_TMA, opt-in): same bits, deeper load queue
+           "tma": {"kernel": "twoshot_pull_tma_kernel<float>", "resnet18_P8": one(8, L_RESNET18, n8, reps, pull_tma=True),
+                   "vgg16_C3_P4": one(4, L_VGG16, n3, 5, pull_tma=True)}}
     # rows a6-a9 fused into the pull two-shot (K7 applied by the chunk owner, gradient reset), as the ring's
     # fused_a6_a9_us beside it
     P, L = 8, L_RESNET18

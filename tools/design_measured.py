@@ -22,6 +22,7 @@ def blocks(d):
 | K3 co-located (8 ranks, ResNet-18 gradient) | {ac['avg_us']:.0f} µs; fused a6-a9 {ac['fused_a6_a9_us']:.0f} µs vs composed {ac['composed_a6_a9_us']:.0f} µs | HBM proxy {ac['frac']:.2f} of the copy peak (algorithmic) |
 | K3 cross-GPU config, per-rank CTA proxy (2 ranks, 32 ch) | {ac['cross_gpu_config_per_rank_busbw_equiv']['GBs']:.0f} GB/s bus-equivalent | not NVLink |
 | K3 pull two-shot (N2), same co-located cases | ResNet-18 P = 8 {ac['pull_two_shot']['resnet18_P8']['avg_us']:.0f} µs (fused a6-a9 {ac['pull_two_shot'].get('fused_a6_a9_resnet18_P8_us', float('nan')):.0f} µs); VGG-16 P = 4 {ac['pull_two_shot']['vgg16_C3_P4']['avg_us']:.0f} µs (ring {ac['vgg16_C3_P4']['avg_us']:.0f}); cross-GPU proxy {ac['pull_two_shot']['cross_gpu_config_per_rank']['busbw_equiv_per_rank_GBs']:.0f} GB/s | HBM {ac['pull_two_shot']['resnet18_P8']['frac']:.2f} / {ac['pull_two_shot']['vgg16_C3_P4']['frac']:.2f} of the copy peak (2·Z per rank algorithmic) |
+| K3 pull two-shot, TMA-staged (opt-in) | ResNet-18 P = 8 {ac['pull_two_shot']['tma']['resnet18_P8']['avg_us']:.0f} µs; VGG-16 P = 4 {ac['pull_two_shot']['tma']['vgg16_C3_P4']['avg_us']:.0f} µs | HBM {ac['pull_two_shot']['tma']['resnet18_P8']['frac']:.2f} / {ac['pull_two_shot']['tma']['vgg16_C3_P4']['frac']:.2f} |
 
 Library kernels are {100 * sum(d['kernel_shares'].values()):.1f} % of the ResNet-18 epoch at N = 1 (the rest is cuDNN forward/backward; at
 P = 1 the allreduce is an identity), {100 * sum(v['kernel_shares'].values()):.2f} % of the VGG-16 epoch.  `gpu_launches` {d['gpu_launches']}."""
