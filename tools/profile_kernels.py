@@ -160,6 +160,10 @@ if __name__ == "__main__":
         print(f"fused pull two-shot a6-a9 P={P} L={L}: {us:.1f} us")
         for c in comms:
             c.destroy()
+    if what == "pull_vgg":                              # C3's VGG-16 gradient, P = 4, register-queued pull
+        pull(max(2, reps // 4), P=4, L=138_357_544)
+    if what == "pull_tma_vgg":                          # the same, TMA-staged (PR_COMM_FLAG_PULL_TMA)
+        pull(max(2, reps // 4), P=4, L=138_357_544, pull_tma=True)
     if what == "pull_cta":                              # per-channel regime: P = 2, 4 channels, 256 MiB
         pull(max(2, reps // 4), P=2, L=(256 << 20) // 4, channels=4)
     if what == "ring_cta":                              # the ring in the same per-channel regime
