@@ -743,6 +743,8 @@ def test_randomized_configs_all_algorithms():
                    threads=int(rng.choice([64, 128, 256, 512])), algo=int(rng.choice(algos)),
                    sys_scope=bool(rng.integers(0, 2)), ts_slot_bytes=int(rng.choice([256, 4096, 65536])),
                    ll_max_bytes=int(rng.choice([4096, 262144])), os_max_bytes=int(rng.choice([1024, 65536])))
+        if cfg["algo"] == pr.ALGO_TWO_SHOT_PULL:                 # both pull data paths (a separate stream of
+            cfg["pull_tma"] = bool(np.random.Generator(np.random.PCG64(case)).integers(0, 2))   # draws)
         comms = pr.comm_init_local(P, 0, pr.comm_config(watchdog_ns=5_000_000_000, **cfg))
         try:
             for _ in range(2):
